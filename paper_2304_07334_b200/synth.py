@@ -1,0 +1,221 @@
+"""Seeded synthetic stand-ins for the paper's datasets.
+
+The public datasets (Gowalla, Yelp2018, Amazon-Books) are not
+available offline.  BASELINE.json configs 2-4 carry their shapes; this module
+generates interaction sets with those user/item/interaction counts:
+
+- per-user degree d_u: geometric with mean 20 (config 1) or lognormal with
+  median 20 and a sigma fitted by bisection so that sum(d_u) hits the
+  interaction target exactly (configs 2-5), capped at num_items / 2;
+- each user's d_u items are drawn WITHOUT replacement from a bounded
+  Zipf(s) over popularity ranks (draw-until-distinct, first occurrences
+  kept), and ranks map to item ids through a seeded permutation so hot rows
+  are scattered across the table;
+- optionally 20 % of each user's items are held out as the test split
+  (int(d * f) items, at least one train item kept).
+
+Everything is a pure function of (config, gen_seed); DESIGN.md records the
+seed used by bench.py and the tests.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .dataset import InteractionSet, from_pairs
+
+GEN_SEED = 12345
+
+
+@dataclass(frozen=True)
+class WorkloadSpec:
+    name: str
+    num_users: int
+    num_items: int
+    interactions: int
+    zipf_s: float
+    degree_law: str          # "geometric" | "lognormal"
+    dim: int
+    negatives: int
+    theta: float
+    mu: float
+    batch: int
+    learning_rate: float = 1e-3
+    epochs: int = 1
+    test_fraction: float = 0.0
+    lognormal_median: float = 20.0
+    extra: dict = field(default_factory=dict)
+
+
+# BASELINE.json "configs" 1-5 (lr 1e-3 for all, SURVEY.md §8 size sheet).
+CONFIGS: dict[str, WorkloadSpec] = {
+    "c1": WorkloadSpec("c1", 1_000, 2_000, 20_000, 1.0, "geometric", 32, 10, 0.5, 10.0, 256),
+    "c2": WorkloadSpec("c2", 30_000, 41_000, 1_030_000, 0.9, "lognormal", 64, 100, 0.9, 150.0,
+                       1024, epochs=20, test_fraction=0.2),
+    "c3": WorkloadSpec("c3", 32_000, 38_000, 1_560_000, 0.8, "lognormal", 64, 500, 0.9, 150.0,
+                       1024),
+    "c4": WorkloadSpec("c4", 53_000, 92_000, 2_980_000, 1.1, "lognormal", 128, 1000, 0.8, 300.0,
+                       2048),
+    "c5": WorkloadSpec("c5", 10_000_000, 2_000_000, 500_000_000, 1.0, "lognormal", 128, 1000,
+                       0.8, 300.0, 8192),
+}
+
+
+def _fit_degrees(rng: np.random.Generator, spec: WorkloadSpec, num_users: int,
+                 target: int) -> np.ndarray:
+    cap = max(1, spec.num_items // 2)
+    if spec.degree_law == "geometric":
+        d = rng.geometric(1.0 / 20.0, size=num_users).astype(np.int64)
+        d = np.clip(d, 1, cap)
+    else:
+        z = rng.standard_normal(num_users)
+        mu = math.log(spec.lognormal_median)
+
+        def total(sigma: float) -> int:
+            return int(np.clip(np.rint(np.exp(mu + sigma * z)), 1, cap).sum())
+
+        lo, hi = 0.0, 4.0
+        for _ in range(60):
+            mid = 0.5 * (lo + hi)
+            if total(mid) < target:
+                lo = mid
+            else:
+                hi = mid
+        d = np.clip(np.rint(np.exp(mu + hi * z)), 1, cap).astype(np.int64)
+    # exact fix-up: spread the remainder over random users within bounds
+    diff = int(target - d.sum())
+    while diff != 0:
+        step = 1 if diff > 0 else -1
+        cand = np.flatnonzero(d < cap) if step > 0 else np.flatnonzero(d > 1)
+        take = rng.choice(cand, size=min(abs(diff), len(cand)), replace=False)
+        d[take] += step
+        diff -= step * len(take)
+    return d
+
+
+def _zipf_cdf(num_items: int, s: float) -> np.ndarray:
+    w = 1.0 / np.power(np.arange(1, num_items + 1, dtype=np.float64), s)
+    c = np.cumsum(w)
+    return c / c[-1]
+
+
+def _distinct_draws(rng, cdf, users_rep: np.ndarray, need: np.ndarray, num_items: int):
+    """For a block of users, draw need[u] distinct Zipf ranks each.
+
+    users_rep: local user index per slot; need: per local user counts.
+    Returns (local_user, rank) arrays with exactly need[u] rows per user."""
+    n_local = len(need)
+    have_u = np.empty(0, np.int64)
+    have_r = np.empty(0, np.int64)
+    have_o = np.empty(0, np.int64)
+    short = need.copy()
+    order_base = 0
+    factor = 1.3
+    while True:
+        todo = np.flatnonzero(short > 0)
+        if len(todo) == 0:
+            break
+        m = np.ceil(short[todo] * factor).astype(np.int64) + 2
+        uu = np.repeat(todo, m)
+        rr = np.searchsorted(cdf, rng.random(len(uu)), side="right").astype(np.int64)
+        rr = np.minimum(rr, num_items - 1)
+        oo = order_base + np.arange(len(uu), dtype=np.int64)
+        order_base += len(uu)
+        cu = np.concatenate([have_u, uu])
+        cr = np.concatenate([have_r, rr])
+        co = np.concatenate([have_o, oo])
+        key = cu * num_items + cr
+        _, first = np.unique(key, return_index=True)
+        cu, cr, co = cu[first], cr[first], co[first]
+        # per user keep the first need[u] distinct ranks in draw order
+        srt = np.lexsort((co, cu))
+        cu, cr, co = cu[srt], cr[srt], co[srt]
+        start = np.searchsorted(cu, np.arange(n_local), side="left")
+        pos = np.arange(len(cu)) - start[cu]
+        keep = pos < need[cu]
+        have_u, have_r, have_o = cu[keep], cr[keep], co[keep]
+        got = np.bincount(have_u, minlength=n_local)
+        short = need - got
+        factor *= 2.0
+    return have_u, have_r
+
+
+def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
+                 test_fraction: float | None = None, users_per_block: int = 200_000,
+                 scale: float = 1.0):
+    """(train, test, spec) for a workload.  ``scale`` < 1 shrinks the user
+    count and interaction target proportionally (for fast tests)."""
+    if isinstance(spec, str):
+        spec = CONFIGS[spec]
+    tf = spec.test_fraction if test_fraction is None else test_fraction
+    num_users = max(1, int(round(spec.num_users * scale)))
+    target = max(num_users, int(round(spec.interactions * scale)))
+    rng = np.random.Generator(np.random.PCG64(gen_seed))
+    deg = _fit_degrees(rng, spec, num_users, target)
+    rank_to_id = rng.permutation(spec.num_items).astype(np.int64)
+    cdf = _zipf_cdf(spec.num_items, spec.zipf_s)
+    tr_u, tr_i, te_u, te_i = [], [], [], []
+    for b0 in range(0, num_users, users_per_block):
+        b1 = min(num_users, b0 + users_per_block)
+        need = deg[b0:b1]
+        lu, lr = _distinct_draws(rng, cdf, None, need, spec.num_items)
+        users = lu + b0
+        items = rank_to_id[lr]
+        if tf > 0:
+            d = need[lu]
+            n_test = (d * tf).astype(np.int64)
+            n_test = np.where(d - n_test < 1, np.maximum(0, d - 1), n_test)
+            key = rng.random(len(lu))
+            srt = np.lexsort((key, lu))
+            lu_s = lu[srt]
+            start = np.searchsorted(lu_s, np.arange(len(need)), side="left")
+            rank = np.empty(len(lu), np.int64)
+            rank[srt] = np.arange(len(lu)) - start[lu_s]
+            is_test = rank < n_test
+            te_u.append(users[is_test])
+            te_i.append(items[is_test])
+            tr_u.append(users[~is_test])
+            tr_i.append(items[~is_test])
+        else:
+            tr_u.append(users)
+            tr_i.append(items)
+    train = from_pairs(np.concatenate(tr_u), np.concatenate(tr_i), num_users, spec.num_items)
+    if tf > 0:
+        test = from_pairs(np.concatenate(te_u), np.concatenate(te_i), num_users, spec.num_items)
+    else:
+        test = InteractionSet(num_users, spec.num_items, np.zeros(num_users + 1, np.int64),
+                              np.empty(0, np.int32))
+    return train, test, spec
+
+
+def make_clustered(num_users: int, num_items: int, clusters: int, per_user: int, *,
+                   affinity: float = 0.95, test_fraction: float = 0.2, seed: int = 0):
+    """Planted-cluster data with a learnable signal (users of cluster c mostly
+    interact with the items of block c).  Used by the convergence tests."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    block = num_items // clusters
+    users = np.repeat(np.arange(num_users, dtype=np.int64), per_user)
+    c = users % clusters
+    lo = c * block
+    hi = np.where(c == clusters - 1, num_items, lo + block)
+    inside = rng.random(len(users)) < affinity
+    items = np.where(inside, lo + (rng.random(len(users)) * (hi - lo)).astype(np.int64),
+                     rng.integers(0, num_items, size=len(users)))
+    key = np.unique(users * num_items + items)
+    users, items = key // num_items, key % num_items
+    r = rng.random(len(users))
+    srt = np.lexsort((r, users))
+    us = users[srt]
+    start = np.searchsorted(us, np.arange(num_users), side="left")
+    cnt = np.bincount(users, minlength=num_users)
+    rank = np.empty(len(users), np.int64)
+    rank[srt] = np.arange(len(users)) - start[us]
+    n_test = (cnt * test_fraction).astype(np.int64)
+    n_test = np.where(cnt - n_test < 1, np.maximum(0, cnt - 1), n_test)
+    is_test = rank < n_test[users]
+    train = from_pairs(users[~is_test], items[~is_test], num_users, num_items)
+    test = from_pairs(users[is_test], items[is_test], num_users, num_items)
+    return train, test
