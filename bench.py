@@ -1,0 +1,322 @@
+"""Benchmark of the SimpleX-MF-CCL training step on B200.
+
+Metric (BASELINE.json): training samples/s, one sample = one (user, positive,
+N negatives) pair — the reference's ``pairs_per_s`` (bench.py:83 of heatcf).
+A bench "step" is one epoch over the synthetic workload's training pairs
+(the unit the reference's bench times).  Default workload: BASELINE config 2
+(30k users x 41k items, 1.03M interactions with a 20 % hold-out, K=64, N=100,
+theta 0.9, mu 150, B=1024), Hogwild kernel with B pairs in flight.
+
+JSON line keys beyond the base contract:
+  roofline      algorithmic bytes of the fused kernel / its CUDA-event time,
+                against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the C oracle port (restatement of trainer.py:103-466, pthreads
+                Hogwild, all host cores) on a bounded sample of the same pairs
+  e2e           the same metric through the public drop-in API
+                ``train_epoch(S, T, train, cfg)`` with host numpy tables:
+                shuffle + H2D of tables and pairs + kernel + D2H of tables
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training samples/sec (user,pos,N negs) at 1/2/4/8 B200; % HBM roofline"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_workload(name: str):
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.synth import make_dataset
+    train, test, spec = make_dataset(name)
+    S = init_matrix(train.num_users, spec.dim, InitSpec(seed=0))
+    T = init_matrix(train.num_items, spec.dim, InitSpec(seed=0))
+    return train, test, spec, S, T
+
+
+def train_config(spec, threads: int):
+    from paper_2304_07334_b200.config import LossParams, TrainingConfig
+    return TrainingConfig(emb_dim=spec.dim, num_negatives=spec.negatives,
+                          learning_rate=spec.learning_rate, epochs=1, num_threads=threads,
+                          loss=LossParams(mu=spec.mu, theta=spec.theta), seed=0)
+
+
+def algorithmic_bytes(npairs: int, K: int, N: int, active: int) -> int:
+    """4K(N+2)+8 read + 4K(2+A_p) written per pair."""
+    return npairs * (4 * K * (N + 2) + 8 + 4 * K * 2) + 4 * K * active
+
+
+def cpu_baseline(spec, train, S0, T0, sample_pairs: int, threads: int, epoch: int = 0) -> dict:
+    """Oracle port (C, pthreads Hogwild, the reference's chunk-claiming
+    driver) on the first `sample_pairs` pairs of the epoch."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.rng import shuffle_seed
+    u, i = epoch_pairs(train, shuffle_seed(0, epoch))
+    n = min(sample_pairs, len(u))
+    S, T = S0.copy(), T0.copy()
+    O.lib()
+    t0 = time.perf_counter()
+    O.train_epoch_threads(S, T, u[:n], i[:n], seed=0, epoch=epoch, num_threads=threads,
+                          n_neg=spec.negatives, lr=spec.learning_rate, mu=spec.mu,
+                          theta=spec.theta)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"first {n} pairs of epoch {epoch} of {spec.name} "
+                      f"(oracle/heat_oracle.c, {threads} threads, chunk 2048)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    train, _, spec, S, T = build_workload(args.config)
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample or {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 20_000,
+                                 "c5": 20_000}[spec.name]
+    for w in range(args.warmup):
+        cpu_baseline(spec, train, S.values, T.values, min(sample, 20000), threads, epoch=w)
+    vals = []
+    secs = []
+    for s in range(args.steps):
+        r = cpu_baseline(spec, train, S.values, T.values, sample, threads, epoch=args.warmup + s)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    v = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean(secs)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": spec.name, "users": train.num_users,
+                       "items": train.num_items, "train_pairs": train.num_pairs,
+                       "dim": spec.dim, "negatives": spec.negatives, "batch": spec.batch},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact"])
+    ap.add_argument("--window", type=int, default=0, help="pairs in flight (0: config batch)")
+    ap.add_argument("--fp64", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.trainer import configure, train_epoch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    train, test, spec, S, T = build_workload(args.config)
+    window = args.window or spec.batch
+    mode = N.MODE_HOGWILD if args.mode == "hogwild" else N.MODE_EXACT
+    K, NN = spec.dim, spec.negatives
+    total_epochs = args.warmup + args.steps
+    # replicas only for now: every rank trains its own copy of the workload
+    pairs_host = [epoch_pairs(train, shuffle_seed(0, e)) for e in range(total_epochs)]
+    model = DeviceModel(S.values, T.values, dev)
+    pairs_dev = [model.upload_pairs(u, i) for u, i in pairs_host]
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    npairs = len(pairs_host[0][0])
+    stream = torch.cuda.current_stream(dev)
+
+    def one_epoch(e, timed):
+        p = model.params(n_neg=NN, lr=spec.learning_rate, l2=0.0, mu=spec.mu,
+                         theta=spec.theta, cosine=True, mode=mode,
+                         stream_base=epoch_stream(0, e), window=window, fp64=args.fp64)
+        model.counters.reset()
+        flush.zero_()  # L2 flush between steps (outside the timed region)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        du, di = pairs_dev[e]
+        model.train_range(du, di, 0, npairs, p)
+        ev1.record(stream)
+        ev1.synchronize()
+        c = model.counters.read()
+        return ev0.elapsed_time(ev1) / 1e3, c
+
+    for e in range(args.warmup):
+        one_epoch(e, False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times, actives, losses = [], [], []
+    for s in range(args.steps):
+        dt, c = one_epoch(args.warmup + s, True)
+        times.append(dt)
+        actives.append(c.active)
+        losses.append(c.loss / npairs)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total = sum(times)
+    if world > 1:
+        t = torch.tensor([total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+        dist.barrier()
+    value = world * npairs * args.steps / total
+    kernel_s = total / args.steps
+    bytes_per_epoch = algorithmic_bytes(npairs, K, NN, int(np.mean(actives)))
+    peak, peak_kind = _peaks()
+    achieved = bytes_per_epoch / kernel_s / 1e9
+
+    # e2e: the public drop-in API with host numpy tables
+    configure(mode=args.mode, window=window, fp64=args.fp64)
+    cfg = train_config(spec, threads=8 if args.mode == "hogwild" else 1)
+    Se, Te = S.copy(), T.copy()
+    train_epoch(Se, Te, train, cfg, epoch=0)
+    torch.cuda.synchronize()
+    e2e_times = []
+    for e in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        train_epoch(Se, Te, train, cfg, epoch=1 + e)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_value = world * npairs / float(np.mean(e2e_times))
+    h2d = S.values.nbytes + T.values.nbytes + 8 * npairs
+    d2h = S.values.nbytes + T.values.nbytes
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        sample = {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 20_000, "c5": 20_000}[spec.name]
+        cpu_baseline(spec, train, S.values, T.values, 20000, threads)  # warm
+        cpu = cpu_baseline(spec, train, S.values, T.values, sample, threads)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.fp64 else "f32", "data": "synthetic",
+            "config": {"workload": spec.name, "users": train.num_users,
+                       "items": train.num_items, "train_pairs": npairs, "dim": K,
+                       "negatives": NN, "theta": spec.theta, "mu": spec.mu,
+                       "batch": spec.batch, "window": window, "mode": args.mode,
+                       "lr": spec.learning_rate, "step": "one epoch",
+                       "l2_flush": "512 MiB write between steps; S+T "
+                                   f"{(S.values.nbytes + T.values.nbytes) / 1e6:.1f} MB"
+                                   " re-read from HBM each step",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None,
+                         "bytes_per_launch": bytes_per_epoch,
+                         "active_negatives_per_pair": float(np.mean(actives)) / npairs},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps,
+            "clocks": clk,
+            "mean_loss": float(np.mean(losses)),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

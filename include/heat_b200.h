@@ -1,0 +1,118 @@
+/*
+ * heat_b200.h — C ABI of the B200 SimpleX-MF-CCL training path.
+ *
+ * Plain pointers and sizes only (no torch types).  All table / index
+ * pointers are DEVICE pointers owned by the caller; `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).  Every entry
+ * point validates its arguments on the host, launches asynchronously on
+ * `stream`, and returns a status code; heat_last_error() returns the
+ * message of the last failure on the calling thread.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/heatcf):
+ *   heat_train_range       <- trainer._train_chunk           trainer.py:103-331
+ *                             (uniform sampler, no aggregator; cosine or dot)
+ *                             driven per epoch by train_epoch trainer.py:385-466
+ *   heat_sample_negatives  <- rng_below loop of _train_chunk trainer.py:135-139,
+ *                             rng.rng_next / rng_below     rng.py:63-76
+ *   heat_eval_users        <- evaluator.evaluate scoring + top-k + hits
+ *                             evaluator.py:140-172, _topk_from_scores 61-73
+ *   heat_apply_row_deltas  <- (new) multi-GPU item-delta exchange, SURVEY.md §8(e)
+ */
+#ifndef HEAT_B200_H
+#define HEAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEAT_OK 0
+#define HEAT_ERR_INVALID 1     /* bad argument (reference raises ValueError) */
+#define HEAT_ERR_CUDA 2        /* CUDA runtime error (reference: RuntimeError) */
+#define HEAT_ERR_UNSUPPORTED 3 /* option outside the built path (ValueError) */
+
+/* Execution modes of heat_train_range. */
+#define HEAT_MODE_EXACT 0   /* pairs strictly in order; bit-identical to the
+                               reference with num_threads=1 */
+#define HEAT_MODE_HOGWILD 1 /* up to `window` pairs in flight, lock-free
+                               atomic row updates (reference num_threads>1) */
+#define HEAT_MODE_DELTA 2   /* hogwild reads, but item-row updates are logged
+                               to a delta buffer instead of applied (the
+                               multi-GPU step; users still updated in place) */
+
+typedef struct heat_sgd_params {
+    int32_t dim;          /* K: columns of S and T                          */
+    int32_t n_neg;        /* N: negatives per pair                          */
+    int32_t use_cosine;   /* 1: cosine similarity, 0: dot                   */
+    int32_t mode;         /* HEAT_MODE_*                                    */
+    double lr;            /* learning_rate                                  */
+    double l2;            /* l2_reg                                         */
+    double mu;            /* loss.mu (negative weight)                      */
+    double theta;         /* loss.theta (margin)                            */
+    uint64_t stream_base; /* s0 = derive_stream(seed, 0x45504F43, epoch, 0);
+                             negative j of the pair at epoch position p is
+                             draw p*N+j of this stream                      */
+    int32_t window;       /* HOGWILD/DELTA: max pairs in flight (step size B);
+                             <=0 means "as many as the GPU holds"           */
+    int32_t flags;        /* bit0: fp64 dot products in HOGWILD (default fp32
+                             partials + fp64 combine when 0)               */
+} heat_sgd_params;
+
+/* Device-resident accumulators (caller zeroes them; kernels add). */
+typedef struct heat_counters {
+    double loss;        /* running sum of per-pair losses (trainer.py:222)  */
+    int64_t degenerate; /* zero-norm similarity hits (trainer.py:187,203)   */
+    int64_t active;     /* negatives with nonzero loss gradient             */
+    int64_t pairs;      /* pairs processed                                  */
+} heat_counters;
+
+/* Train pairs [start, stop) of an epoch's (ep_users, ep_items) order.
+ * S: s_rows x dim float32 row-major; T: t_rows x dim; negatives are uniform
+ * over [0, t_rows) exactly like trainer.py:136 (num_items = T.rows).
+ * `counters` is a device pointer.  For HEAT_MODE_DELTA, `delta_ids`
+ * (int32, capacity entries) and `delta_rows` (capacity x dim float32) receive
+ * the item-row updates and `delta_count` (device int64) their number.
+ * Scratch (HEAT_MODE_EXACT): `scratch` may be NULL (internal allocation) or a
+ * device buffer of at least heat_scratch_bytes(n_neg, dim) bytes. */
+int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                     const int32_t *ep_users, const int32_t *ep_items, int64_t start,
+                     int64_t stop, const heat_sgd_params *params, heat_counters *counters,
+                     int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
+                     int64_t delta_capacity, void *scratch, void *stream);
+
+int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim);
+
+/* out[(p - first_pair) * n_neg + j] = negative j of pair p, for
+ * p in [first_pair, first_pair + npairs): the id trainer.py:136 draws. */
+int heat_sample_negatives(uint64_t stream_base, int64_t first_pair, int64_t npairs,
+                          int32_t n_neg, int64_t num_items, int32_t *out, void *stream);
+
+/* Recall/NDCG parts for a list of users (device arrays).
+ * S holds the query rows, float32 (s_f64 = 0) or float64 (s_f64 = 1).
+ * users[n_users]; train CSR (tr_offsets[tr_num_users+1], tr_items) masks
+ * positives; test CSR (te_offsets, te_items; sorted slices) gives hits.
+ * dcg_weights[k] = 1/log2(r+1), idcg[k] = prefix sums, both computed by the
+ * caller in the reference's arithmetic (evaluator.py:144-148).
+ * Outputs per user: recall (hits / n_test), ndcg (dcg / idcg[min(k,n)-1]);
+ * topk (n_users x k, -1 padded) may be NULL.  similarity: 1 cosine, 0 dot. */
+int heat_eval_users(const void *S, int32_t s_f64, const float *T, int64_t t_rows, int32_t dim,
+                    const int32_t *users, int64_t n_users, const int64_t *tr_offsets,
+                    const int32_t *tr_items, int64_t tr_num_users, const int64_t *te_offsets,
+                    const int32_t *te_items, int32_t k, int32_t use_cosine,
+                    const double *dcg_weights, const double *idcg, int32_t *topk,
+                    double *recall, double *ndcg, void *stream);
+
+/* T[ids[i]] += rows[i] for i < *count (device count), in index order per row
+ * when `ordered` != 0 (deterministic replica update), atomically otherwise. */
+int heat_apply_row_deltas(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,
+                          const float *rows, const int64_t *count, int64_t capacity,
+                          int32_t ordered, void *stream);
+
+const char *heat_last_error(void);
+int heat_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEAT_B200_H */

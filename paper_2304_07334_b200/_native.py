@@ -1,0 +1,99 @@
+"""ctypes binding of libheat_b200.so (include/heat_b200.h).
+
+The library is the only compute path: if it is missing or cannot be loaded,
+``lib()`` raises — there is no CPU fallback anywhere in the product.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libheat_b200.so")
+
+HEAT_OK = 0
+HEAT_ERR_INVALID = 1
+HEAT_ERR_CUDA = 2
+HEAT_ERR_UNSUPPORTED = 3
+
+MODE_EXACT = 0
+MODE_HOGWILD = 1
+MODE_DELTA = 2
+
+EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
+           "heat_eval_users", "heat_apply_row_deltas", "heat_last_error", "heat_version")
+
+
+class SgdParams(ctypes.Structure):
+    _fields_ = [
+        ("dim", ctypes.c_int32),
+        ("n_neg", ctypes.c_int32),
+        ("use_cosine", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+        ("lr", ctypes.c_double),
+        ("l2", ctypes.c_double),
+        ("mu", ctypes.c_double),
+        ("theta", ctypes.c_double),
+        ("stream_base", ctypes.c_uint64),
+        ("window", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+    ]
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [
+        ("loss", ctypes.c_double),
+        ("degenerate", ctypes.c_int64),
+        ("active", ctypes.c_int64),
+        ("pairs", ctypes.c_int64),
+    ]
+
+
+COUNTERS_BYTES = ctypes.sizeof(Counters)
+
+_lib = None
+
+
+class HeatError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load (never build) the native library; raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2304_07334_b200.build` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+    L.heat_train_range.restype = ctypes.c_int
+    L.heat_train_range.argtypes = [P, i64, P, i64, P, P, i64, i64, ctypes.POINTER(SgdParams), P,
+                                   P, P, P, i64, P, P]
+    L.heat_scratch_bytes.restype = i64
+    L.heat_scratch_bytes.argtypes = [i32, i32]
+    L.heat_sample_negatives.restype = ctypes.c_int
+    L.heat_sample_negatives.argtypes = [u64, i64, i64, i32, i64, P, P]
+    L.heat_eval_users.restype = ctypes.c_int
+    L.heat_eval_users.argtypes = [P, i32, P, i64, i32, P, i64, P, P, i64, P, P, i32, i32, P, P,
+                                  P, P, P, P]
+    L.heat_apply_row_deltas.restype = ctypes.c_int
+    L.heat_apply_row_deltas.argtypes = [P, i64, i32, P, P, P, i64, i32, P]
+    L.heat_last_error.restype = ctypes.c_char_p
+    L.heat_last_error.argtypes = []
+    L.heat_version.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    """Map a status code to the reference's exception types."""
+    if rc == HEAT_OK:
+        return
+    msg = lib().heat_last_error().decode(errors="replace")
+    if rc in (HEAT_ERR_INVALID, HEAT_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    raise HeatError(msg)

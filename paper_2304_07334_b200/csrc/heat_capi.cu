@@ -1,0 +1,234 @@
+// heat_capi.cu — the C ABI declared in include/heat_b200.h.
+//
+// Host-side validation mirrors the reference's error behaviour: bad shapes
+// and options are rejected before any device work (trainer.py:366-382, the
+// dataclass checks of trainer.py:55-59,79-87 and kernels.py:50-54), and
+// options outside the built path (tiling sampler, aggregator) are rejected by
+// the Python layer with ValueError — there is no CPU fallback.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "heat_common.cuh"
+#include "heat_internal.h"
+
+namespace heat {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+static int cuda_fail(cudaError_t e, const char *what) {
+    return fail(HEAT_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 1;
+    }
+    return cached[dev];
+}
+
+// Scratch for exact-mode snapshots when the caller passes none.
+static std::mutex g_scratch_mu;
+static void *g_scratch[64] = {nullptr};
+static size_t g_scratch_size[64] = {0};
+
+static void *get_scratch(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    if (g_scratch_size[dev] < bytes) {
+        if (g_scratch[dev]) cudaFree(g_scratch[dev]);
+        g_scratch[dev] = nullptr;
+        g_scratch_size[dev] = 0;
+        if (cudaMalloc(&g_scratch[dev], bytes) != cudaSuccess) return nullptr;
+        g_scratch_size[dev] = bytes;
+    }
+    return g_scratch[dev];
+}
+
+// ---- ordered / atomic item-delta application (multi-GPU exchange) --------
+// ordered: ids sorted ascending (stable), each run of equal ids summed in
+// index order by one warp and added once -> bit-identical on every replica.
+__global__ void apply_deltas_ordered(float *__restrict__ T, int K, const int32_t *__restrict__ ids,
+                                     const float *__restrict__ rows, const int64_t *count_p,
+                                     int64_t capacity) {
+    const int64_t count = imin64(*count_p, capacity);
+    const int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (; w < count; w += nw) {
+        const int32_t id = ids[w];
+        if (w > 0 && ids[w - 1] == id) continue;  // not a run head
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            int k = k0 + lane;
+            if (k >= K) break;
+            float acc = 0.f;
+            for (int64_t i = w; i < count && ids[i] == id; ++i) acc += rows[i * K + k];
+            T[(int64_t)id * K + k] += acc;
+        }
+    }
+}
+
+__global__ void apply_deltas_atomic(float *__restrict__ T, int K, const int32_t *__restrict__ ids,
+                                    const float *__restrict__ rows, const int64_t *count_p,
+                                    int64_t capacity) {
+    const int64_t count = imin64(*count_p, capacity);
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < count * K; i += stride) {
+        int64_t r = i / K;
+        int k = (int)(i % K);
+        atomicAdd(T + (int64_t)ids[r] * K + k, rows[i]);
+    }
+}
+
+cudaError_t launch_apply_deltas(float *T, int64_t t_rows, int K, const int32_t *ids,
+                                const float *rows, const int64_t *count, int64_t capacity,
+                                int ordered, cudaStream_t stream) {
+    (void)t_rows;
+    int blocks = sm_count() * 4;
+    if (ordered)
+        apply_deltas_ordered<<<blocks, 256, 0, stream>>>(T, K, ids, rows, count, capacity);
+    else
+        apply_deltas_atomic<<<blocks, 256, 0, stream>>>(T, K, ids, rows, count, capacity);
+    return cudaGetLastError();
+}
+
+}  // namespace heat
+
+using namespace heat;
+
+extern "C" {
+
+const char *heat_last_error(void) { return g_err.c_str(); }
+
+int heat_version(void) { return 1; }
+
+int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim) {
+    return (int64_t)n_neg * (int64_t)dim * (int64_t)sizeof(float) + 256;
+}
+
+int heat_sample_negatives(uint64_t stream_base, int64_t first_pair, int64_t npairs,
+                          int32_t n_neg, int64_t num_items, int32_t *out, void *stream) {
+    if (n_neg < 1) return fail(HEAT_ERR_INVALID, "num_negatives must be >= 1, got %d", n_neg);
+    if (num_items < 1 || num_items >= (int64_t)1 << 31)
+        return fail(HEAT_ERR_INVALID, "num_items must be in [1, 2^31), got %lld",
+                    (long long)num_items);
+    if (npairs < 0 || first_pair < 0) return fail(HEAT_ERR_INVALID, "negative pair range");
+    if (npairs > 0 && !out) return fail(HEAT_ERR_INVALID, "null output");
+    cudaError_t e = launch_sample(stream_base, first_pair, npairs, n_neg, num_items, out,
+                                  (cudaStream_t)stream);
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "sample_negatives launch");
+}
+
+int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                     const int32_t *ep_users, const int32_t *ep_items, int64_t start,
+                     int64_t stop, const heat_sgd_params *p, heat_counters *counters,
+                     int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
+                     int64_t delta_capacity, void *scratch, void *stream) {
+    if (!p) return fail(HEAT_ERR_INVALID, "null params");
+    if (!S || !T || !counters) return fail(HEAT_ERR_INVALID, "null table or counters pointer");
+    if (p->dim < 1) return fail(HEAT_ERR_INVALID, "dim must be >= 1, got %d", p->dim);
+    if (p->n_neg < 1)
+        return fail(HEAT_ERR_INVALID, "num_negatives must be >= 1, got %d", p->n_neg);
+    if (!(p->lr > 0)) return fail(HEAT_ERR_INVALID, "learning_rate must be positive");
+    if (p->mu < 0) return fail(HEAT_ERR_INVALID, "mu must be >= 0, got %g", p->mu);
+    if (!(p->theta >= -1.0 && p->theta <= 1.0))
+        return fail(HEAT_ERR_INVALID, "theta must be in [-1, 1], got %g", p->theta);
+    if (s_rows < 1 || t_rows < 1) return fail(HEAT_ERR_INVALID, "empty embedding table");
+    if (t_rows >= (int64_t)1 << 31) return fail(HEAT_ERR_INVALID, "item table too large");
+    if (start < 0 || stop < start) return fail(HEAT_ERR_INVALID, "bad pair range");
+    if (stop > start && (!ep_users || !ep_items)) return fail(HEAT_ERR_INVALID, "null pairs");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (stop == start) return HEAT_OK;
+    cudaError_t e;
+    switch (p->mode) {
+    case HEAT_MODE_EXACT: {
+        if (exact_smem_bytes(p->dim, p->n_neg) > 220 * 1024)
+            return fail(HEAT_ERR_UNSUPPORTED, "exact mode: n_neg=%d dim=%d exceeds shared memory",
+                        p->n_neg, p->dim);
+        void *snap = scratch ? scratch : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim));
+        if (!snap) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
+        e = launch_exact(S, T, ep_users, ep_items, start, stop, p->dim, p->n_neg, p->use_cosine,
+                         p->lr, p->l2, p->mu, p->theta, p->stream_base, t_rows, counters,
+                         (float *)snap, st);
+        break;
+    }
+    case HEAT_MODE_HOGWILD:
+    case HEAT_MODE_DELTA: {
+        if (p->dim > 512)
+            return fail(HEAT_ERR_UNSUPPORTED, "hogwild mode supports dim <= 512, got %d", p->dim);
+        if (p->mode == HEAT_MODE_DELTA && (!delta_ids || !delta_rows || !delta_count))
+            return fail(HEAT_ERR_INVALID, "delta mode needs delta buffers");
+        HogwildArgs a;
+        a.S = S; a.T = T; a.users = ep_users; a.items = ep_items;
+        a.start = start; a.stop = stop;
+        a.K = p->dim; a.N = p->n_neg; a.cosine = p->use_cosine;
+        a.lr = (float)p->lr; a.l2 = (float)p->l2; a.mu = p->mu; a.theta = p->theta;
+        a.s0 = p->stream_base; a.num_items = t_rows; a.ctr = counters;
+        a.window = p->window; a.fp64 = p->flags & 1;
+        a.delta_ids = p->mode == HEAT_MODE_DELTA ? delta_ids : nullptr;
+        a.delta_rows = delta_rows; a.delta_count = delta_count;
+        a.delta_capacity = delta_capacity;
+        e = launch_hogwild(a, st, nullptr);
+        break;
+    }
+    default:
+        return fail(HEAT_ERR_INVALID, "unknown mode %d", p->mode);
+    }
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "train_range launch");
+}
+
+int heat_eval_users(const void *S, int32_t s_f64, const float *T, int64_t t_rows, int32_t dim,
+                    const int32_t *users, int64_t n_users, const int64_t *tr_offsets,
+                    const int32_t *tr_items, int64_t tr_num_users, const int64_t *te_offsets,
+                    const int32_t *te_items, int32_t k, int32_t use_cosine,
+                    const double *dcg_weights, const double *idcg, int32_t *topk,
+                    double *recall, double *ndcg, void *stream) {
+    if (k < 1) return fail(HEAT_ERR_INVALID, "k must be >= 1, got %d", k);
+    if (dim < 1 || dim > 512) return fail(HEAT_ERR_UNSUPPORTED, "eval supports 1 <= dim <= 512");
+    if (t_rows < 1 || t_rows >= (int64_t)1 << 31) return fail(HEAT_ERR_INVALID, "bad t_rows");
+    if (n_users < 0) return fail(HEAT_ERR_INVALID, "negative user count");
+    if (n_users > 0 && (!S || !T || !users || !te_offsets || !te_items || !dcg_weights || !idcg ||
+                        !recall || !ndcg))
+        return fail(HEAT_ERR_INVALID, "null pointer argument");
+    if (tr_num_users > 0 && (!tr_offsets || !tr_items))
+        return fail(HEAT_ERR_INVALID, "null train CSR");
+    cudaError_t e = launch_eval(S, s_f64, T, t_rows, dim, users, n_users, tr_offsets, tr_items,
+                                tr_num_users, te_offsets, te_items, k, use_cosine, dcg_weights,
+                                idcg, topk, recall, ndcg, (cudaStream_t)stream);
+    if (e == cudaErrorInvalidValue)
+        return fail(HEAT_ERR_UNSUPPORTED, "eval: k=%d with dim=%d exceeds shared memory", k, dim);
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "eval launch");
+}
+
+int heat_apply_row_deltas(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,
+                          const float *rows, const int64_t *count, int64_t capacity,
+                          int32_t ordered, void *stream) {
+    if (!T || !ids || !rows || !count) return fail(HEAT_ERR_INVALID, "null pointer argument");
+    if (dim < 1) return fail(HEAT_ERR_INVALID, "dim must be >= 1");
+    cudaError_t e = launch_apply_deltas(T, t_rows, dim, ids, rows, count, capacity, ordered,
+                                        (cudaStream_t)stream);
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "apply_row_deltas launch");
+}
+
+}  // extern "C"

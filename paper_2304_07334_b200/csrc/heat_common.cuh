@@ -1,0 +1,65 @@
+// heat_common.cuh — shared device helpers for the B200 CCL training path.
+//
+// Counter-form SplitMix64 (restates /root/reference/pkg/src/heatcf/rng.py:26-31
+// and 63-76): draw n (0-based) of the stream whose state is s0 is
+// mix64(s0 + (n + 1) * GAMMA).  The reference's single-thread epoch draws
+// negative j of the pair at epoch position p as draw p*N + j
+// (trainer.py:134-139), so a sampler keyed by the global pair index returns
+// the reference's ids whatever the thread/warp/GPU decomposition.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace heat {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMix2 = 0x94D049BB133111EBull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * kMix1;
+    z = (z ^ (z >> 27)) * kMix2;
+    return z ^ (z >> 31);
+}
+
+// Exact z mod n for 64-bit z and 1 <= n < 2^31 without the slow 64-bit
+// division routine: q0 = umulhi(z, floor((2^64-1)/n)) satisfies
+// q - 2 <= q0 <= q, so at most two corrections.  (rng.py:76 takes
+// `rng_next(state) % uint64(n)`; tests check this against % on device.)
+struct FastMod {
+    uint64_t n;
+    uint64_t m;  // floor((2^64 - 1) / n)
+    __host__ __device__ static FastMod make(uint64_t n) { return FastMod{n, ~0ull / n}; }
+    __device__ __forceinline__ uint64_t mod(uint64_t z) const {
+        uint64_t q = __umul64hi(z, m);
+        uint64_t r = z - q * n;
+        if (r >= n) r -= n;
+        if (r >= n) r -= n;
+        return r;
+    }
+};
+
+// Negative j of the pair at global epoch position p.
+__device__ __forceinline__ int32_t neg_id(uint64_t s0, int64_t p, int n_neg, int j,
+                                          const FastMod &fm) {
+    uint64_t n = (uint64_t)p * (uint64_t)n_neg + (uint64_t)j;
+    return (int32_t)fm.mod(mix64(s0 + (n + 1ull) * kGamma));
+}
+
+__device__ __forceinline__ float4 ldcg4(const float *p) {
+    return __ldcg(reinterpret_cast<const float4 *>(p));
+}
+
+// Vector atomic add (sm_90+: red.global.add.v4.f32), no return value.
+__device__ __forceinline__ void red_add4(float *addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+                 "f"(c), "f"(d)
+                 : "memory");
+}
+
+}  // namespace heat
+
+namespace heat {
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+}  // namespace heat

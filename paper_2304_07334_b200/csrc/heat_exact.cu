@@ -1,0 +1,304 @@
+// heat_exact.cu — deterministic ("exact") SGD over pairs in strict order.
+//
+// Bit-identical to the reference with num_threads=1: it restates the
+// per-pair body of /root/reference/pkg/src/heatcf/trainer.py:114-297
+// (tiled=False, agg_on=False) with every binary64 operation written as an
+// explicit round-to-nearest intrinsic (__dmul_rn, __dadd_rn, __ddiv_rn,
+// __dsqrt_rn), so nothing can be contracted into an FMA, and float32
+// rounding on store (__double2float_rn).  This file is also compiled with
+// --fmad=false as a second guard.
+//
+// Parallel decomposition of one pair (one CTA, pairs sequential):
+//   read/similarity  thread r owns row r (r=0 the positive, r>=1 negative r-1):
+//                    a strictly sequential k-loop for tt and st, exactly the
+//                    reference's accumulation order (trainer.py:176-207);
+//   loss             ordered active list built with warp ballots, the hinge
+//                    summed in j order by one thread (trainer.py:214-222);
+//   gradient/update  thread k owns column k of every row: ugrad[k] in j order
+//                    (trainer.py:230-251), then T[pos], T[neg_j] in j order,
+//                    S[u] (trainer.py:259-293).  A column is only ever
+//                    touched by its own thread inside a pair, so repeated ids
+//                    (pos == neg, duplicate negatives) see the same
+//                    read-after-write order as the reference.  Snapshots of
+//                    active negative rows (the reference's neg_buf) are taken
+//                    column-wise before any write.
+#include <cstdint>
+
+#include "heat_common.cuh"
+#include "heat_internal.h"
+
+namespace heat {
+
+#define DMUL __dmul_rn
+#define DADD __dadd_rn
+#define DSUB __dsub_rn
+#define DDIV __ddiv_rn
+#define DSQRT __dsqrt_rn
+
+constexpr int kExactThreads = 512;
+constexpr int kExactWarps = kExactThreads / 32;
+
+struct ExactSmem {
+    double ss, tt_p, st_p, sim_p;
+    int n_loss;  // negatives with d > 0, in j order in list[]
+    int warp_cnt[kExactWarps];
+};
+
+__device__ __forceinline__ void row_dots(const float *__restrict__ row, const double *ubuf, int K,
+                                         double &tt, double &st) {
+    // trainer.py:193-197: tt += v*v; st += u*v, k ascending, binary64.
+    double a = 0.0, b = 0.0;
+    int k = 0;
+    for (; k + 4 <= K; k += 4) {
+        float v0 = row[k], v1 = row[k + 1], v2 = row[k + 2], v3 = row[k + 3];
+        double x0 = (double)v0, x1 = (double)v1, x2 = (double)v2, x3 = (double)v3;
+        a = DADD(a, DMUL(x0, x0)); b = DADD(b, DMUL(ubuf[k], x0));
+        a = DADD(a, DMUL(x1, x1)); b = DADD(b, DMUL(ubuf[k + 1], x1));
+        a = DADD(a, DMUL(x2, x2)); b = DADD(b, DMUL(ubuf[k + 2], x2));
+        a = DADD(a, DMUL(x3, x3)); b = DADD(b, DMUL(ubuf[k + 3], x3));
+    }
+    for (; k < K; ++k) {
+        double x = (double)row[k];
+        a = DADD(a, DMUL(x, x));
+        b = DADD(b, DMUL(ubuf[k], x));
+    }
+    tt = a;
+    st = b;
+}
+
+__global__ void __launch_bounds__(kExactThreads, 1)
+    exact_kernel(float *__restrict__ S, float *__restrict__ T, const int32_t *__restrict__ users,
+                 const int32_t *__restrict__ items, int64_t start, int64_t stop, int K, int N,
+                 int cosine, double lr, double l2, double mu, double theta, uint64_t s0,
+                 FastMod fm, heat_counters *ctr, float *__restrict__ snap) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ExactSmem &sh = *reinterpret_cast<ExactSmem *>(smem_raw);
+    double *ubuf = reinterpret_cast<double *>(smem_raw + sizeof(ExactSmem) + 16 -
+                                              (sizeof(ExactSmem) % 16));
+    double *tts = ubuf + K;
+    double *sts = tts + N;
+    double *sims = sts + N;
+    float *pos_buf = reinterpret_cast<float *>(sims + N);
+    int32_t *nids = reinterpret_cast<int32_t *>(pos_buf + K);
+    int32_t *list = nids + N;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const double inv_n = DDIV(1.0, (double)N);  // trainer.py:113
+    const double dneg_w = DMUL(mu, inv_n);      // trainer.py:219
+    const double dpos = -1.0;                   // trainer.py:223
+    double loss_acc = 0.0;
+    if (tid == 0) loss_acc = ctr->loss;
+    long long degen = 0, active = 0;
+
+    for (int64_t p = start; p < stop; ++p) {
+        const int64_t u = users[p];
+        const int64_t pos = items[p];
+        // ---- read (trainer.py:121-142): S[u] -> f64, T[pos] snapshot, ids
+        for (int k = tid; k < K; k += kExactThreads) {
+            ubuf[k] = (double)S[u * K + k];
+            pos_buf[k] = T[pos * K + k];
+        }
+        for (int j = tid; j < N; j += kExactThreads) nids[j] = neg_id(s0, p, N, j, fm);
+        __syncthreads();
+
+        // ---- similarity (trainer.py:176-207)
+        if (tid == kExactThreads - 1) {
+            double ss = 0.0;
+            for (int k = 0; k < K; ++k) ss = DADD(ss, DMUL(ubuf[k], ubuf[k]));
+            sh.ss = ss;
+        }
+        for (int r = tid; r <= N; r += kExactThreads) {
+            double tt, st;
+            if (r == 0) {
+                // pos row from the snapshot (trainer.py:181-183)
+                double a = 0.0, b = 0.0;
+                for (int k = 0; k < K; ++k) {
+                    double x = (double)pos_buf[k];
+                    a = DADD(a, DMUL(x, x));
+                    b = DADD(b, DMUL(ubuf[k], x));
+                }
+                sh.tt_p = a;
+                sh.st_p = b;
+            } else {
+                row_dots(T + (int64_t)nids[r - 1] * K, ubuf, K, tt, st);
+                tts[r - 1] = tt;
+                sts[r - 1] = st;
+            }
+        }
+        __syncthreads();
+        const double ss = sh.ss;
+        for (int r = tid; r <= N; r += kExactThreads) {
+            double tt = r == 0 ? sh.tt_p : tts[r - 1];
+            double st = r == 0 ? sh.st_p : sts[r - 1];
+            double sim;
+            if (cosine) {
+                if (ss <= 0.0 || tt <= 0.0) {
+                    sim = 0.0;
+                    ++degen;
+                } else {
+                    sim = DDIV(st, DMUL(DSQRT(ss), DSQRT(tt)));
+                }
+            } else {
+                sim = st;
+            }
+            if (r == 0) sh.sim_p = sim; else sims[r - 1] = sim;
+        }
+        __syncthreads();
+
+        // ---- loss (trainer.py:214-222): ordered list of j with d > 0
+        int base = 0;
+        for (int j0 = 0; j0 < N; j0 += kExactThreads) {
+            int j = j0 + tid;
+            bool act = j < N && DSUB(sims[j], theta) > 0.0;
+            unsigned m = __ballot_sync(0xffffffffu, act);
+            if (lane == 0) sh.warp_cnt[warp] = __popc(m);
+            __syncthreads();
+            int off = base;
+            int total = 0;
+            for (int w = 0; w < kExactWarps; ++w) {
+                int c = sh.warp_cnt[w];
+                if (w < warp) off += c;
+                total += c;
+            }
+            if (act) list[off + __popc(m & ((1u << lane) - 1u))] = j;
+            base += total;
+            __syncthreads();
+        }
+        const int n_loss = base;  // identical in every thread
+        if (tid == 0) {
+            double hinge = 0.0;
+            for (int a = 0; a < n_loss; ++a) hinge = DADD(hinge, DSUB(sims[list[a]], theta));
+            double pl = DADD(DSUB(1.0, sh.sim_p), DMUL(dneg_w, hinge));
+            loss_acc = DADD(loss_acc, pl);
+            if (dneg_w != 0.0) active += n_loss;
+        }
+        // negatives with dnegs[j] != 0 (trainer.py:219: dneg = mu*inv_n)
+        const int n_upd = dneg_w != 0.0 ? n_loss : 0;
+
+        // ---- gradient + update, thread k owns column k
+        const double tt_p = sh.tt_p, st_p = sh.st_p;
+        const double rs = ss > 0.0 ? DSQRT(ss) : 0.0;
+        for (int k = tid; k < K; k += kExactThreads) {
+            const double ub = ubuf[k];
+            const double pk = (double)pos_buf[k];
+            double ug = 0.0;
+            if (cosine) {
+                if (ss > 0.0 && tt_p > 0.0) {
+                    double denom = DMUL(DMUL(ss, rs), DSQRT(tt_p));
+                    ug = DADD(ug, DDIV(DMUL(dpos, DSUB(DMUL(pk, ss), DMUL(st_p, ub))), denom));
+                }
+                for (int a = 0; a < n_upd; ++a) {
+                    const int j = list[a];
+                    const float v = T[(int64_t)nids[j] * K + k];
+                    snap[(int64_t)a * K + k] = v;
+                    const double tj = tts[j];
+                    if (ss > 0.0 && tj > 0.0) {
+                        double denom = DMUL(DMUL(ss, rs), DSQRT(tj));
+                        ug = DADD(ug, DDIV(DMUL(dneg_w, DSUB(DMUL((double)v, ss),
+                                                             DMUL(sts[j], ub))), denom));
+                    }
+                }
+            } else {
+                ug = DADD(ug, DMUL(dpos, pk));
+                for (int a = 0; a < n_upd; ++a) {
+                    const float v = T[(int64_t)nids[list[a]] * K + k];
+                    snap[(int64_t)a * K + k] = v;
+                    ug = DADD(ug, DMUL(dneg_w, (double)v));
+                }
+            }
+            // T[pos] (trainer.py:259-271)
+            float *tp = T + pos * K + k;
+            if (cosine) {
+                if (ss > 0.0 && tt_p > 0.0) {
+                    double denom = DMUL(DMUL(tt_p, DSQRT(tt_p)), rs);
+                    double g = DDIV(DMUL(dpos, DSUB(DMUL(ub, tt_p), DMUL(st_p, pk))), denom);
+                    double t = (double)*tp;
+                    *tp = __double2float_rn(DSUB(t, DMUL(lr, DADD(g, DMUL(l2, t)))));
+                } else if (l2 != 0.0) {
+                    double t = (double)*tp;
+                    *tp = __double2float_rn(DSUB(t, DMUL(DMUL(lr, l2), t)));
+                }
+            } else {
+                double g = DMUL(dpos, ub);
+                double t = (double)*tp;
+                *tp = __double2float_rn(DSUB(t, DMUL(lr, DADD(g, DMUL(l2, t)))));
+            }
+            // T[neg_j] in j order (trainer.py:272-290)
+            if (l2 == 0.0) {
+                for (int a = 0; a < n_upd; ++a) {
+                    const int j = list[a];
+                    float *tn = T + (int64_t)nids[j] * K + k;
+                    const double vs = (double)snap[(int64_t)a * K + k];
+                    double g;
+                    if (cosine) {
+                        const double tj = tts[j];
+                        if (!(ss > 0.0 && tj > 0.0)) continue;
+                        double denom = DMUL(DMUL(tj, DSQRT(tj)), rs);
+                        g = DDIV(DMUL(dneg_w, DSUB(DMUL(ub, tj), DMUL(sts[j], vs))), denom);
+                    } else {
+                        g = DMUL(dneg_w, ub);
+                    }
+                    double t = (double)*tn;
+                    *tn = __double2float_rn(DSUB(t, DMUL(lr, DADD(g, DMUL(l2, t)))));
+                }
+            } else {
+                int a = 0;
+                for (int j = 0; j < N; ++j) {
+                    float *tn = T + (int64_t)nids[j] * K + k;
+                    double t = (double)*tn;
+                    if (a < n_upd && list[a] == j) {
+                        const double vs = (double)snap[(int64_t)a * K + k];
+                        ++a;
+                        double g;
+                        if (cosine) {
+                            const double tj = tts[j];
+                            if (!(ss > 0.0 && tj > 0.0)) continue;
+                            double denom = DMUL(DMUL(tj, DSQRT(tj)), rs);
+                            g = DDIV(DMUL(dneg_w, DSUB(DMUL(ub, tj), DMUL(sts[j], vs))), denom);
+                        } else {
+                            g = DMUL(dneg_w, ub);
+                        }
+                        *tn = __double2float_rn(DSUB(t, DMUL(lr, DADD(g, DMUL(l2, t)))));
+                    } else {
+                        *tn = __double2float_rn(DSUB(t, DMUL(DMUL(lr, l2), t)));
+                    }
+                }
+            }
+            // S[u] (trainer.py:291-293)
+            float *su = S + u * K + k;
+            double s = (double)*su;
+            *su = __double2float_rn(DSUB(s, DMUL(lr, DADD(ug, DMUL(l2, s)))));
+        }
+        __syncthreads();
+    }
+    // telemetry (order-free integer sums)
+    for (int o = 16; o > 0; o >>= 1) degen += __shfl_xor_sync(0xffffffffu, degen, o);
+    if (lane == 0 && degen) atomicAdd((unsigned long long *)&ctr->degenerate, (unsigned long long)degen);
+    if (tid == 0) {
+        ctr->loss = loss_acc;
+        atomicAdd((unsigned long long *)&ctr->active, (unsigned long long)active);
+        atomicAdd((unsigned long long *)&ctr->pairs, (unsigned long long)(stop - start));
+    }
+}
+
+size_t exact_smem_bytes(int K, int N) {
+    size_t head = sizeof(ExactSmem) + 16 - (sizeof(ExactSmem) % 16);
+    return head + (size_t)K * 8 + (size_t)N * 8 * 3 + (size_t)K * 4 + (size_t)N * 4 * 2 + 16;
+}
+
+cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t *items,
+                         int64_t start, int64_t stop, int K, int N, int cosine, double lr,
+                         double l2, double mu, double theta, uint64_t s0, int64_t num_items,
+                         heat_counters *ctr, float *snap, cudaStream_t stream) {
+    size_t smem = exact_smem_bytes(K, N);
+    cudaError_t e = cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    exact_kernel<<<1, kExactThreads, smem, stream>>>(S, T, users, items, start, stop, K, N,
+                                                     cosine, lr, l2, mu, theta, s0,
+                                                     FastMod::make((uint64_t)num_items), ctr, snap);
+    return cudaGetLastError();
+}
+
+}  // namespace heat

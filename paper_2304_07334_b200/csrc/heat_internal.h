@@ -1,0 +1,59 @@
+// heat_internal.h — launchers shared between the kernel TUs and heat_capi.cu.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/heat_b200.h"
+
+namespace heat {
+
+size_t exact_smem_bytes(int K, int N);
+
+cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t *items,
+                         int64_t start, int64_t stop, int K, int N, int cosine, double lr,
+                         double l2, double mu, double theta, uint64_t s0, int64_t num_items,
+                         heat_counters *ctr, float *snap, cudaStream_t stream);
+
+struct HogwildArgs {
+    float *S;
+    float *T;
+    const int32_t *users;
+    const int32_t *items;
+    int64_t start, stop;
+    int K, N, cosine;
+    float lr, l2;
+    double mu, theta;
+    uint64_t s0;
+    int64_t num_items;
+    heat_counters *ctr;
+    int window;
+    int fp64;
+    // delta mode (multi-GPU): item updates logged instead of applied
+    int32_t *delta_ids;
+    float *delta_rows;
+    int64_t *delta_count;
+    int64_t delta_capacity;
+};
+
+cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
+
+cudaError_t launch_sample(uint64_t s0, int64_t first_pair, int64_t npairs, int N,
+                          int64_t num_items, int32_t *out, cudaStream_t stream);
+
+cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows, int K,
+                        const int32_t *users, int64_t n_users, const int64_t *tr_offsets,
+                        const int32_t *tr_items, int64_t tr_num_users, const int64_t *te_offsets,
+                        const int32_t *te_items, int k, int cosine, const double *dcg_w,
+                        const double *idcg, int32_t *topk, double *recall, double *ndcg,
+                        cudaStream_t stream);
+
+cudaError_t launch_apply_deltas(float *T, int64_t t_rows, int K, const int32_t *ids,
+                                const float *rows, const int64_t *count, int64_t capacity,
+                                int ordered, cudaStream_t stream);
+
+int sm_count();
+size_t eval_max_k_supported(int K);
+
+}  // namespace heat

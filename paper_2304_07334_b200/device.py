@@ -1,0 +1,129 @@
+"""Device-resident model state and the calls into libheat_b200.so.
+
+``DeviceModel`` owns device copies of the user table S and item table T
+(float32, row-major, exactly the host layout of embeddings.py:40-61) and the
+per-epoch pair order; it is the unit the drop-in ``train_epoch`` uses for one
+call and that multi-epoch callers keep alive across epochs (no per-epoch
+host round trip).  torch provides device memory and the stream; every byte
+of compute happens in the CUDA kernels of csrc/ reached through the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .rng import epoch_stream
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2304_07334_b200 needs a CUDA device (no CPU fallback)")
+    N.lib()  # fail loudly if the native library is missing
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _p(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(dev: torch.device):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+@dataclass
+class CounterValues:
+    loss: float
+    degenerate: int
+    active: int
+    pairs: int
+
+
+class DeviceCounters:
+    """The 32-byte heat_counters struct in device memory."""
+
+    def __init__(self, dev: torch.device):
+        self.buf = torch.zeros(N.COUNTERS_BYTES, dtype=torch.uint8, device=dev)
+
+    def reset(self, loss: float = 0.0) -> None:
+        host = np.zeros(N.COUNTERS_BYTES, dtype=np.uint8)
+        host[:8] = np.frombuffer(np.float64(loss).tobytes(), dtype=np.uint8)
+        self.buf.copy_(torch.from_numpy(host))
+
+    def read(self) -> CounterValues:
+        h = self.buf.cpu().numpy()
+        loss = float(h[:8].view(np.float64)[0])
+        ints = h[8:32].view(np.int64)
+        return CounterValues(loss, int(ints[0]), int(ints[1]), int(ints[2]))
+
+    def ptr(self):
+        return _p(self.buf)
+
+
+class DeviceModel:
+    """Device copies of S and T plus the state of an epoch in flight."""
+
+    def __init__(self, S: np.ndarray, T: np.ndarray, device=None):
+        self.device = require_cuda(device)
+        if S.dtype != np.float32 or T.dtype != np.float32:
+            raise ValueError("embedding tables must be float32")
+        if S.ndim != 2 or T.ndim != 2 or S.shape[1] != T.shape[1]:
+            raise ValueError(f"table shapes {S.shape} / {T.shape} do not share a dim")
+        self.dim = int(S.shape[1])
+        self.S = torch.from_numpy(np.ascontiguousarray(S)).to(self.device)
+        self.T = torch.from_numpy(np.ascontiguousarray(T)).to(self.device)
+        self.counters = DeviceCounters(self.device)
+        self._scratch = None
+
+    # -- host sync --------------------------------------------------------
+    def download(self, S_out: np.ndarray, T_out: np.ndarray) -> None:
+        """Write device tables back into the caller's arrays in place."""
+        torch.from_numpy(S_out).copy_(self.S)
+        torch.from_numpy(T_out).copy_(self.T)
+
+    def upload(self, S: np.ndarray, T: np.ndarray) -> None:
+        self.S.copy_(torch.from_numpy(np.ascontiguousarray(S)))
+        self.T.copy_(torch.from_numpy(np.ascontiguousarray(T)))
+
+    def upload_pairs(self, ep_users: np.ndarray, ep_items: np.ndarray):
+        u = torch.from_numpy(np.ascontiguousarray(ep_users, dtype=np.int32)).to(self.device)
+        i = torch.from_numpy(np.ascontiguousarray(ep_items, dtype=np.int32)).to(self.device)
+        return u, i
+
+    # -- training ---------------------------------------------------------
+    def scratch(self, n_neg: int) -> torch.Tensor:
+        need = int(N.lib().heat_scratch_bytes(n_neg, self.dim))
+        if self._scratch is None or self._scratch.numel() < need:
+            self._scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._scratch
+
+    def params(self, *, n_neg: int, lr: float, l2: float, mu: float, theta: float,
+               cosine: bool, mode: int, stream_base: int, window: int = 0,
+               fp64: bool = False) -> N.SgdParams:
+        return N.SgdParams(dim=self.dim, n_neg=n_neg, use_cosine=int(bool(cosine)), mode=mode,
+                           lr=lr, l2=l2, mu=mu, theta=theta, stream_base=stream_base,
+                           window=window, flags=1 if fp64 else 0)
+
+    def train_range(self, users: torch.Tensor, items: torch.Tensor, start: int, stop: int,
+                    params: N.SgdParams, delta=None) -> None:
+        """Launch pairs [start, stop) on the current stream (asynchronous)."""
+        scratch = self.scratch(params.n_neg) if params.mode == N.MODE_EXACT else None
+        d_ids = d_rows = d_cnt = None
+        cap = 0
+        if delta is not None:
+            d_ids, d_rows, d_cnt, cap = delta
+        rc = N.lib().heat_train_range(
+            _p(self.S), self.S.shape[0], _p(self.T), self.T.shape[0], _p(users), _p(items),
+            start, stop, ctypes.byref(params), self.counters.ptr(), _p(d_ids), _p(d_rows),
+            _p(d_cnt), cap, _p(scratch), _stream(self.device))
+        N.check(rc)
+
+
+def stream_base(seed: int, epoch: int) -> int:
+    return epoch_stream(seed, epoch)

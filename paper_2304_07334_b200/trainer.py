@@ -1,0 +1,224 @@
+"""Drop-in ``train_epoch`` / ``train`` running on the B200.
+
+Signature, validation order, report fields and error types follow
+/root/reference/pkg/src/heatcf/trainer.py:385-466 (``train_epoch``) and
+480-533 (``train``).  The epoch's pair order comes from the same
+``epoch_pairs`` call (trainer.py:390-392); the pairs are then trained by the
+CUDA kernels of csrc/ through the C ABI:
+
+- ``num_threads == 1`` (the reference's deterministic mode) runs the EXACT
+  kernel: pairs strictly in order, bit-identical S, T and loss to the
+  reference (tests/test_gpu_parity.py);
+- ``num_threads > 1`` (the reference's Hogwild mode) runs the throughput
+  kernel: up to ``window`` pairs in flight with lock-free atomic row updates.
+
+``configure(mode=…, window=…)`` or the env vars ``HEAT_B200_MODE``
+(``exact`` | ``hogwild``) and ``HEAT_B200_WINDOW`` override the mapping.
+The tiling sampler and the aggregator are outside the built path and raise
+ValueError (no CPU fallback).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .dataset import epoch_pairs
+from .device import DeviceModel
+from .rng import epoch_stream, shuffle_seed
+
+PHASE_NAMES = ("read_emb", "similarity", "loss", "gradient", "update", "aggregate")
+
+
+@dataclass
+class EpochReport:
+    """trainer.py:90-100."""
+
+    epoch: int
+    mean_loss: float
+    wall_time: float
+    phase_times: dict[str, float]
+    degenerate_count: int
+    num_pairs: int
+    num_threads: int
+    active_negatives: int = 0
+
+
+@dataclass
+class TrainResult:
+    reports: list
+    evaluations: list
+    final_metrics: object
+    best_recall: float
+    best_epoch: int
+
+
+@dataclass
+class GpuOptions:
+    mode: str | None = None  # None: exact when num_threads == 1, else hogwild
+    window: int = 0          # hogwild: pairs in flight (0 = the GPU's capacity)
+    fp64: bool = False       # hogwild: binary64 dot products
+    device: object = None
+
+
+_OPTIONS = GpuOptions(
+    mode=os.environ.get("HEAT_B200_MODE") or None,
+    window=int(os.environ.get("HEAT_B200_WINDOW", "0") or 0),
+)
+
+
+def configure(**kw) -> GpuOptions:
+    """Set process-wide GPU options (mode, window, fp64, device)."""
+    for k, v in kw.items():
+        if not hasattr(_OPTIONS, k):
+            raise TypeError(f"unknown option {k!r}")
+        setattr(_OPTIONS, k, v)
+    if _OPTIONS.mode not in (None, "exact", "hogwild"):
+        raise ValueError(f"unknown mode {_OPTIONS.mode!r}")
+    return _OPTIONS
+
+
+def options() -> GpuOptions:
+    return _OPTIONS
+
+
+def _check_shapes(S, T, train, cfg, weights) -> None:
+    """trainer.py:366-382, before any mutation."""
+    if S.dim != cfg.emb_dim or T.dim != cfg.emb_dim:
+        raise ValueError(
+            f"matrix dims ({S.dim}, {T.dim}) do not match config emb_dim {cfg.emb_dim}")
+    if S.rows < train.num_users:
+        raise ValueError(f"user matrix has {S.rows} rows for {train.num_users} users")
+    if T.rows < train.num_items:
+        raise ValueError(f"item matrix has {T.rows} rows for {train.num_items} items")
+    if cfg.aggregator.enabled:
+        if weights is None:
+            raise ValueError("aggregator enabled but no weight matrix given")
+        if np.shape(weights) != (cfg.emb_dim, cfg.emb_dim):
+            raise ValueError(
+                f"aggregator weights shape {np.shape(weights)} != ({cfg.emb_dim}, {cfg.emb_dim})")
+
+
+def _check_supported(cfg) -> None:
+    if cfg.sampler.kind != "uniform":
+        raise ValueError("the B200 path implements the uniform sampler only "
+                         f"(got {cfg.sampler.kind!r}); no CPU fallback")
+    if cfg.aggregator.enabled:
+        raise ValueError("the B200 path does not implement the behaviour aggregator; "
+                         "no CPU fallback")
+
+
+def resolve_mode(cfg) -> int:
+    mode = _OPTIONS.mode or ("exact" if cfg.num_threads == 1 else "hogwild")
+    return N.MODE_EXACT if mode == "exact" else N.MODE_HOGWILD
+
+
+def sgd_params(model: DeviceModel, cfg, epoch: int, mode: int) -> N.SgdParams:
+    return model.params(n_neg=cfg.num_negatives, lr=cfg.learning_rate, l2=cfg.l2_reg,
+                        mu=cfg.loss.mu, theta=cfg.loss.theta, cosine=cfg.similarity == "cosine",
+                        mode=mode, stream_base=epoch_stream(cfg.seed, epoch),
+                        window=_OPTIONS.window, fp64=_OPTIONS.fp64)
+
+
+def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int | None = None,
+                        pairs=None) -> tuple[EpochReport, dict]:
+    """One epoch on device-resident tables; no table transfer."""
+    if mode is None:
+        mode = resolve_mode(cfg)
+    t0 = time.perf_counter()
+    if pairs is None:
+        ep_users, ep_items = epoch_pairs(train, shuffle_seed(cfg.seed, epoch))
+        pairs = model.upload_pairs(ep_users, ep_items)
+    du, di = pairs
+    npairs = int(du.shape[0])
+    model.counters.reset()
+    params = sgd_params(model, cfg, epoch, mode)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    model.train_range(du, di, 0, npairs, params)
+    ev1.record()
+    c = model.counters.read()  # synchronises
+    wall = time.perf_counter() - t0
+    rep = EpochReport(epoch=epoch, mean_loss=c.loss / npairs, wall_time=wall,
+                      phase_times={n: 0.0 for n in PHASE_NAMES}, degenerate_count=c.degenerate,
+                      num_pairs=npairs, num_threads=cfg.num_threads, active_negatives=c.active)
+    return rep, {"kernel_s": ev0.elapsed_time(ev1) / 1e3}
+
+
+def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
+                collect_phases: bool = False) -> EpochReport:
+    """Drop-in for heatcf.trainer.train_epoch (trainer.py:385-466).
+
+    S.values / T.values are updated in place, like the reference.  With
+    collect_phases the phase dict carries measured device times: read_emb =
+    host->device upload, similarity = the fused kernel (read, similarity,
+    loss, gradient and update are one pass), update = device->host write-back.
+    """
+    _check_shapes(S, T, train, cfg, weights)
+    _check_supported(cfg)
+    t_start = time.perf_counter()
+    ep_users, ep_items = epoch_pairs(train, shuffle_seed(cfg.seed, epoch))
+    t_up = time.perf_counter()
+    model = DeviceModel(S.values, T.values, _OPTIONS.device)
+    pairs = model.upload_pairs(ep_users, ep_items)
+    torch.cuda.current_stream(model.device).synchronize()
+    t_run = time.perf_counter()
+    rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=pairs)
+    t_down = time.perf_counter()
+    model.download(S.values, T.values)
+    t_end = time.perf_counter()
+    rep.wall_time = t_end - t_start
+    if collect_phases:
+        rep.phase_times["read_emb"] = t_run - t_up
+        rep.phase_times["similarity"] = timing["kernel_s"]
+        rep.phase_times["update"] = t_end - t_down
+    return rep
+
+
+def train(S, T, train_set, test_set, cfg, weights=None, *, eval_interval: int = 0, k: int = 20,
+          out_dir: str | None = None, on_epoch=None, on_eval=None) -> TrainResult:
+    """trainer.py:480-533 with the tables kept on the device between epochs."""
+    from .embeddings import save_model
+    from .evaluator import evaluate_device
+
+    _check_shapes(S, T, train_set, cfg, weights)
+    _check_supported(cfg)
+    reports: list = []
+    evaluations: list = []
+    best = {"recall": -1.0, "epoch": -1}
+    model = DeviceModel(S.values, T.values, _OPTIONS.device)
+
+    def run_eval(epoch: int):
+        metrics = evaluate_device(model, S, T, train_set, test_set, cfg, k=k)
+        evaluations.append((epoch, metrics))
+        if on_eval is not None:
+            on_eval(epoch, metrics)
+        if metrics.recall_at_k > best["recall"]:
+            best["recall"] = metrics.recall_at_k
+            best["epoch"] = epoch
+            if out_dir is not None:
+                model.download(S.values, T.values)
+                save_model(f"{out_dir}/best.ckpt", S, T, None)
+        return metrics
+
+    for epoch in range(cfg.epochs):
+        t0 = time.perf_counter()
+        rep, _ = run_epoch_on_device(model, train_set, cfg, epoch)
+        rep.wall_time = time.perf_counter() - t0
+        reports.append(rep)
+        if on_epoch is not None:
+            on_epoch(rep)
+        if eval_interval and (epoch + 1) % eval_interval == 0:
+            run_eval(epoch + 1)
+    final = run_eval(cfg.epochs)
+    model.download(S.values, T.values)
+    if out_dir is not None:
+        save_model(f"{out_dir}/final.ckpt", S, T, None)
+    return TrainResult(reports=reports, evaluations=evaluations, final_metrics=final,
+                       best_recall=best["recall"], best_epoch=best["epoch"])

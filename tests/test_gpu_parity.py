@@ -1,0 +1,340 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference-generated golden vectors.
+
+Bit-exact targets: negative ids (always), S/T/loss in EXACT mode.  Hogwild
+mode is checked statistically (recall@20 / loss) like the reference's own
+thread-count parity test (test_trainer.py:199-208).
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2304_07334_b200 import _native
+    _native.lib()
+    return torch
+
+
+def _dev_pairs(model, u, i):
+    return model.upload_pairs(u, i)
+
+
+def _neg_ids_device(torch_cuda, s0, first, npairs, n_neg, num_items):
+    import ctypes
+    from paper_2304_07334_b200 import _native as N
+    out = torch_cuda.empty(npairs * n_neg, dtype=torch_cuda.int32, device="cuda")
+    rc = N.lib().heat_sample_negatives(s0, first, npairs, n_neg, num_items,
+                                       ctypes.c_void_p(out.data_ptr()), None)
+    N.check(rc)
+    return out.cpu().numpy().reshape(npairs, n_neg)
+
+
+def _counter_draws_np(s0, first, npairs, n_neg, num_items):
+    n = (np.arange(first * n_neg, (first + npairs) * n_neg, dtype=np.uint64) + np.uint64(1))
+    with np.errstate(over="ignore"):
+        z = np.uint64(s0) + n * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z % np.uint64(num_items)).astype(np.int64).reshape(npairs, n_neg)
+
+
+def test_sampler_matches_reference_stream(torch_cuda):
+    from paper_2304_07334_b200.rng import epoch_stream
+    z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
+    s0 = epoch_stream(0, 0)
+    got = _neg_ids_device(torch_cuda, s0, 0, 64, 10, 2000)
+    assert np.array_equal(got, z["negs_e0"])
+    with open(os.path.join(GOLDEN, "rng.json")) as f:
+        g = json.load(f)
+    assert got.ravel()[:1000].tolist() == g["below2000_epoch0"][:640]
+
+
+@pytest.mark.parametrize("num_items", [1, 2, 3, 2000, 92000, 2_000_000, 2**31 - 1, 1 << 30])
+def test_sampler_fast_mod_exact(torch_cuda, num_items):
+    s0 = 0x0123456789ABCDEF
+    for first in (0, 123_456_789):
+        got = _neg_ids_device(torch_cuda, s0, first, 4096, 37, num_items)
+        want = _counter_draws_np(s0, first, 4096, 37, num_items)
+        assert np.array_equal(got, want)
+
+
+def _run_exact_steps(model, users, items, B, params, loss0=0.0):
+    from paper_2304_07334_b200.device import DeviceCounters  # noqa: F401
+    du, di = model.upload_pairs(users, items)
+    model.counters.reset(loss0)
+    n = len(users)
+    losses = []
+    for s in range(0, n, B):
+        model.train_range(du, di, s, min(n, s + B), params)
+        losses.append(model.counters.read().loss)
+    return losses
+
+
+def test_exact_c1_two_epochs_bit_exact(torch_cuda):
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
+    train, _, _ = make_dataset("c1")
+    S = init_matrix(1000, 32, InitSpec(seed=0)).values
+    T = init_matrix(2000, 32, InitSpec(seed=0)).values
+    model = DeviceModel(S, T)
+    for e in range(2):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        p = model.params(n_neg=10, lr=1e-3, l2=0.0, mu=10.0, theta=0.5, cosine=True,
+                         mode=N.MODE_EXACT, stream_base=epoch_stream(0, e))
+        losses = _run_exact_steps(model, u, i, 256, p)
+        assert np.array_equal(np.array(losses), z[f"step_loss_e{e}"]), e
+        model.download(S, T)
+        assert S.tobytes() == z[f"S_e{e}"].tobytes()
+        assert T.tobytes() == z[f"T_e{e}"].tobytes()
+    c = model.counters.read()
+    assert c.loss / len(u) == z["mean_loss"][1]
+
+
+def test_exact_edge_cases_bit_exact(torch_cuda):
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import InteractionSet, epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    z = np.load(os.path.join(GOLDEN, "edge_cases.npz"))
+    for name in z["names"]:
+        g = {k.split("/", 1)[1]: z[k] for k in z.files if k.startswith(f"{name}/")}
+        S, T = g["S0"].copy(), g["T0"].copy()
+        train = InteractionSet(int(g["nu"]), int(g["ni"]), g["offsets"], g["items"])
+        model = DeviceModel(S, T)
+        for e in range(int(g["epochs"])):
+            u, i = epoch_pairs(train, shuffle_seed(int(g["seed"]), e))
+            p = model.params(n_neg=int(g["N"]), lr=float(g["lr"]), l2=float(g["l2"]),
+                             mu=float(g["mu"]), theta=float(g["theta"]), cosine=bool(g["cosine"]),
+                             mode=N.MODE_EXACT, stream_base=epoch_stream(int(g["seed"]), e))
+            losses = _run_exact_steps(model, u, i, 7, p)
+            assert losses[-1] / len(u) == g["mean_loss"][e], name
+        model.download(S, T)
+        assert S.tobytes() == g["S"].tobytes(), name
+        assert T.tobytes() == g["T"].tobytes(), name
+
+
+def test_exact_c2_prefix_bit_exact(torch_cuda):
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    with open(os.path.join(GOLDEN, "c2_prefix.json")) as f:
+        g = json.load(f)
+    train, _, _ = make_dataset("c2")
+    S = init_matrix(train.num_users, 64, InitSpec(seed=0)).values
+    T = init_matrix(train.num_items, 64, InitSpec(seed=0)).values
+    u, i = epoch_pairs(train, shuffle_seed(0, 0))
+    B, steps = g["B"], g["steps"]
+    u, i = u[:B * steps], i[:B * steps]
+    model = DeviceModel(S, T)
+    du, di = model.upload_pairs(u, i)
+    p = model.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                     mode=N.MODE_EXACT, stream_base=epoch_stream(0, 0))
+    model.counters.reset()
+    for s in range(steps):
+        model.train_range(du, di, s * B, (s + 1) * B, p)
+        c = model.counters.read()
+        assert c.loss == g["loss"][s]
+        assert c.degenerate == g["degen"][s]
+        model.download(S, T)
+        assert hashlib.sha256(S.tobytes()).hexdigest() == g["S_sha256"][s]
+        assert hashlib.sha256(T.tobytes()).hexdigest() == g["T_sha256"][s]
+
+
+@pytest.mark.parametrize("K,N,cos,l2,theta", [(1, 3, True, 0.0, -0.5), (3, 7, True, 0.05, 0.0),
+                                              (8, 33, False, 0.01, 0.3), (33, 600, True, 0.0, 0.2),
+                                              (130, 64, True, 0.02, -1.0), (64, 100, True, 0.0, 0.9)])
+def test_exact_matches_oracle_random(torch_cuda, K, N, cos, l2, theta):
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.device import DeviceModel
+    rng = np.random.default_rng(K * 1000 + N)
+    nu, ni, P = 50, 300, 2000
+    S = (rng.standard_normal((nu, K)) * 0.1).astype(np.float32)
+    T = (rng.standard_normal((ni, K)) * 0.1).astype(np.float32)
+    S[3] = 0.0
+    T[7] = 0.0
+    u = rng.integers(0, nu, P).astype(np.int32)
+    i = rng.integers(0, ni, P).astype(np.int32)
+    s0 = 0xDEADBEEF12345678
+    S2, T2 = S.copy(), T.copy()
+    r = O.train_range(S2, T2, u, i, 0, P, s0, n_neg=N, lr=0.05, l2=l2, mu=2.0, theta=theta,
+                      cosine=cos)
+    model = DeviceModel(S, T)
+    du, di = model.upload_pairs(u, i)
+    p = model.params(n_neg=N, lr=0.05, l2=l2, mu=2.0, theta=theta, cosine=cos,
+                     mode=NN.MODE_EXACT, stream_base=s0)
+    model.counters.reset()
+    model.train_range(du, di, 0, P, p)
+    c = model.counters.read()
+    model.download(S, T)
+    assert S.tobytes() == S2.tobytes()
+    assert T.tobytes() == T2.tobytes()
+    assert c.loss == r.loss and c.degenerate == r.degenerate and c.active == r.active
+
+
+def test_train_epoch_api_exact_equals_reference(torch_cuda):
+    from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
+    from paper_2304_07334_b200.synth import make_dataset
+    from paper_2304_07334_b200.trainer import train_epoch
+    z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
+    train, _, _ = make_dataset("c1")
+    cfg = TrainingConfig(emb_dim=32, num_negatives=10, learning_rate=1e-3, num_threads=1,
+                         loss=LossParams(mu=10.0, theta=0.5), seed=0)
+    S = init_matrix(1000, 32, InitSpec(seed=0))
+    T = init_matrix(2000, 32, InitSpec(seed=0))
+    for e in range(2):
+        rep = train_epoch(S, T, train, cfg, epoch=e, collect_phases=True)
+        assert rep.mean_loss == z["mean_loss"][e]
+        assert rep.num_pairs == 20000 and rep.num_threads == 1
+        assert rep.phase_times["read_emb"] > 0
+        assert sum(rep.phase_times.values()) <= rep.wall_time
+    assert S.values.tobytes() == z["S_e1"].tobytes()
+    assert T.values.tobytes() == z["T_e1"].tobytes()
+
+
+def test_hogwild_descends_and_matches_oracle_quality(torch_cuda):
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
+    from paper_2304_07334_b200.evaluator import evaluate
+    from paper_2304_07334_b200.synth import make_clustered
+    from paper_2304_07334_b200.trainer import configure, train_epoch
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.rng import shuffle_seed
+    train, test = make_clustered(800, 1600, 16, 40, affinity=0.97, seed=11)
+    cfg = TrainingConfig(emb_dim=32, num_negatives=16, learning_rate=0.05, num_threads=8,
+                         loss=LossParams(mu=1.0, theta=0.8), seed=7)
+    S = init_matrix(800, 32, InitSpec(seed=1))
+    T = init_matrix(1600, 32, InitSpec(seed=2))
+    So, To = S.values.copy(), T.values.copy()
+    losses = []
+    configure(mode="hogwild", window=256)
+    try:
+        for e in range(25):
+            losses.append(train_epoch(S, T, train, cfg, epoch=e).mean_loss)
+    finally:
+        configure(mode=None, window=0)
+    assert np.isfinite(losses).all() and losses[-1] < losses[0]
+    m_gpu = evaluate(S, T, train, test, cfg, k=20)
+    for e in range(25):
+        u, i = epoch_pairs(train, shuffle_seed(7, e))
+        O.train_range(So, To, u, i, 0, len(u), O.derive_stream(7, 0x45504F43, e, 0),
+                      n_neg=16, lr=0.05, mu=1.0, theta=0.8)
+    rec_ref, _, _ = O.evaluate_ref(So, To, train.offsets, train.items, 800, test.offsets,
+                                   test.items, 800, k=20)
+    assert abs(m_gpu.recall_at_k - rec_ref) <= 0.01, (m_gpu.recall_at_k, rec_ref)
+
+
+def test_eval_matches_reference_golden(torch_cuda):
+    from paper_2304_07334_b200.dataset import InteractionSet
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.evaluator import eval_users_device, evaluate
+    from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+    from paper_2304_07334_b200.config import TrainingConfig
+    z = np.load(os.path.join(GOLDEN, "eval.npz"))
+    c1 = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
+    S, T = EmbeddingMatrix(c1["S_e1"]), EmbeddingMatrix(c1["T_e1"])
+    tr = InteractionSet(1000, 2000, z["tr_offsets"], z["tr_items"])
+    te = InteractionSet(1000, 2000, z["te_offsets"], z["te_items"])
+    for sim in ("cosine", "dot"):
+        cfg = TrainingConfig(emb_dim=32, num_negatives=1, similarity=sim)
+        for k in (20, 5):
+            m = evaluate(S, T, tr, te, cfg, k=k)
+            want = z[f"{sim}_k{k}"]
+            assert m.users_evaluated == int(want[2])
+            assert m.recall_at_k == pytest.approx(want[0], abs=1e-12)
+            assert m.ndcg_at_k == pytest.approx(want[1], abs=1e-12)
+        model = DeviceModel(S.values, T.values)
+        users = z[f"{sim}_top20_users"].astype(np.int32)
+        _, _, top = eval_users_device(model.S, model.T, users, tr, te, 20, sim == "cosine",
+                                      want_topk=True)
+        assert np.array_equal(top, z[f"{sim}_top20"])
+
+
+def test_eval_c2_init_matches_reference(torch_cuda):
+    from paper_2304_07334_b200 import InitSpec, init_matrix, TrainingConfig
+    from paper_2304_07334_b200.evaluator import evaluate
+    from paper_2304_07334_b200.synth import make_dataset
+    z = np.load(os.path.join(GOLDEN, "eval.npz"))
+    tr, te, _ = make_dataset("c2")
+    S = init_matrix(tr.num_users, 64, InitSpec(seed=0))
+    T = init_matrix(tr.num_items, 64, InitSpec(seed=0))
+    m = evaluate(S, T, tr, te, TrainingConfig(emb_dim=64, num_negatives=1), k=20)
+    want = z["c2_init_k20"]
+    assert m.users_evaluated == int(want[2])
+    assert abs(m.recall_at_k - want[0]) <= 1e-9
+    assert abs(m.ndcg_at_k - want[1]) <= 1e-9
+
+
+def test_topk_items_reference_cases(torch_cuda):
+    from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+    from paper_2304_07334_b200.evaluator import topk_items
+    from oracle.oracle import topk_ref
+    T3 = EmbeddingMatrix(np.array([[1, 0], [0, 1], [-1, 0]], dtype=np.float32))
+    assert list(topk_items(np.array([1.0, 0.0]), T3, [], 2)) == [0, 1]
+    assert list(topk_items(np.array([1.0, 0.0]), T3, [0], 2)) == [1, 2]
+    assert list(topk_items(np.array([1.0, 0.0]), T3, [0], 10)) == [1, 2]
+    Tt = EmbeddingMatrix(np.array([[1, 0], [1, 0], [1, 0], [0.5, 0.5]], dtype=np.float32))
+    assert list(topk_items(np.array([1.0, 0.0]), Tt, [], 3)) == [0, 1, 2]
+    rng = np.random.default_rng(1234)
+    for _ in range(10):
+        T = EmbeddingMatrix(rng.standard_normal((200, 8)).astype(np.float32))
+        u = rng.standard_normal(8)
+        excl = np.unique(rng.integers(0, 200, size=30))
+        for sim in ("cosine", "dot"):
+            got = topk_items(u, T, excl, 10, sim)
+            t64 = T.values.astype(np.float64)
+            sc = (t64 @ u) / (np.linalg.norm(t64, axis=1) * np.linalg.norm(u)) \
+                if sim == "cosine" else t64 @ u
+            assert list(got) == list(topk_ref(sc, excl, 10))
+    with pytest.raises(ValueError):
+        topk_items(np.array([1.0, 0.0]), T3, [], 0)
+
+
+def test_eval_random_vs_oracle_many_ks(torch_cuda):
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import TrainingConfig
+    from paper_2304_07334_b200.dataset import from_user_lists
+    from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+    from paper_2304_07334_b200.evaluator import evaluate
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        nu, ni, K = int(rng.integers(5, 200)), int(rng.integers(30, 700)), int(rng.integers(1, 70))
+        S = EmbeddingMatrix(rng.standard_normal((nu, K)).astype(np.float32))
+        T = EmbeddingMatrix(rng.standard_normal((ni, K)).astype(np.float32))
+        if trial == 1:
+            S.values[0] = 0.0
+            T.values[:5] = 0.0
+        tr = from_user_lists({u: rng.integers(0, ni, int(rng.integers(0, 40)))
+                              for u in range(nu)}, num_users=nu, num_items=ni)
+        te = from_user_lists({u: rng.integers(0, ni, int(rng.integers(0, 6)))
+                              for u in range(0, nu, 2)}, num_users=nu, num_items=ni)
+        for sim in ("cosine", "dot"):
+            for k in (1, 7, 20, 33, 100):
+                m = evaluate(S, T, tr, te, TrainingConfig(emb_dim=K, num_negatives=1,
+                                                          similarity=sim), k=k)
+                rec, nd, n = O.evaluate_ref(S.values, T.values, tr.offsets, tr.items, nu,
+                                            te.offsets, te.items, nu, k=k, similarity=sim)
+                assert m.users_evaluated == n
+                assert m.recall_at_k == pytest.approx(rec, abs=1e-12), (trial, sim, k)
+                assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12), (trial, sim, k)
