@@ -38,6 +38,8 @@ struct HogwildArgs {
 };
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
+cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t stream, int *workers_out,
+                                  bool bulk);
 
 cudaError_t launch_sample(uint64_t s0, int64_t first_pair, int64_t npairs, int N,
                           int64_t num_items, int32_t *out, cudaStream_t stream);

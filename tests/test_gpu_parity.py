@@ -338,3 +338,75 @@ def test_eval_random_vs_oracle_many_ks(torch_cuda):
                 assert m.users_evaluated == n
                 assert m.recall_at_k == pytest.approx(rec, abs=1e-12), (trial, sim, k)
                 assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12), (trial, sim, k)
+
+
+def _rel_fro(a, b):
+    return float(np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(b.astype(np.float64)))
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("force_generic", [False, True])
+def test_hogwild_window1_tracks_reference(torch_cuda, fp64, force_generic, monkeypatch):
+    """window=1 -> one worker, pairs in order: the throughput kernel's math
+    (fp32 or fp64 partial dots, fused update) must track the reference
+    within the north_star tolerance (1e-4, norm-relative) over a c1 epoch."""
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    if force_generic:
+        monkeypatch.setenv("HEAT_FORCE_GENERIC", "1")
+    z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
+    train, _, _ = make_dataset("c1")
+    S = init_matrix(1000, 32, InitSpec(seed=0)).values
+    T = init_matrix(2000, 32, InitSpec(seed=0)).values
+    model = DeviceModel(S, T)
+    u, i = epoch_pairs(train, shuffle_seed(0, 0))
+    du, di = model.upload_pairs(u, i)
+    p = model.params(n_neg=10, lr=1e-3, l2=0.0, mu=10.0, theta=0.5, cosine=True,
+                     mode=N.MODE_HOGWILD, stream_base=epoch_stream(0, 0), window=1, fp64=fp64)
+    model.counters.reset()
+    model.train_range(du, di, 0, len(u), p)
+    c = model.counters.read()
+    model.download(S, T)
+    assert c.pairs == len(u)
+    assert abs(c.loss / len(u) - z["mean_loss"][0]) <= 1e-4 * abs(z["mean_loss"][0])
+    assert _rel_fro(S, z["S_e0"]) <= 1e-4, _rel_fro(S, z["S_e0"])
+    assert _rel_fro(T, z["T_e0"]) <= 1e-4, _rel_fro(T, z["T_e0"])
+
+
+@pytest.mark.parametrize("K,N,cos,l2,theta", [(16, 7, True, 0.0, -0.5), (32, 33, False, 0.01, 0.3),
+                                              (64, 100, True, 0.02, 0.2), (128, 300, True, 0.0, 0.1),
+                                              (64, 5, True, 0.0, -1.0), (48, 20, True, 0.01, 0.0)])
+def test_hogwild_window1_vs_oracle(torch_cuda, K, N, cos, l2, theta):
+    """Branch coverage of the throughput kernels (fast K in {16,32,64,128},
+    generic otherwise): sequential run vs the oracle, 1e-4 norm-relative."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.device import DeviceModel
+    rng = np.random.default_rng(K + N)
+    nu, ni, P = 40, 250, 600
+    S = (rng.standard_normal((nu, K)) * 0.1).astype(np.float32)
+    T = (rng.standard_normal((ni, K)) * 0.1).astype(np.float32)
+    S[3] = 0.0
+    T[7] = 0.0
+    u = rng.integers(0, nu, P).astype(np.int32)
+    i = rng.integers(0, ni, P).astype(np.int32)
+    s0 = 0x1234567890ABCDEF
+    S2, T2 = S.copy(), T.copy()
+    r = O.train_range(S2, T2, u, i, 0, P, s0, n_neg=N, lr=0.01, l2=l2, mu=2.0, theta=theta,
+                      cosine=cos)
+    model = DeviceModel(S, T)
+    du, di = model.upload_pairs(u, i)
+    p = model.params(n_neg=N, lr=0.01, l2=l2, mu=2.0, theta=theta, cosine=cos,
+                     mode=NN.MODE_HOGWILD, stream_base=s0, window=1, fp64=True)
+    model.counters.reset()
+    model.train_range(du, di, 0, P, p)
+    c = model.counters.read()
+    model.download(S, T)
+    assert c.degenerate == r.degenerate
+    assert abs(c.active - r.active) <= max(2, r.active // 1000)
+    assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss)
+    assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
