@@ -73,13 +73,17 @@ typedef struct heat_counters {
  * `counters` is a device pointer.  For HEAT_MODE_DELTA, `delta_ids`
  * (int32, capacity entries) and `delta_rows` (capacity x dim float32) receive
  * the item-row updates and `delta_count` (device int64) their number.
+ * `pair_index` (optional, int64 per pair) is the pair's global epoch position,
+ * the key of its negative draws (a user shard trains a subset of the epoch
+ * and must draw the 1-GPU run's negatives); NULL means position p itself.
  * Scratch (HEAT_MODE_EXACT): `scratch` may be NULL (internal allocation) or a
  * device buffer of at least heat_scratch_bytes(n_neg, dim) bytes. */
 int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      const int32_t *ep_users, const int32_t *ep_items, int64_t start,
                      int64_t stop, const heat_sgd_params *params, heat_counters *counters,
                      int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
-                     int64_t delta_capacity, void *scratch, void *stream);
+                     int64_t delta_capacity, const int64_t *pair_index, void *scratch,
+                     void *stream);
 
 int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim);
 

@@ -72,7 +72,7 @@ def lib():
     P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     L.heat_train_range.restype = ctypes.c_int
     L.heat_train_range.argtypes = [P, i64, P, i64, P, P, i64, i64, ctypes.POINTER(SgdParams), P,
-                                   P, P, P, i64, P, P]
+                                   P, P, P, i64, P, P, P]
     L.heat_scratch_bytes.restype = i64
     L.heat_scratch_bytes.argtypes = [i32, i32]
     L.heat_sample_negatives.restype = ctypes.c_int

@@ -144,7 +144,8 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      const int32_t *ep_users, const int32_t *ep_items, int64_t start,
                      int64_t stop, const heat_sgd_params *p, heat_counters *counters,
                      int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
-                     int64_t delta_capacity, void *scratch, void *stream) {
+                     int64_t delta_capacity, const int64_t *pair_index, void *scratch,
+                     void *stream) {
     if (!p) return fail(HEAT_ERR_INVALID, "null params");
     if (!S || !T || !counters) return fail(HEAT_ERR_INVALID, "null table or counters pointer");
     if (p->dim < 1) return fail(HEAT_ERR_INVALID, "dim must be >= 1, got %d", p->dim);
@@ -170,7 +171,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         if (!snap) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
         e = launch_exact(S, T, ep_users, ep_items, start, stop, p->dim, p->n_neg, p->use_cosine,
                          p->lr, p->l2, p->mu, p->theta, p->stream_base, t_rows, counters,
-                         (float *)snap, st);
+                         (float *)snap, pair_index, st);
         break;
     }
     case HEAT_MODE_HOGWILD:
@@ -189,6 +190,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         a.delta_ids = p->mode == HEAT_MODE_DELTA ? delta_ids : nullptr;
         a.delta_rows = delta_rows; a.delta_count = delta_count;
         a.delta_capacity = delta_capacity;
+        a.pair_index = pair_index;
         e = launch_hogwild(a, st, nullptr);
         break;
     }

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kExactThreads, 1)
     exact_kernel(float *__restrict__ S, float *__restrict__ T, const int32_t *__restrict__ users,
                  const int32_t *__restrict__ items, int64_t start, int64_t stop, int K, int N,
                  int cosine, double lr, double l2, double mu, double theta, uint64_t s0,
-                 FastMod fm, heat_counters *ctr, float *__restrict__ snap) {
+                 FastMod fm, heat_counters *ctr, float *__restrict__ snap,
+                 const int64_t *__restrict__ pair_index) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ExactSmem &sh = *reinterpret_cast<ExactSmem *>(smem_raw);
     double *ubuf = reinterpret_cast<double *>(smem_raw + sizeof(ExactSmem) + 16 -
@@ -99,7 +100,8 @@ __global__ void __launch_bounds__(kExactThreads, 1)
             ubuf[k] = (double)S[u * K + k];
             pos_buf[k] = T[pos * K + k];
         }
-        for (int j = tid; j < N; j += kExactThreads) nids[j] = neg_id(s0, p, N, j, fm);
+        const int64_t pg = pair_index ? pair_index[p] : p;  // RNG key
+        for (int j = tid; j < N; j += kExactThreads) nids[j] = neg_id(s0, pg, N, j, fm);
         __syncthreads();
 
         // ---- similarity (trainer.py:176-207)
@@ -290,14 +292,16 @@ size_t exact_smem_bytes(int K, int N) {
 cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t *items,
                          int64_t start, int64_t stop, int K, int N, int cosine, double lr,
                          double l2, double mu, double theta, uint64_t s0, int64_t num_items,
-                         heat_counters *ctr, float *snap, cudaStream_t stream) {
+                         heat_counters *ctr, float *snap, const int64_t *pair_index,
+                         cudaStream_t stream) {
     size_t smem = exact_smem_bytes(K, N);
     cudaError_t e = cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     exact_kernel<<<1, kExactThreads, smem, stream>>>(S, T, users, items, start, stop, K, N,
                                                      cosine, lr, l2, mu, theta, s0,
-                                                     FastMod::make((uint64_t)num_items), ctr, snap);
+                                                     FastMod::make((uint64_t)num_items), ctr, snap,
+                                                     pair_index);
     return cudaGetLastError();
 }
 

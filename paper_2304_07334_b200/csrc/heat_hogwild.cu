@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kHogThreads)
         ++mine;
         const int64_t u = a.users[p];
         const int64_t pos = a.items[p];
+        const int64_t pg = a.pair_index ? a.pair_index[p] : p;  // RNG key
         float ur[C], ug[C];
         double ssp = 0.0;
 #pragma unroll
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kHogThreads)
 
         double hinge = 0.0, sim_p = 0.0;
         for (int r = 0; r <= N; ++r) {
-            const int32_t id = r == 0 ? (int32_t)pos : neg_id(a.s0, p, N, r - 1, fm);
+            const int32_t id = r == 0 ? (int32_t)pos : neg_id(a.s0, pg, N, r - 1, fm);
             double ttp = 0.0, stp = 0.0;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -279,8 +280,9 @@ __global__ void __launch_bounds__(kHogThreads)
         ++mine;
         const int64_t u = a.users[p];
         const int64_t pos = a.items[p];
+        const int64_t pg = a.pair_index ? a.pair_index[p] : p;  // RNG key
         for (int r = lane; r < nb * RPB; r += 32)
-            ids[r] = r == 0 ? (int32_t)pos : (r <= N ? neg_id(a.s0, p, N, r - 1, fm) : 0);
+            ids[r] = r == 0 ? (int32_t)pos : (r <= N ? neg_id(a.s0, pg, N, r - 1, fm) : 0);
         const float4 u4 = ldcg4(a.S + u * K + c * 4);
         A ssp = (A)u4.x * (A)u4.x + (A)u4.y * (A)u4.y + (A)u4.z * (A)u4.z + (A)u4.w * (A)u4.w;
 #pragma unroll

@@ -139,7 +139,10 @@ __global__ void __launch_bounds__(32)
     }
     // counter-form SplitMix64 state of this lane's next draw:
     // s0 + (p*N + j + 1) * GAMMA with j = 32*ps + lane - 1
-    uint64_t rng_state = a.s0 + ((uint64_t)(a.start + gw) * (uint64_t)N + (uint64_t)lane) * kGamma;
+    auto rng_key = [&](int64_t pp) -> uint64_t {
+        return (uint64_t)(a.pair_index ? a.pair_index[pp] : pp);
+    };
+    uint64_t rng_state = a.s0 + (rng_key(a.start + gw) * (uint64_t)N + (uint64_t)lane) * kGamma;
     // this lane's fixed 16-byte chunk and row-within-instruction
     constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;  // rows per copy instruction
     constexpr int NI = 32 / RPI;                          // copy instructions per stage
@@ -202,7 +205,8 @@ __global__ void __launch_bounds__(32)
             pf_u = nx_u;
             pf_pos = nx_pos;
             const int64_t pn = a.start + gw + pt * n_workers;
-            rng_state = a.s0 + ((uint64_t)pn * (uint64_t)N + (uint64_t)lane) * kGamma;
+            if (pt < my_pairs)
+                rng_state = a.s0 + (rng_key(pn) * (uint64_t)N + (uint64_t)lane) * kGamma;
             if (pt + 1 < my_pairs) {
                 nx_u = a.users[pn + n_workers];
                 nx_pos = a.items[pn + n_workers];

@@ -14,7 +14,8 @@ size_t exact_smem_bytes(int K, int N);
 cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t *items,
                          int64_t start, int64_t stop, int K, int N, int cosine, double lr,
                          double l2, double mu, double theta, uint64_t s0, int64_t num_items,
-                         heat_counters *ctr, float *snap, cudaStream_t stream);
+                         heat_counters *ctr, float *snap, const int64_t *pair_index,
+                         cudaStream_t stream);
 
 struct HogwildArgs {
     float *S;
@@ -35,6 +36,8 @@ struct HogwildArgs {
     float *delta_rows;
     int64_t *delta_count;
     int64_t delta_capacity;
+    // global epoch position of local pair p (RNG key); NULL = p itself
+    const int64_t *pair_index;
 };
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);

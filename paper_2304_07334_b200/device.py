@@ -111,7 +111,8 @@ class DeviceModel:
                            window=window, flags=1 if fp64 else 0)
 
     def train_range(self, users: torch.Tensor, items: torch.Tensor, start: int, stop: int,
-                    params: N.SgdParams, delta=None) -> None:
+                    params: N.SgdParams, delta=None, pair_index: torch.Tensor | None = None,
+                    stream=None) -> None:
         """Launch pairs [start, stop) on the current stream (asynchronous)."""
         scratch = self.scratch(params.n_neg) if params.mode == N.MODE_EXACT else None
         d_ids = d_rows = d_cnt = None
@@ -121,7 +122,8 @@ class DeviceModel:
         rc = N.lib().heat_train_range(
             _p(self.S), self.S.shape[0], _p(self.T), self.T.shape[0], _p(users), _p(items),
             start, stop, ctypes.byref(params), self.counters.ptr(), _p(d_ids), _p(d_rows),
-            _p(d_cnt), cap, _p(scratch), _stream(self.device))
+            _p(d_cnt), cap, _p(pair_index), _p(scratch),
+            _stream(self.device) if stream is None else ctypes.c_void_p(stream.cuda_stream))
         N.check(rc)
 
 
