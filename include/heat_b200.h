@@ -17,6 +17,7 @@
  *   heat_eval_users        <- evaluator.evaluate scoring + top-k + hits
  *                             evaluator.py:140-172, _topk_from_scores 61-73
  *   heat_apply_row_deltas  <- (new) multi-GPU item-delta exchange, SURVEY.md §8(e)
+ *   heat_epoch_pairs       <- dataset.epoch_pairs (host)    dataset.py:146-158
  */
 #ifndef HEAT_B200_H
 #define HEAT_B200_H
@@ -112,6 +113,16 @@ int heat_eval_users(const void *S, int32_t s_f64, const float *T, int64_t t_rows
 int heat_apply_row_deltas(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,
                           const float *rows, const int64_t *count, int64_t capacity,
                           int32_t ordered, void *stream);
+
+/* HOST function: one epoch's (user, positive) order, bit-identical to
+ * numpy Generator(PCG64(seed)).permutation applied to the CSR pairs
+ * (dataset.py:146-158).  offsets/items/out_* are host arrays; the PCG64 state
+ * words are numpy's after its own seeding (bit_generator.state).  Returns 0,
+ * or -1 on bad input. */
+int heat_epoch_pairs(const int64_t *offsets, int64_t num_users, const int32_t *items, int64_t P,
+                     uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                     int32_t has_uint32, uint32_t uinteger, int32_t *out_users,
+                     int32_t *out_items);
 
 const char *heat_last_error(void);
 int heat_version(void);

@@ -22,7 +22,8 @@ MODE_HOGWILD = 1
 MODE_DELTA = 2
 
 EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
-           "heat_eval_users", "heat_apply_row_deltas", "heat_last_error", "heat_version")
+           "heat_eval_users", "heat_apply_row_deltas", "heat_epoch_pairs", "heat_last_error",
+           "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -82,6 +83,8 @@ def lib():
                                   P, P, P, P]
     L.heat_apply_row_deltas.restype = ctypes.c_int
     L.heat_apply_row_deltas.argtypes = [P, i64, i32, P, P, P, i64, i32, P]
+    L.heat_epoch_pairs.restype = ctypes.c_int
+    L.heat_epoch_pairs.argtypes = [P, i64, P, i64, u64, u64, u64, u64, i32, ctypes.c_uint32, P, P]
     L.heat_last_error.restype = ctypes.c_char_p
     L.heat_last_error.argtypes = []
     L.heat_version.restype = ctypes.c_int

@@ -24,7 +24,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 # per-file extra flags: the exact kernel must never contract a*b+c into FMA
 EXTRA = {"heat_exact.cu": ["--fmad=false"]}
 SOURCES = ["heat_capi.cu", "heat_sample.cu", "heat_exact.cu", "heat_hogwild.cu", "heat_hogwild_staged.cu",
-           "heat_eval.cu"]
+           "heat_eval.cu", "heat_host.cpp"]
 
 
 def nvcc() -> str:
@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(BUILD, src.rsplit(".", 1)[0] + ".o")
         cmd = [cc, *ARCH, *COMMON, *EXTRA.get(src, []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -93,12 +93,49 @@ def with_universe(s: InteractionSet, num_users: int, num_items: int) -> Interact
     return InteractionSet(num_users, num_items, offsets, s.items)
 
 
-def epoch_pairs(train, seed: int) -> tuple[np.ndarray, np.ndarray]:
+def epoch_pairs(train, seed: int, out=None) -> tuple[np.ndarray, np.ndarray]:
     """One epoch's (user, positive) pairs in seed order (dataset.py:146-158).
 
-    Same construction as the reference — repeat users by degree, then one
-    numpy PCG64 ``permutation`` — so the order is identical in this process.
+    The order is numpy's Generator(PCG64(seed)).permutation of the CSR pairs.
+    With the native library present the shuffle runs in C++
+    (csrc/heat_host.cpp: the same PCG64 stream and Fisher-Yates swaps, applied
+    to the packed pairs; bit-identical, GIL released); `out` may supply the
+    two int32 output arrays (e.g. pinned host buffers).
     """
+    if train.num_pairs == 0:
+        raise ValueError("training set has no pairs")
+    lib = _native_lib()
+    if lib is not None:
+        import ctypes
+        st = np.random.PCG64(seed).state
+        s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+        P = int(train.num_pairs)
+        offsets = np.ascontiguousarray(train.offsets, dtype=np.int64)
+        items = np.ascontiguousarray(train.items, dtype=np.int32)
+        if out is None:
+            out = (np.empty(P, dtype=np.int32), np.empty(P, dtype=np.int32))
+        ou, oi = out
+        m64 = (1 << 64) - 1
+        rc = lib.heat_epoch_pairs(offsets.ctypes.data, int(train.num_users), items.ctypes.data, P,
+                                  s >> 64, s & m64, inc >> 64, inc & m64,
+                                  int(st["has_uint32"]), int(st["uinteger"]),
+                                  ou.ctypes.data, oi.ctypes.data)
+        if rc != 0:
+            raise ValueError("inconsistent interaction set")
+        return ou, oi
+    return epoch_pairs_numpy(train, seed)
+
+
+def _native_lib():
+    try:
+        from . import _native
+        return _native.lib()
+    except (ImportError, OSError):
+        return None
+
+
+def epoch_pairs_numpy(train, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """The reference's construction verbatim in numpy (dataset.py:154-158)."""
     if train.num_pairs == 0:
         raise ValueError("training set has no pairs")
     counts = np.diff(train.offsets)

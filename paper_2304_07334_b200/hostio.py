@@ -1,0 +1,122 @@
+"""Host side of the drop-in call: epoch-order prefetch and page-locked I/O.
+
+The reference's ``train_epoch`` mutates the caller's numpy tables in place
+(trainer.py:417) and builds the epoch order on the host every call
+(trainer.py:390-392).  For the device path that means a host->device copy of
+S, T and the pair order and a device->host copy of S and T per call.  This
+module keeps that host work off the critical path:
+
+* ``PairPrefetcher`` — after epoch e's order is produced, epoch e+1's order
+  (same interaction set, same seed) is computed on a host thread by the
+  native shuffle (csrc/heat_host.cpp, GIL released) into page-locked buffers,
+  so a training loop calling train_epoch(epoch=e+1) finds it ready;
+* ``pin_array`` — page-locks a caller's numpy buffer once (cudaHostRegister)
+  so table copies run as async DMA at full PCIe rate; registrations are kept
+  in a small LRU that also holds a reference to the array, so a registered
+  address can never be freed and reused behind our back.
+"""
+
+from __future__ import annotations
+
+import threading
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from .dataset import epoch_pairs
+
+
+def _train_key(train) -> tuple:
+    return (id(train), id(train.items), id(train.offsets), int(train.num_pairs),
+            int(train.num_users))
+
+
+class PairPrefetcher:
+    """One-slot look-ahead cache of epoch orders in pinned host memory."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._pending: dict = {}  # key -> (thread, holder)
+        self._pool: list = []     # reusable pinned (users, items) buffers
+
+    def _buffers(self, P: int):
+        with self._lock:
+            for i, (u, it) in enumerate(self._pool):
+                if u.numel() == P:
+                    return self._pool.pop(i)
+        pin = torch.cuda.is_available()
+        return (torch.empty(P, dtype=torch.int32, pin_memory=pin),
+                torch.empty(P, dtype=torch.int32, pin_memory=pin))
+
+    def release(self, bufs) -> None:
+        with self._lock:
+            if len(self._pool) < 4:
+                self._pool.append(bufs)
+
+    def _compute(self, train, seed: int, bufs):
+        epoch_pairs(train, seed, out=(bufs[0].numpy(), bufs[1].numpy()))
+        return bufs
+
+    def get(self, train, seed: int):
+        """(users, items) pinned torch tensors of the order for `seed`."""
+        key = (_train_key(train), seed)
+        with self._lock:
+            hit = self._pending.pop(key, None)
+        if hit is not None:
+            th, holder = hit
+            th.join()
+            if "err" not in holder:
+                return holder["bufs"]
+        return self._compute(train, seed, self._buffers(train.num_pairs))
+
+    def prefetch(self, train, seed: int) -> None:
+        key = (_train_key(train), seed)
+        with self._lock:
+            if key in self._pending:
+                return
+            # keep only the newest look-ahead
+            stale = list(self._pending.items())
+            self._pending.clear()
+        for _, (th, holder) in stale:
+            th.join()
+            if "bufs" in holder:
+                self.release(holder["bufs"])
+        holder: dict = {}
+        bufs = self._buffers(train.num_pairs)
+
+        def run():
+            try:
+                holder["bufs"] = self._compute(train, seed, bufs)
+            except BaseException as exc:  # surfaced as a miss; recomputed inline
+                holder["err"] = exc
+
+        th = threading.Thread(target=run, daemon=True)
+        with self._lock:
+            self._pending[key] = (th, holder)
+        th.start()
+
+
+PREFETCH = PairPrefetcher()
+
+_pins: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
+_PIN_SLOTS = 6
+
+
+def pin_array(a: np.ndarray) -> bool:
+    """Page-lock `a`'s buffer (idempotent); returns whether it is pinned."""
+    if not torch.cuda.is_available() or a.nbytes == 0 or not a.flags.c_contiguous:
+        return False
+    key = (a.ctypes.data, a.nbytes)
+    if key in _pins:
+        _pins.move_to_end(key)
+        return True
+    cudart = torch.cuda.cudart()
+    rc = cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+    if int(rc) != 0:
+        return False
+    _pins[key] = a
+    while len(_pins) > _PIN_SLOTS:
+        (ptr, _), old = _pins.popitem(last=False)
+        cudart.cudaHostUnregister(ptr)
+    return True

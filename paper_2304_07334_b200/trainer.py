@@ -155,23 +155,43 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
                 collect_phases: bool = False) -> EpochReport:
     """Drop-in for heatcf.trainer.train_epoch (trainer.py:385-466).
 
-    S.values / T.values are updated in place, like the reference.  With
-    collect_phases the phase dict carries measured device times: read_emb =
-    host->device upload, similarity = the fused kernel (read, similarity,
-    loss, gradient and update are one pass), update = device->host write-back.
+    S.values / T.values are updated in place, like the reference.  The epoch
+    order comes from the native shuffle, prefetched one epoch ahead on a host
+    thread (hostio.PairPrefetcher); the caller's tables are page-locked once
+    so the per-call host<->device copies are async DMA.  wall_time spans the
+    whole call.  With collect_phases the phase dict carries measured times:
+    read_emb = host->device upload, similarity = the fused kernel (read,
+    similarity, loss, gradient and update are one pass), update =
+    device->host write-back.
     """
+    from .hostio import PREFETCH, pin_array
+
     _check_shapes(S, T, train, cfg, weights)
     _check_supported(cfg)
+    if train.num_pairs == 0:  # dataset.py:154 raises inside epoch_pairs
+        raise ValueError("training set has no pairs")
     t_start = time.perf_counter()
-    ep_users, ep_items = epoch_pairs(train, shuffle_seed(cfg.seed, epoch))
+    model = _session_model(S.values, T.values)  # raises without CUDA: no CPU fallback
+    bufs = PREFETCH.get(train, shuffle_seed(cfg.seed, epoch))
+    PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + 1))
+    dev = model.device
+    stream = torch.cuda.current_stream(dev)
+    pin_array(S.values)
+    pin_array(T.values)
     t_up = time.perf_counter()
-    model = DeviceModel(S.values, T.values, _OPTIONS.device)
-    pairs = model.upload_pairs(ep_users, ep_items)
-    torch.cuda.current_stream(model.device).synchronize()
+    model.S.copy_(torch.from_numpy(S.values), non_blocking=True)
+    model.T.copy_(torch.from_numpy(T.values), non_blocking=True)
+    du = bufs[0].to(dev, non_blocking=True)
+    di = bufs[1].to(dev, non_blocking=True)
+    if collect_phases:
+        stream.synchronize()
     t_run = time.perf_counter()
-    rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=pairs)
+    rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=(du, di))
+    PREFETCH.release(bufs)
     t_down = time.perf_counter()
-    model.download(S.values, T.values)
+    torch.from_numpy(S.values).copy_(model.S, non_blocking=True)
+    torch.from_numpy(T.values).copy_(model.T, non_blocking=True)
+    stream.synchronize()
     t_end = time.perf_counter()
     rep.wall_time = t_end - t_start
     if collect_phases:
@@ -179,6 +199,23 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
         rep.phase_times["similarity"] = timing["kernel_s"]
         rep.phase_times["update"] = t_end - t_down
     return rep
+
+
+_SESSION: dict = {}
+
+
+def _session_model(S: np.ndarray, T: np.ndarray) -> DeviceModel:
+    """Reusable device buffers for the drop-in call (contents are always
+    overwritten from the caller's arrays, so reuse never leaks state)."""
+    from .device import require_cuda
+    dev = require_cuda(_OPTIONS.device)
+    key = (str(dev), S.shape, T.shape)
+    m = _SESSION.get(key)
+    if m is None:
+        _SESSION.clear()
+        m = DeviceModel(S, T, dev)
+        _SESSION[key] = m
+    return m
 
 
 def train(S, T, train_set, test_set, cfg, weights=None, *, eval_interval: int = 0, k: int = 20,

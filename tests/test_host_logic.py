@@ -234,3 +234,22 @@ def test_gloo_world2_delta_exchange_keeps_replicas_identical():
         for j in range(len(ids)):
             want[ids[j]] += rows[j]
     assert np.allclose(T0, want, atol=1e-6)
+
+
+def test_native_epoch_shuffle_is_numpy_bit_identical():
+    import time
+    from paper_2304_07334_b200.dataset import epoch_pairs_numpy
+    for name, scale in (("c1", 1.0), ("c2", 0.2)):
+        tr, _, _ = make_dataset(name, scale=scale)
+        for seed in (0, 1, 12345, R.shuffle_seed(0, 3), 2**62 + 7):
+            u, i = epoch_pairs(tr, seed)
+            un, inn = epoch_pairs_numpy(tr, seed)
+            assert np.array_equal(u, un) and np.array_equal(i, inn)
+    tiny = from_user_lists({0: [4], 2: [1, 3]}, num_users=3, num_items=5)
+    for seed in range(20):
+        assert [a.tolist() for a in epoch_pairs(tiny, seed)] == \
+            [a.tolist() for a in epoch_pairs_numpy(tiny, seed)]
+    tr, _, _ = make_dataset("c2")
+    t0 = time.perf_counter(); epoch_pairs(tr, 5); t1 = time.perf_counter()
+    epoch_pairs_numpy(tr, 5); t2 = time.perf_counter()
+    print(f"native shuffle {1e3*(t1-t0):.1f} ms vs numpy {1e3*(t2-t1):.1f} ms")
