@@ -476,15 +476,20 @@ cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *worke
         if (workers_out) *workers_out = 0;
         return cudaSuccess;
     }
-    // staged (default: cp.async ring) | tma (bulk-copy ring) | regs | generic
+    // resident (default when the pair fits in smem) | staged (cp.async ring) |
+    // tma (bulk-copy ring) | regs | generic
     const char *impl = getenv("HEAT_HOGWILD_IMPL");
     const bool aligned = ((uintptr_t)a.S % 16 == 0) && ((uintptr_t)a.T % 16 == 0);
     if (getenv("HEAT_FORCE_GENERIC")) impl = "generic";
-    if (aligned && (!impl || impl[0] == 's' || impl[0] == 't')) {
+    if (aligned && (!impl || impl[0] == 'r' && impl[1] == 'e')) {
+        cudaError_t e = launch_hogwild_resident(a, stream, workers_out);
+        if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
+    }
+    if (aligned && (!impl || impl[0] == 's' || impl[0] == 't' || (impl[0] == 'r' && impl[1] == 'e'))) {
         cudaError_t e = launch_hogwild_staged(a, stream, workers_out, impl && impl[0] == 't');
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
-    if (!impl || impl[0] != 'g') {
+    if (!impl || impl[0] != 'g') {  // regs
         cudaError_t e = cudaErrorNotSupported;
         switch (a.K) {
         case 16: e = launch_fast<16>(a, stream, workers_out); break;

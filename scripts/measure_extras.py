@@ -1,0 +1,77 @@
+"""Timings beside the headline bench: EXACT (bit-parity) mode throughput, the
+recall@20 evaluator, and the Hogwild kernel per config.  One JSON line per
+measurement (CUDA events, after warm-up, L2 flushed before each timed call)."""
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2304_07334_b200 import _native as N  # noqa: E402
+from paper_2304_07334_b200.config import TrainingConfig  # noqa: E402
+from paper_2304_07334_b200.dataset import epoch_pairs  # noqa: E402
+from paper_2304_07334_b200.device import DeviceModel  # noqa: E402
+from paper_2304_07334_b200.embeddings import InitSpec, init_matrix  # noqa: E402
+from paper_2304_07334_b200.evaluator import evaluate_device  # noqa: E402
+from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed  # noqa: E402
+from paper_2304_07334_b200.synth import make_dataset  # noqa: E402
+
+flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+
+def timed(fn):
+    flush.zero_()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def exact(cfg_name, npairs):
+    tr, _, sp = make_dataset(cfg_name)
+    S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0)).values
+    T = init_matrix(tr.num_items, sp.dim, InitSpec(seed=0)).values
+    m = DeviceModel(S, T)
+    u, i = epoch_pairs(tr, shuffle_seed(0, 0))
+    n = min(npairs, len(u))
+    du, di = m.upload_pairs(u[:n], i[:n])
+    p = m.params(n_neg=sp.negatives, lr=sp.learning_rate, l2=0.0, mu=sp.mu, theta=sp.theta,
+                 cosine=True, mode=N.MODE_EXACT, stream_base=epoch_stream(0, 0))
+    m.train_range(du, di, 0, min(n, 256), p)
+    torch.cuda.synchronize()
+    dt = timed(lambda: m.train_range(du, di, 0, n, p))
+    print(json.dumps({"what": "exact_mode", "config": cfg_name, "pairs": n, "seconds": dt,
+                      "samples_per_s": n / dt}), flush=True)
+
+
+def evaluation(cfg_name):
+    tr, te, sp = make_dataset(cfg_name)
+    S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0))
+    T = init_matrix(tr.num_items, sp.dim, InitSpec(seed=0))
+    m = DeviceModel(S.values, T.values)
+    cfg = TrainingConfig(emb_dim=sp.dim, num_negatives=1)
+    evaluate_device(m, S, T, tr, te, cfg, k=20)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = evaluate_device(m, S, T, tr, te, cfg, k=20)
+    dt = time.perf_counter() - t0
+    users = r.users_evaluated
+    flops = 2.0 * users * tr.num_items * sp.dim
+    print(json.dumps({"what": "evaluate", "config": cfg_name, "users": users,
+                      "items": tr.num_items, "seconds": dt, "recall@20": r.recall_at_k,
+                      "score_gflop": flops / 1e9, "gflops": flops / dt / 1e9}), flush=True)
+
+
+if __name__ == "__main__":
+    exact("c1", 20000)
+    exact("c2", 50000)
+    evaluation("c2")
