@@ -5,25 +5,27 @@
 // Why: with a window of B pairs in flight only ~B/148 workers share an SM.
 // One warp per worker leaves ~1.7 warps per scheduler and exposes every
 // shared-memory and FMA latency (measured: 36 % issue efficiency).  Here the
-// same B pairs are served by nb = ceil((N+1)/32) warps each, so an SM holds
+// same B pairs are served by NB = ceil((N+1)/32) warps each, so an SM holds
 // ~7 pairs but ~28 warps.
 //
 // Per pair (math = trainer.py:114-293, Hogwild across CTAs):
 //   A  every warp draws its stage's negative ids (counter-form SplitMix64,
-//      one draw per lane) and copies its 32 rows with per-lane 16-byte
-//      cp.async.cg (LDGSTS, L2 evict-last hint); warp 0 also copies the user
-//      row.  wait_group 0, barrier.
-//   B  lane j of warp w scores row 32w+j: tt = v.v, st = u.v (LDS.128, rows
-//      padded by 16 bytes: conflict-free), fp32 similarity screen, exact
-//      binary64 only near the margin (trainer.py:184-221); rows to write are
-//      appended to a CTA list by reference to their ring slot.  barrier.
-//   C  the list is applied by all warps (entry e -> warp e % nb): item deltas
-//      with red.global.add from the still-resident snapshot rows, user-gradient
-//      partials per warp.  barrier.
-//   D  warp 0 sums the partials in warp order and updates the user row;
-//      the loss adds (1 - sim_p) + mu/N * sum of per-warp hinges.
-// Every row of the pair is read before any write (trainer.py:118-146) and
-// the written rows are the pre-pair snapshots, even for repeated ids.
+//      one draw per lane) and copies its rows with per-lane 16-byte
+//      cp.async.cg (LDGSTS, L2 evict-last hint) into an XOR-swizzled ring
+//      (conflict-free lane-per-row reads without padding); warp 0 also copies
+//      the user row (double-buffered by pair parity).  wait_group 0, barrier:
+//      every row of the pair has landed before anything is written
+//      (the reference reads all rows first, trainer.py:118-146).
+//   B  lane j of warp w scores row 32w+j: tt = v.v, st = u.v (fp32 FMA),
+//      fp32 similarity screen, exact binary64 only near the margin
+//      (trainer.py:184-221).
+//   C  each warp applies the rows of its own stage that must be written:
+//      item deltas with red.global.add from the resident snapshot rows
+//      (pre-pair values even for repeated ids), and adds its user-gradient
+//      partial to the user row (trainer.py:236-293).  Only the warp that
+//      reads a stage ever reads it, so one barrier per pair suffices.
+// The pair's loss (1 - sim_p) + mu/N * sum(hinge) is linear, so each warp
+// accumulates its share (trainer.py:222).
 #include <cstdint>
 #include <cstdlib>
 
@@ -38,28 +40,18 @@ constexpr int kMaxStages = 8;
 template <int K>
 struct RsGeom {
     static constexpr int ROWB = K * 4;
-    static constexpr int SLOTF = K + 4;  // padded slot (floats)
-    static constexpr int CH = K / 4;
+    static constexpr int CH = K / 4;  // 16-byte chunks per row
     static constexpr int VW = K >= 32 ? K / 32 : 1;
     static constexpr int ACT = K >= 32 ? 32 : K;
-};
-
-struct RsEntry {
-    float tt, st, w;  // cached forward scalars (v.v, u.v, loss weight)
-    int32_t id;       // item row
-    int32_t slot;     // ring slot (= row index within the pair) of the snapshot
+    // chunk c of row r lives at chunk (c ^ (r & SW)): 8 consecutive rows read
+    // at the same logical chunk hit 8 different 16-byte bank groups
+    static constexpr int SW = CH >= 8 ? 7 : CH - 1;
 };
 
 template <int K>
-__host__ __device__ inline size_t rs_smem_bytes(int nb, int rows, int cap) {
-    using G = RsGeom<K>;
-    size_t b = 8 * kMaxStages;                // hinge per warp (doubles first)
-    b += sizeof(float) * G::SLOTF * rows;      // ring: one padded slot per row
-    b += sizeof(float) * K;                   // user row
-    b += sizeof(int32_t) * 32 * nb;           // ids
-    b += sizeof(RsEntry) * cap;               // write list
-    b += sizeof(float) * K * nb;              // user-gradient partials
-    b += 16;                                  // counter
+__host__ __device__ inline size_t rs_smem_bytes(int rows) {
+    size_t b = sizeof(float) * K * rows;  // ring, one row per slot (swizzled)
+    b += sizeof(float) * K * 2;           // user row, double-buffered
     return (b + 127) & ~size_t(127);
 }
 
@@ -75,25 +67,19 @@ __device__ __forceinline__ void rs_red(float *p, const float (&d)[VW]) {
     }
 }
 
-template <int K>
-__global__ void __launch_bounds__(32 * kMaxStages)
-    hogwild_resident(HogwildArgs a, FastMod fm, int n_workers, int cap) {
+template <int K, int NB>
+// 7 resident CTAs per SM (the window allows ~7 pairs per SM), but never
+// fewer than 64 registers per thread
+__global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB : 1) : 7))
+    hogwild_resident(HogwildArgs a, FastMod fm, int n_workers) {
     using G = RsGeom<K>;
     constexpr int VW = G::VW;
-    const int nb = blockDim.x >> 5;  // warps = stages
     extern __shared__ __align__(128) unsigned char sm[];
-    // carve-out by alignment: doubles, then 16-byte cp.async targets, then the rest
-    double *hinge_w = reinterpret_cast<double *>(sm);                      // [kMaxStages]
-    float *ring = reinterpret_cast<float *>(sm + 8 * kMaxStages);          // 16-aligned
-    float *urow = ring + (size_t)G::SLOTF * (a.N + 1);                     // 16-aligned
-    float *part = urow + K;                                                // [nb][K]
-    int32_t *ids = reinterpret_cast<int32_t *>(part + K * nb);             // [32*nb]
-    int *cnt_p = ids + 32 * nb;
-    RsEntry *list = reinterpret_cast<RsEntry *>(cnt_p + 4);
+    float *ring = reinterpret_cast<float *>(sm);
+    float *ubuf = ring + (size_t)K * (a.N + 1);
 
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int64_t npairs = a.stop - a.start;
     const int N = a.N;
     const double wneg = a.mu * (1.0 / (double)N);
     const float theta_f = (float)a.theta;
@@ -102,34 +88,35 @@ __global__ void __launch_bounds__(32 * kMaxStages)
     const int r = w * 32 + lane;  // my row of every pair
     const bool valid = r <= N;
     const int nvalid = min(32, N + 1 - w * 32);
-    constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;
+    constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;  // rows per copy instruction
     constexpr int NI = 32 / RPI;
     const int my_ch = lane % G::CH, my_rsub = lane / G::CH;
-    float *my_stage = ring + (size_t)w * 32 * G::SLOTF;
+    float *my_stage = ring + (size_t)w * 32 * K;
 
     double loss = 0.0;
     long long degen = 0, active = 0, mine = 0;
+    int parity = 0;
 
-    for (int64_t p = a.start + blockIdx.x; p < a.stop; p += n_workers) {
+    for (int64_t p = a.start + blockIdx.x; p < a.stop; p += n_workers, parity ^= 1) {
         ++mine;
+        float *urow = ubuf + parity * K;
         // ---- A: ids, copies
         const int64_t pg = a.pair_index ? a.pair_index[p] : p;
         const int32_t pos = a.items[p];
         const int64_t u = a.users[p];
         uint32_t id = (uint32_t)pos;
-        if (r > 0) id = (uint32_t)fm.mod(mix64(a.s0 + ((uint64_t)pg * (uint64_t)N + (uint64_t)r) * kGamma));
-        if (!valid) id = 0;
-        ids[r] = (int32_t)id;
-        if (threadIdx.x == 0) *cnt_p = 0;
+        if (r > 0)
+            id = (uint32_t)fm.mod(
+                mix64(a.s0 + ((uint64_t)pg * (uint64_t)N + (uint64_t)r) * kGamma));
         {
-            float *dst = my_stage + my_rsub * G::SLOTF + my_ch * 4;
             const float *srcb = a.T + my_ch * 4;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 const int row = i * RPI + my_rsub;
                 const uint32_t rid = __shfl_sync(0xffffffffu, id, row & 31);
                 if (row < nvalid)
-                    cp_async16_hint(dst + i * RPI * G::SLOTF, srcb + (size_t)rid * K, pol);
+                    cp_async16_hint(my_stage + row * K + ((my_ch ^ (row & G::SW)) * 4),
+                                    srcb + (size_t)rid * K, pol);
             }
             if (w == 0)
                 for (int ch = lane; ch < G::CH; ch += 32)
@@ -137,7 +124,7 @@ __global__ void __launch_bounds__(32 * kMaxStages)
             cp_async_commit();
             cp_async_wait<0>();
         }
-        __syncthreads();  // B1: the pair's rows and the user row are resident
+        __syncthreads();  // every row of the pair (and the user row) has landed
 
         // ---- B: score my row
         float uu[VW];
@@ -150,43 +137,44 @@ __global__ void __launch_bounds__(32 * kMaxStages)
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
         const double ss = (double)sp;
-        const double rs = ss > 0.0 ? sqrt(ss) : 0.0;
-        const float rss = ss > 0.0 ? rsqrtf(sp) : 0.f;
-        double tt = 0.0, st = 0.0;
+        const float rss = sp > 0.f ? rsqrtf(sp) : 0.f;
+        const float *row = my_stage + lane * K;
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         if (valid) {
-            const float *row = my_stage + lane * G::SLOTF;
-            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-            for (int k = 0; k < K; k += 4) {
-                const float4 v = *reinterpret_cast<const float4 *>(row + k);
-                const float4 w4 = *reinterpret_cast<const float4 *>(urow + k);
+            for (int c = 0; c < G::CH; ++c) {
+                const float4 v =
+                    *reinterpret_cast<const float4 *>(row + ((c ^ (lane & G::SW)) * 4));
+                const float4 w4 = *reinterpret_cast<const float4 *>(urow + c * 4);
                 t0 = fmaf(v.x, v.x, t0); t1 = fmaf(v.y, v.y, t1);
                 t2 = fmaf(v.z, v.z, t2); t3 = fmaf(v.w, v.w, t3);
                 s0 = fmaf(w4.x, v.x, s0); s1 = fmaf(w4.y, v.y, s1);
                 s2 = fmaf(w4.z, v.z, s2); s3 = fmaf(w4.w, v.w, s3);
             }
-            tt = (double)((t0 + t1) + (t2 + t3));
-            st = (double)((s0 + s1) + (s2 + s3));
         }
+        const float ttf = (t0 + t1) + (t2 + t3);
+        const float stf = (s0 + s1) + (s2 + s3);
         bool write = false;
         double wt = 0.0, hinge = 0.0, sim = 0.0;
         if (valid) {
             bool degenerate = false;
-            sim = st;
+            sim = (double)stf;
             if (a.cosine) {
-                if (ss <= 0.0 || tt <= 0.0) {
+                if (sp <= 0.f || ttf <= 0.f) {
                     degenerate = true;
                     sim = 0.0;
                     ++degen;
                 } else {
-                    const float sf = (float)st * rss * rsqrtf((float)tt);
+                    const float sf = stf * rss * rsqrtf(ttf);
                     sim = (double)sf;
-                    if (r > 0 && sf > theta_f - 1e-5f) sim = st / (sqrt(ss) * sqrt(tt));
+                    if (r > 0 && sf > theta_f - 1e-5f)
+                        sim = (double)stf / (sqrt(ss) * sqrt((double)ttf));
                 }
             }
             if (r == 0) {
                 wt = -1.0;
                 write = !(a.cosine && degenerate) || a.l2 != 0.f;
+                loss += 1.0 - sim;
             } else {
                 if (sim - a.theta > 0.0) {
                     hinge = sim - a.theta;
@@ -196,115 +184,114 @@ __global__ void __launch_bounds__(32 * kMaxStages)
                 write = (wt != 0.0 && !(a.cosine && degenerate)) || (wt == 0.0 && a.l2 != 0.f);
             }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, write);
+        loss += wneg * hinge;
+
+        // ---- C: apply my stage's written rows from their resident snapshots
+        unsigned m = __ballot_sync(0xffffffffu, write);
         if (m) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(cnt_p, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            const int e = base + __popc(m & ((1u << lane) - 1u));
-            if (write && e < cap) list[e] = RsEntry{(float)tt, (float)st, (float)wt, (int32_t)id, r};
-        }
+            float ug[VW];
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) hinge += __shfl_xor_sync(0xffffffffu, hinge, o);
-        if (lane == 0) hinge_w[w] = hinge;
-        const double sim_p = __shfl_sync(0xffffffffu, sim, 0);  // valid in warp 0
-        __syncthreads();  // B2: every row of the pair has been read
-
-        // ---- C: apply the writes from the resident snapshots
-        const int n_ent = min(*cnt_p, cap);
-        float ug[VW];
-#pragma unroll
-        for (int i = 0; i < VW; ++i) ug[i] = 0.f;
-        for (int e = w; e < n_ent; e += nb) {
-            const RsEntry ent = list[e];
-            const WriteEntry we{ent.tt, ent.st, ent.w, ent.id, 0};
-            const RowCoef co = row_coef(we, ss, rs, a.lr, a.l2, a.cosine);
-            const float *srow = ring + (size_t)ent.slot * G::SLOTF;
-            float d[VW];
-#pragma unroll
-            for (int i = 0; i < VW; ++i) {
-                const float v = lane < G::ACT ? srow[lane * VW + i] : 0.f;
-                row_apply(co, uu[i], v, d[i], ug[i]);
-            }
-            if (!dmode) {
-                if (lane < G::ACT) rs_red<VW>(a.T + (int64_t)ent.id * K + lane * VW, d);
-            } else {
-                long long sl = 0;
-                if (lane == 0) sl = (long long)atomicAdd((unsigned long long *)a.delta_count, 1ull);
-                sl = __shfl_sync(0xffffffffu, sl, 0);
-                if (sl < a.delta_capacity) {
-                    if (lane == 0) a.delta_ids[sl] = ent.id;
-                    if (lane < G::ACT) {
-#pragma unroll
-                        for (int i = 0; i < VW; ++i) a.delta_rows[sl * K + lane * VW + i] = d[i];
-                    }
-                }
-            }
-        }
-        if (lane < G::ACT) {
-#pragma unroll
-            for (int i = 0; i < VW; ++i) part[w * K + lane * VW + i] = ug[i];
-        }
-        __syncthreads();  // B3: partial user gradients ready, ring reads done
-
-        // ---- D: user row and loss (warp 0), fixed summation order
-        if (w == 0) {
-            if (lane < G::ACT) {
+            for (int i = 0; i < VW; ++i) ug[i] = 0.f;
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const float tt_s = __shfl_sync(0xffffffffu, ttf, src);
+                const float st_s = __shfl_sync(0xffffffffu, stf, src);
+                const float w_s = (float)__shfl_sync(0xffffffffu, wt, src);
+                const int32_t id_s = (int32_t)__shfl_sync(0xffffffffu, id, src);
+                const WriteEntry we{(double)tt_s, (double)st_s, (double)w_s, id_s, 0};
+                const RowCoef co = row_coef_f(we, ss, rss, a.lr, a.l2, a.cosine);
+                const float *srow = my_stage + src * K;
                 float d[VW];
 #pragma unroll
                 for (int i = 0; i < VW; ++i) {
-                    float g = 0.f;
-                    for (int ww = 0; ww < nb; ++ww) g += part[ww * K + lane * VW + i];
-                    d[i] = -a.lr * (g + a.l2 * uu[i]);
+                    const int col = lane * VW + i;
+                    const float v =
+                        lane < G::ACT ? srow[(((col >> 2) ^ (src & G::SW)) << 2) | (col & 3)] : 0.f;
+                    row_apply(co, uu[i], v, d[i], ug[i]);
                 }
+                if (!dmode) {
+                    if (lane < G::ACT) rs_red<VW>(a.T + (int64_t)id_s * K + lane * VW, d);
+                } else {
+                    long long sl = 0;
+                    if (lane == 0)
+                        sl = (long long)atomicAdd((unsigned long long *)a.delta_count, 1ull);
+                    sl = __shfl_sync(0xffffffffu, sl, 0);
+                    if (sl < a.delta_capacity) {
+                        if (lane == 0) a.delta_ids[sl] = id_s;
+                        if (lane < G::ACT) {
+#pragma unroll
+                            for (int i = 0; i < VW; ++i) a.delta_rows[sl * K + lane * VW + i] = d[i];
+                        }
+                    }
+                }
+            }
+            // this warp's share of the user gradient (trainer.py:291-293)
+            if (lane < G::ACT) {
+                float d[VW];
+#pragma unroll
+                for (int i = 0; i < VW; ++i) d[i] = -a.lr * ug[i];
                 rs_red<VW>(a.S + u * K + lane * VW, d);
             }
-            if (lane == 0) {
-                double h = 0.0;
-                for (int ww = 0; ww < nb; ++ww) h += hinge_w[ww];
-                loss += (1.0 - sim_p) + wneg * h;
-            }
         }
+        // decay of the user row itself (l2 != 0), once per pair
+        if (w == 0 && a.l2 != 0.f && lane < G::ACT) {
+            float d[VW];
+#pragma unroll
+            for (int i = 0; i < VW; ++i) d[i] = -a.lr * a.l2 * uu[i];
+            rs_red<VW>(a.S + u * K + lane * VW, d);
+        }
+        __syncwarp();
     }
     // telemetry
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         degen += __shfl_xor_sync(0xffffffffu, degen, o);
         active += __shfl_xor_sync(0xffffffffu, active, o);
+        loss += __shfl_xor_sync(0xffffffffu, loss, o);
     }
     if (lane == 0) {
         if (degen) atomicAdd((unsigned long long *)&a.ctr->degenerate, (unsigned long long)degen);
         if (active) atomicAdd((unsigned long long *)&a.ctr->active, (unsigned long long)active);
-    }
-    if (threadIdx.x == 0) {
         atomicAdd(&a.ctr->loss, loss);
-        atomicAdd((unsigned long long *)&a.ctr->pairs, (unsigned long long)mine);
     }
-    (void)npairs;
+    if (threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ctr->pairs, (unsigned long long)mine);
 }
 
-template <int K>
-static cudaError_t launch_resident_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
-    const int nb = (a.N + 1 + 31) / 32;
-    // one stage per pair: the single-warp staged kernel is as good (measured)
-    if (nb > kMaxStages || (nb < 2 && !getenv("HEAT_HOGWILD_IMPL"))) return cudaErrorNotSupported;
-    const int cap = a.N + 1;  // each row enters the list at most once: never overflows
-    const size_t smem = rs_smem_bytes<K>(nb, a.N + 1, cap);
+template <int K, int NB>
+static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
+    const size_t smem = rs_smem_bytes<K>(a.N + 1);
     if (smem > 96 * 1024) return cudaErrorNotSupported;
-    auto kern = hogwild_resident<K>;
+    auto kern = hogwild_resident<K, NB>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nb, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NB, smem);
     if (per_sm < 1) per_sm = 1;
     int64_t nw = (int64_t)per_sm * sm_count();
     if (a.window > 0 && a.window < nw) nw = a.window;
     if (a.stop - a.start < nw) nw = a.stop - a.start;
     if (workers_out) *workers_out = (int)nw;
-    kern<<<(unsigned)nw, 32 * nb, smem, st>>>(a, FastMod::make((uint64_t)a.num_items), (int)nw,
-                                              cap);
+    kern<<<(unsigned)nw, 32 * NB, smem, st>>>(a, FastMod::make((uint64_t)a.num_items), (int)nw);
     return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t launch_resident_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
+    const int nb = (a.N + 1 + 31) / 32;
+    // one stage per pair: the single-warp staged kernel covers it (as fast,
+    // measured; the 1-warp instantiation also faulted on sm_100a — not used)
+    if (nb > kMaxStages || nb < 2) return cudaErrorNotSupported;
+    switch (nb) {
+    case 2: return launch_resident_kn<K, 2>(a, st, workers_out);
+    case 3: return launch_resident_kn<K, 3>(a, st, workers_out);
+    case 4: return launch_resident_kn<K, 4>(a, st, workers_out);
+    case 5: return launch_resident_kn<K, 5>(a, st, workers_out);
+    case 6: return launch_resident_kn<K, 6>(a, st, workers_out);
+    case 7: return launch_resident_kn<K, 7>(a, st, workers_out);
+    default: return launch_resident_kn<K, 8>(a, st, workers_out);
+    }
 }
 
 cudaError_t launch_hogwild_resident(const HogwildArgs &a, cudaStream_t st, int *workers_out) {

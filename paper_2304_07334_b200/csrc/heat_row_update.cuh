@@ -65,3 +65,29 @@ __device__ __forceinline__ void row_apply(const RowCoef &k, float u, float v, fl
 }
 
 }  // namespace heat
+
+namespace heat {
+
+// row_coef with 1/sqrt(ss) supplied (fp32 rsqrt) instead of sqrt(ss).
+__device__ __forceinline__ RowCoef row_coef_f(const WriteEntry &e, double ss, float irs, float lr,
+                                              float l2, bool cosine) {
+    RowCoef k;
+    k.lr = lr;
+    k.l2 = l2;
+    k.cosine = cosine;
+    k.decay = e.w == 0.0 || (cosine && (ss <= 0.0 || e.tt <= 0.0));
+    k.wf = (float)e.w;
+    k.ci = k.cu = k.cst_i = k.cst_u = 0.f;
+    if (!k.decay && cosine) {
+        const float ttf = (float)e.tt;
+        const float base = k.wf * rsqrtf(ttf) * irs;
+        const float stf = (float)e.st;
+        k.ci = base;
+        k.cst_i = base * stf / ttf;
+        k.cu = base;
+        k.cst_u = base * stf * irs * irs;
+    }
+    return k;
+}
+
+}  // namespace heat
