@@ -1,0 +1,58 @@
+"""install() against the real reference package, when it is importable
+(build container only: /root/reference is absent on the GPU box).  Checks the
+rebinding itself on CPU; the GPU run of heatcf.train through the patched
+entry points is exercised where both exist."""
+
+import importlib
+import os
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture
+def heatcf_mod(monkeypatch):
+    if not os.path.isdir(REF):
+        pytest.skip("reference not present")
+    monkeypatch.setenv("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    monkeypatch.setenv("PYTHONDONTWRITEBYTECODE", "1")
+    sys.dont_write_bytecode = True
+    monkeypatch.syspath_prepend(REF)
+    try:
+        return importlib.import_module("heatcf")
+    except Exception as exc:  # pragma: no cover
+        pytest.skip(f"heatcf not importable: {exc}")
+
+
+def test_install_rebinds_and_uninstall_restores(heatcf_mod):
+    import heatcf.evaluator
+    import heatcf.trainer
+    from paper_2304_07334_b200 import evaluator, trainer
+    from paper_2304_07334_b200.install import install, uninstall
+    orig_te, orig_ev = heatcf.trainer.train_epoch, heatcf.evaluator.evaluate
+    install(heatcf_mod)
+    try:
+        assert heatcf.trainer.train_epoch is trainer.train_epoch
+        assert heatcf.evaluator.evaluate is evaluator.evaluate
+        assert heatcf_mod.train_epoch is trainer.train_epoch
+    finally:
+        uninstall()
+    assert heatcf.trainer.train_epoch is orig_te
+    assert heatcf.evaluator.evaluate is orig_ev
+
+
+def test_reference_objects_flow_through_validation(heatcf_mod):
+    """heatcf's own dataclasses are accepted (duck typing) and validated in
+    the reference's order before any device work."""
+    from paper_2304_07334_b200.trainer import train_epoch
+    train = heatcf_mod.dataset.from_user_lists({0: [1]}, num_users=2, num_items=3)
+    S = heatcf_mod.init_matrix(2, 8, heatcf_mod.InitSpec(seed=1))
+    T = heatcf_mod.init_matrix(3, 8, heatcf_mod.InitSpec(seed=2))
+    with pytest.raises(ValueError):
+        train_epoch(S, T, train, heatcf_mod.TrainingConfig(emb_dim=4, num_negatives=1))
+    with pytest.raises(ValueError):
+        train_epoch(S, T, train, heatcf_mod.TrainingConfig(
+            emb_dim=8, num_negatives=1,
+            sampler=heatcf_mod.SamplerConfig(kind="tiling", tile_size=2, refresh_interval=2)))
