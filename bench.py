@@ -168,19 +168,33 @@ def run_reference(args):
     return 0
 
 
+def _ncu_traffic(config: str):
+    """DRAM bytes per launch of the Hogwild kernel from the committed ncu
+    summary (profiles/ncu_<config>.json, written from an `ncu --set full`
+    capture of this bench command), or None."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20, help="timed epochs")
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact"])
     ap.add_argument("--window", type=int, default=0, help="pairs in flight (0: config batch)")
     ap.add_argument("--fp64", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="user-sharded path even at N=1")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
     args.e2e_steps = max(0, args.e2e_steps)
     if args.impl == "reference":
@@ -202,80 +216,132 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    sharded = world > 1 or args.sharded
 
     train, test, spec, S, T = build_workload(args.config)
     window = args.window or spec.batch
     mode = N.MODE_HOGWILD if args.mode == "hogwild" else N.MODE_EXACT
     K, NN = spec.dim, spec.negatives
     total_epochs = args.warmup + args.steps
-    # replicas only for now: every rank trains its own copy of the workload
-    pairs_host = [epoch_pairs(train, shuffle_seed(0, e)) for e in range(total_epochs)]
+    npairs = train.num_pairs
     model = DeviceModel(S.values, T.values, dev)
-    pairs_dev = [model.upload_pairs(u, i) for u, i in pairs_host]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    npairs = len(pairs_host[0][0])
     stream = torch.cuda.current_stream(dev)
 
-    def one_epoch(e, timed):
-        p = model.params(n_neg=NN, lr=spec.learning_rate, l2=0.0, mu=spec.mu,
-                         theta=spec.theta, cosine=True, mode=mode,
-                         stream_base=epoch_stream(0, e), window=window, fp64=args.fp64)
-        model.counters.reset()
-        flush.zero_()  # L2 flush between steps (outside the timed region)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        du, di = pairs_dev[e]
-        model.train_range(du, di, 0, npairs, p)
-        ev1.record(stream)
-        ev1.synchronize()
-        c = model.counters.read()
-        return ev0.elapsed_time(ev1) / 1e3, c
+    def params(e):
+        return model.params(n_neg=NN, lr=spec.learning_rate, l2=0.0, mu=spec.mu,
+                            theta=spec.theta, cosine=True, mode=mode,
+                            stream_base=epoch_stream(0, e), window=window, fp64=args.fp64)
+
+    launches_per_epoch = 1
+    if not sharded:
+        pairs_dev = []
+        for e in range(total_epochs):  # inputs resident in HBM before timing
+            u, i = epoch_pairs(train, shuffle_seed(0, e))
+            pairs_dev.append(model.upload_pairs(u, i))
+
+        def one_epoch(e):
+            model.counters.reset()
+            flush.zero_()  # L2 flush between steps, outside the timed region
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            du, di = pairs_dev[e]
+            model.train_range(du, di, 0, npairs, params(e))
+            ev1.record(stream)
+            ev1.synchronize()
+            return ev0.elapsed_time(ev1) / 1e3, model.counters.read()
+    else:
+        from paper_2304_07334_b200.parallel import ShardedTrainer, exchange_deltas
+        trainer = ShardedTrainer(model, world, rank)
+        host_pairs = [epoch_pairs(train, shuffle_seed(0, e)) for e in range(total_epochs)]
+
+        def one_epoch(e):
+            nonlocal launches_per_epoch
+            u, i = host_pairs[e]
+            trainer.prepare_epoch(u, i, params(e), spec.batch)  # shard upload, untimed
+            model.counters.reset()
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            nl = 0
+            for s in range(trainer.num_steps):
+                d_ids, d_rows, count = trainer.local_step(s)
+                nl += 1
+                if world > 1:
+                    all_ids, all_rows, valid = exchange_deltas(d_ids, d_rows, count)
+                else:
+                    all_ids, all_rows = d_ids[:count], d_rows[:count]
+                    valid = torch.ones(count, dtype=torch.bool, device=dev)
+                trainer.apply_ordered(all_ids, all_rows, valid)
+                nl += 1
+            ev1.record(stream)
+            ev1.synchronize()
+            launches_per_epoch = nl
+            return ev0.elapsed_time(ev1) / 1e3, model.counters.read()
 
     for e in range(args.warmup):
-        one_epoch(e, False)
+        one_epoch(e)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    times, actives, losses = [], [], []
+    times, actives, losses, pairs_done = [], [], [], []
     for s in range(args.steps):
-        dt, c = one_epoch(args.warmup + s, True)
+        dt, c = one_epoch(args.warmup + s)
         times.append(dt)
         actives.append(c.active)
-        losses.append(c.loss / npairs)
+        losses.append(c.loss)
+        pairs_done.append(c.pairs)
     torch.cuda.synchronize()
     clk = clocks.stop()
     total = sum(times)
+    act_total = float(np.sum(actives))
+    loss_total = float(np.sum(losses))
     if world > 1:
         t = torch.tensor([total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
+        agg = torch.tensor([act_total, loss_total, float(sum(pairs_done))], dtype=torch.float64,
+                           device=dev)
+        dist.all_reduce(agg)
+        act_total, loss_total = float(agg[0]), float(agg[1])
+        assert int(agg[2]) == npairs * args.steps, "every pair trained exactly once"
         dist.barrier()
-    value = world * npairs * args.steps / total
+    value = npairs * args.steps / total  # whole job: every pair of every timed epoch
     kernel_s = total / args.steps
-    bytes_per_epoch = algorithmic_bytes(npairs, K, NN, int(np.mean(actives)))
+    bytes_per_epoch = algorithmic_bytes(npairs, K, NN, int(act_total / args.steps))
     peak, peak_kind = _peaks()
-    achieved = bytes_per_epoch / kernel_s / 1e9
+    achieved = bytes_per_epoch / kernel_s / 1e9 / world  # per GPU, vs the per-GPU peak
 
-    # e2e: the public drop-in API with host numpy tables
-    configure(mode=args.mode, window=window, fp64=args.fp64)
-    cfg = train_config(spec, threads=8 if args.mode == "hogwild" else 1)
-    Se, Te = S.copy(), T.copy()
-    if args.e2e_steps:
+    # e2e: the public drop-in API with host numpy tables (1 GPU path)
+    e2e = None
+    if not sharded and args.e2e_steps:
+        configure(mode=args.mode, window=window, fp64=args.fp64)
+        cfg = train_config(spec, threads=8 if args.mode == "hogwild" else 1)
+        Se, Te = S.copy(), T.copy()
         train_epoch(Se, Te, train, cfg, epoch=0)
-    torch.cuda.synchronize()
-    e2e_times = []
-    for e in range(args.e2e_steps):
+        train_epoch(Se, Te, train, cfg, epoch=1)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        train_epoch(Se, Te, train, cfg, epoch=1 + e)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_value = world * npairs / float(np.mean(e2e_times)) if e2e_times else None
-    h2d = S.values.nbytes + T.values.nbytes + 8 * npairs
-    d2h = S.values.nbytes + T.values.nbytes
+        for e in range(args.e2e_steps):
+            rep = train_epoch(Se, Te, train, cfg, epoch=2 + e)
+            assert np.isfinite(rep.mean_loss)  # the step's result, read back on the host
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": npairs / e2e_s, "unit": "samples/s",
+               "h2d_bytes_per_step": S.values.nbytes + T.values.nbytes + 8 * npairs,
+               "d2h_bytes_per_step": S.values.nbytes + T.values.nbytes + 32,
+               "path": "paper_2304_07334_b200.train_epoch (host numpy S/T, shuffle, H2D, "
+                       "kernel, D2H), steady state over consecutive epochs"}
+    elif sharded and args.e2e_steps:
+        e2e = {"value": None, "unit": "samples/s", "h2d_bytes_per_step": None,
+               "d2h_bytes_per_step": None, "note": "sharded e2e not measured this round"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         sample = {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 20_000, "c5": 20_000}[spec.name]
         cpu_baseline(spec, train, S.values, T.values, 20000, threads)  # warm
@@ -283,31 +349,33 @@ def main():
         cpu.pop("seconds", None)
 
     if rank == 0:
+        prof = _ncu_traffic(spec.name)
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64" if args.fp64 else "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32", "data": "synthetic",
             "config": {"workload": spec.name, "users": train.num_users,
                        "items": train.num_items, "train_pairs": npairs, "dim": K,
                        "negatives": NN, "theta": spec.theta, "mu": spec.mu,
                        "batch": spec.batch, "window": window, "mode": args.mode,
                        "lr": spec.learning_rate, "step": "one epoch",
-                       "l2_flush": "512 MiB write between steps; S+T "
-                                   f"{(S.values.nbytes + T.values.nbytes) / 1e6:.1f} MB"
-                                   " re-read from HBM each step",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single"},
+                       "l2_flush": "512 MiB write before every timed epoch; S+T "
+                                   f"{(S.values.nbytes + T.values.nbytes) / 1e6:.1f} MB",
+                       "parallelism": (f"users sharded x{world}, item-delta all-gather"
+                                       if sharded else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None,
+                         "traffic": prof.get("dram_bytes_per_launch") if prof else None,
+                         "traffic_source": prof.get("source") if prof else None,
+                         "l2_hit_rate_pct": prof.get("l2_hit_rate_pct") if prof else None,
                          "bytes_per_launch": bytes_per_epoch,
-                         "active_negatives_per_pair": float(np.mean(actives)) / npairs},
+                         "active_negatives_per_pair": act_total / args.steps / npairs},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "gpu_launches": args.steps,
+            "e2e": e2e,
+            "gpu_launches": launches_per_epoch * args.steps,
             "clocks": clk,
-            "mean_loss": float(np.mean(losses)),
+            "mean_loss": loss_total / args.steps / npairs,
         }
         print(json.dumps(line))
     if world > 1:

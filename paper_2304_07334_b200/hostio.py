@@ -51,7 +51,7 @@ class PairPrefetcher:
 
     def release(self, bufs) -> None:
         with self._lock:
-            if len(self._pool) < 4:
+            if len(self._pool) < 6:
                 self._pool.append(bufs)
 
     def _compute(self, train, seed: int, bufs):
@@ -70,15 +70,18 @@ class PairPrefetcher:
                 return holder["bufs"]
         return self._compute(train, seed, self._buffers(train.num_pairs))
 
+    MAX_PENDING = 3
+
     def prefetch(self, train, seed: int) -> None:
         key = (_train_key(train), seed)
         with self._lock:
             if key in self._pending:
                 return
-            # keep only the newest look-ahead
-            stale = list(self._pending.items())
-            self._pending.clear()
-        for _, (th, holder) in stale:
+            stale = []
+            while len(self._pending) >= self.MAX_PENDING:  # drop the oldest look-ahead
+                old = next(iter(self._pending))
+                stale.append(self._pending.pop(old))
+        for th, holder in stale:
             th.join()
             if "bufs" in holder:
                 self.release(holder["bufs"])

@@ -173,7 +173,8 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     t_start = time.perf_counter()
     model = _session_model(S.values, T.values)  # raises without CUDA: no CPU fallback
     bufs = PREFETCH.get(train, shuffle_seed(cfg.seed, epoch))
-    PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + 1))
+    for ahead in (1, 2):  # two host threads keep the next orders coming
+        PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + ahead))
     dev = model.device
     stream = torch.cuda.current_stream(dev)
     pin_array(S.values)
