@@ -95,9 +95,15 @@ class ClockSampler:
 
 
 def build_workload(name: str):
+    """Synthetic stand-in of a BASELINE config.  c5 keeps its full 10 M x 2 M
+    tables (5.1 GB + 1.0 GB: the HBM-bound case) with interactions generated
+    for a seeded 2 % of the users (10 M of its 500 M interactions)."""
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.synth import make_dataset
-    train, test, spec = make_dataset(name)
+    if name == "c5":
+        train, test, spec = make_dataset(name, sample_users=0.02)
+    else:
+        train, test, spec = make_dataset(name)
     S = init_matrix(train.num_users, spec.dim, InitSpec(seed=0))
     T = init_matrix(train.num_items, spec.dim, InitSpec(seed=0))
     return train, test, spec, S, T

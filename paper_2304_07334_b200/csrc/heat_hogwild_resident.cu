@@ -11,8 +11,8 @@
 // Per pair (math = trainer.py:114-293, Hogwild across CTAs):
 //   A  every warp draws its stage's negative ids (counter-form SplitMix64,
 //      one draw per lane) and copies its rows with per-lane 16-byte
-//      cp.async.cg (LDGSTS, L2 evict-last hint) into an XOR-swizzled ring
-//      (conflict-free lane-per-row reads without padding); warp 0 also copies
+//      cp.async.cg (LDGSTS, L2 evict-last hint) into a padded ring
+//      (rows padded by 16 bytes: conflict-free lane-per-row reads); warp 0 also copies
 //      the user row (double-buffered by pair parity).  wait_group 0, barrier:
 //      every row of the pair has landed before anything is written
 //      (the reference reads all rows first, trainer.py:118-146).
@@ -43,14 +43,15 @@ struct RsGeom {
     static constexpr int CH = K / 4;  // 16-byte chunks per row
     static constexpr int VW = K >= 32 ? K / 32 : 1;
     static constexpr int ACT = K >= 32 ? 32 : K;
-    // chunk c of row r lives at chunk (c ^ (r & SW)): 8 consecutive rows read
-    // at the same logical chunk hit 8 different 16-byte bank groups
-    static constexpr int SW = CH >= 8 ? 7 : CH - 1;
+    // rows padded by 16 bytes: lane j reading row j at the same chunk hits
+    // bank group (j * (K/4 + 1)) mod 8 — conflict-free LDS.128, constant
+    // offsets (an XOR swizzle saves 1.6 KB but costs ~400 instructions/pair)
+    static constexpr int SLOTF = K + 4;
 };
 
 template <int K>
 __host__ __device__ inline size_t rs_smem_bytes(int rows) {
-    size_t b = sizeof(float) * K * rows;  // ring, one row per slot (swizzled)
+    size_t b = sizeof(float) * RsGeom<K>::SLOTF * rows;  // ring, one padded slot per row
     b += sizeof(float) * K * 2;           // user row, double-buffered
     return (b + 127) & ~size_t(127);
 }
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     constexpr int VW = G::VW;
     extern __shared__ __align__(128) unsigned char sm[];
     float *ring = reinterpret_cast<float *>(sm);
-    float *ubuf = ring + (size_t)K * (a.N + 1);
+    float *ubuf = ring + (size_t)G::SLOTF * (a.N + 1);
 
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
@@ -91,23 +92,40 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;  // rows per copy instruction
     constexpr int NI = 32 / RPI;
     const int my_ch = lane % G::CH, my_rsub = lane / G::CH;
-    float *my_stage = ring + (size_t)w * 32 * K;
+    float *my_stage = ring + (size_t)w * 32 * G::SLOTF;
 
     double loss = 0.0;
     long long degen = 0, active = 0, mine = 0;
     int parity = 0;
+    // counter-form SplitMix64: draw (pg*N + r - 1) of the epoch stream has
+    // state s0 + (pg*N + r) * GAMMA = s0 + pg*(N*GAMMA) + r*GAMMA
+    const uint64_t lane_off = (uint64_t)r * kGamma;
+    const uint64_t pair_step = (uint64_t)N * kGamma;
+    // pair metadata one pair ahead, so no dependent global load sits at the
+    // head of a pair
+    int64_t p = a.start + blockIdx.x;
+    int32_t nx_pos = 0, nx_u = 0;
+    int64_t nx_pg = 0;
+    if (p < a.stop) {
+        nx_pos = a.items[p];
+        nx_u = a.users[p];
+        nx_pg = a.pair_index ? a.pair_index[p] : p;
+    }
 
-    for (int64_t p = a.start + blockIdx.x; p < a.stop; p += n_workers, parity ^= 1) {
+    for (; p < a.stop; p += n_workers, parity ^= 1) {
         ++mine;
         float *urow = ubuf + parity * K;
         // ---- A: ids, copies
-        const int64_t pg = a.pair_index ? a.pair_index[p] : p;
-        const int32_t pos = a.items[p];
-        const int64_t u = a.users[p];
+        const int32_t pos = nx_pos;
+        const int64_t u = nx_u;
+        const int64_t pg = nx_pg;
+        if (p + n_workers < a.stop) {
+            nx_pos = a.items[p + n_workers];
+            nx_u = a.users[p + n_workers];
+            nx_pg = a.pair_index ? a.pair_index[p + n_workers] : p + n_workers;
+        }
         uint32_t id = (uint32_t)pos;
-        if (r > 0)
-            id = (uint32_t)fm.mod(
-                mix64(a.s0 + ((uint64_t)pg * (uint64_t)N + (uint64_t)r) * kGamma));
+        if (r > 0) id = (uint32_t)fm.mod(mix64(a.s0 + (uint64_t)pg * pair_step + lane_off));
         {
             const float *srcb = a.T + my_ch * 4;
 #pragma unroll
@@ -115,7 +133,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
                 const int row = i * RPI + my_rsub;
                 const uint32_t rid = __shfl_sync(0xffffffffu, id, row & 31);
                 if (row < nvalid)
-                    cp_async16_hint(my_stage + row * K + ((my_ch ^ (row & G::SW)) * 4),
+                    cp_async16_hint(my_stage + row * G::SLOTF + my_ch * 4,
                                     srcb + (size_t)rid * K, pol);
             }
             if (w == 0)
@@ -138,13 +156,12 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
         for (int o = 16; o >= 1; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
         const double ss = (double)sp;
         const float rss = sp > 0.f ? rsqrtf(sp) : 0.f;
-        const float *row = my_stage + lane * K;
+        const float *row = my_stage + lane * G::SLOTF;
         float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         if (valid) {
 #pragma unroll
             for (int c = 0; c < G::CH; ++c) {
-                const float4 v =
-                    *reinterpret_cast<const float4 *>(row + ((c ^ (lane & G::SW)) * 4));
+                const float4 v = *reinterpret_cast<const float4 *>(row + c * 4);
                 const float4 w4 = *reinterpret_cast<const float4 *>(urow + c * 4);
                 t0 = fmaf(v.x, v.x, t0); t1 = fmaf(v.y, v.y, t1);
                 t2 = fmaf(v.z, v.z, t2); t3 = fmaf(v.w, v.w, t3);
@@ -201,13 +218,12 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
                 const int32_t id_s = (int32_t)__shfl_sync(0xffffffffu, id, src);
                 const WriteEntry we{(double)tt_s, (double)st_s, (double)w_s, id_s, 0};
                 const RowCoef co = row_coef_f(we, ss, rss, a.lr, a.l2, a.cosine);
-                const float *srow = my_stage + src * K;
+                const float *srow = my_stage + src * G::SLOTF;
                 float d[VW];
 #pragma unroll
                 for (int i = 0; i < VW; ++i) {
                     const int col = lane * VW + i;
-                    const float v =
-                        lane < G::ACT ? srow[(((col >> 2) ^ (src & G::SW)) << 2) | (col & 3)] : 0.f;
+                    const float v = lane < G::ACT ? srow[col] : 0.f;
                     row_apply(co, uu[i], v, d[i], ug[i]);
                 }
                 if (!dmode) {

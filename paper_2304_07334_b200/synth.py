@@ -145,15 +145,29 @@ def _distinct_draws(rng, cdf, users_rep: np.ndarray, need: np.ndarray, num_items
 
 def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
                  test_fraction: float | None = None, users_per_block: int = 200_000,
-                 scale: float = 1.0):
-    """(train, test, spec) for a workload.  ``scale`` < 1 shrinks the user
-    count and interaction target proportionally (for fast tests)."""
+                 scale: float = 1.0, sample_users: float | None = None):
+    """(train, test, spec) for a workload.
+
+    ``scale`` < 1 shrinks the user count and interaction target together
+    (small, fast variants for tests).  ``sample_users`` = f keeps the FULL
+    user universe (so S keeps its size and its random-access footprint) but
+    generates interactions for a seeded random fraction f of the users only —
+    the config-5 stand-in (10 M x 2 M tables, 5.1 GB + 1.0 GB, far beyond L2)
+    without generating all 500 M interactions on the host."""
     if isinstance(spec, str):
         spec = CONFIGS[spec]
     tf = spec.test_fraction if test_fraction is None else test_fraction
-    num_users = max(1, int(round(spec.num_users * scale)))
-    target = max(num_users, int(round(spec.interactions * scale)))
     rng = np.random.Generator(np.random.PCG64(gen_seed))
+    if sample_users is not None:
+        universe = spec.num_users
+        num_users = max(1, int(round(universe * sample_users)))
+        target = max(num_users, int(round(spec.interactions * sample_users)))
+        user_ids = np.sort(rng.choice(universe, size=num_users, replace=False)).astype(np.int64)
+    else:
+        universe = None
+        num_users = max(1, int(round(spec.num_users * scale)))
+        target = max(num_users, int(round(spec.interactions * scale)))
+        user_ids = None
     deg = _fit_degrees(rng, spec, num_users, target)
     rank_to_id = rng.permutation(spec.num_items).astype(np.int64)
     cdf = _zipf_cdf(spec.num_items, spec.zipf_s)
@@ -162,7 +176,7 @@ def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
         b1 = min(num_users, b0 + users_per_block)
         need = deg[b0:b1]
         lu, lr = _distinct_draws(rng, cdf, None, need, spec.num_items)
-        users = lu + b0
+        users = lu + b0 if user_ids is None else user_ids[lu + b0]
         items = rank_to_id[lr]
         if tf > 0:
             d = need[lu]
@@ -182,11 +196,12 @@ def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
         else:
             tr_u.append(users)
             tr_i.append(items)
-    train = from_pairs(np.concatenate(tr_u), np.concatenate(tr_i), num_users, spec.num_items)
+    nu = num_users if universe is None else universe
+    train = from_pairs(np.concatenate(tr_u), np.concatenate(tr_i), nu, spec.num_items)
     if tf > 0:
-        test = from_pairs(np.concatenate(te_u), np.concatenate(te_i), num_users, spec.num_items)
+        test = from_pairs(np.concatenate(te_u), np.concatenate(te_i), nu, spec.num_items)
     else:
-        test = InteractionSet(num_users, spec.num_items, np.zeros(num_users + 1, np.int64),
+        test = InteractionSet(nu, spec.num_items, np.zeros(nu + 1, np.int64),
                               np.empty(0, np.int32))
     return train, test, spec
 
