@@ -274,11 +274,14 @@ def main():
             ev0.record(stream)
             nl = 0
             for s in range(trainer.num_steps):
-                d_ids, d_rows, count = trainer.local_step(s)
-                nl += 1
                 if world > 1:
-                    all_ids, all_rows, valid = exchange_deltas(d_ids, d_rows, count)
+                    d_ids, d_rows, d_cnt = trainer.local_step(s, sync=False)
+                    nl += 1
+                    all_ids, all_rows, valid = exchange_deltas(d_ids, d_rows, d_cnt,
+                                                               capacity=trainer.cap)
                 else:
+                    d_ids, d_rows, count = trainer.local_step(s)
+                    nl += 1
                     all_ids, all_rows = d_ids[:count], d_rows[:count]
                     valid = torch.ones(count, dtype=torch.bool, device=dev)
                 trainer.apply_ordered(all_ids, all_rows, valid)

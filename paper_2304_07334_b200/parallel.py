@@ -79,15 +79,25 @@ def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group=None) -> None:
         dist.all_gather(parts, inp, group=group)
 
 
-def exchange_deltas(ids: torch.Tensor, rows: torch.Tensor, count: int, group=None):
+def exchange_deltas(ids: torch.Tensor, rows: torch.Tensor, count, group=None,
+                    capacity: int | None = None):
     """All-gather every rank's delta log.  Returns (ids, rows, valid) of the
-    rank-major concatenation, padded to world * max_count entries."""
+    rank-major concatenation, padded to world * max_count entries.
+
+    `count` may be a host int or the kernel's device counter (int64[1]); with
+    the device counter the only host synchronisation of the step is reading
+    the gathered counts.  Raises if any rank's log overflowed `capacity`."""
     world = dist.get_world_size(group)
     dev = ids.device
-    cnt = torch.tensor([count], dtype=torch.int64, device=dev)
+    cnt = count if torch.is_tensor(count) else torch.tensor([count], dtype=torch.int64,
+                                                              device=dev)
     counts = torch.empty(world, dtype=torch.int64, device=dev)
-    _all_gather_flat(counts, cnt, group)
-    cmax = int(counts.max().item())
+    _all_gather_flat(counts, cnt.reshape(1), group)
+    host_counts = counts.cpu()  # the step's single host sync
+    cmax = int(host_counts.max())
+    if capacity is not None and cmax > capacity:
+        raise RuntimeError(f"delta log overflow ({cmax} > {capacity} entries on some rank); "
+                           "raise the capacity margin")
     K = rows.shape[1]
     if cmax == 0:
         z = torch.empty(0, dtype=ids.dtype, device=dev)
@@ -100,6 +110,7 @@ def exchange_deltas(ids: torch.Tensor, rows: torch.Tensor, count: int, group=Non
     _all_gather_flat(all_rows, send_rows, group)
     pos = torch.arange(cmax, device=dev).repeat(world)
     valid = pos < counts.repeat_interleave(cmax)
+    valid.n_valid = int(host_counts.sum())  # known on the host: no second sync
     return all_ids, all_rows, valid
 
 
@@ -133,7 +144,9 @@ class ShardedTrainer:
         if all_ids.numel() == 0:
             return
         order = merge_order(all_ids, valid)
-        n_valid = int(valid.sum().item())
+        n_valid = getattr(valid, "n_valid", None)
+        if n_valid is None:
+            n_valid = int(valid.sum().item())
         ids_s = all_ids[order][:n_valid].contiguous()
         rows_s = all_rows[order][:n_valid].contiguous()
         cnt = torch.tensor([n_valid], dtype=torch.int64, device=ids_s.device)
@@ -161,14 +174,17 @@ class ShardedTrainer:
     def num_steps(self) -> int:
         return len(self.bounds) - 1
 
-    def local_step(self, s: int):
-        """Run step s on this rank's pairs; returns (ids, rows, count) of the log."""
+    def local_step(self, s: int, sync: bool = True):
+        """Run step s on this rank's pairs; returns (ids, rows, count) of the
+        log — count as a host int (sync=True) or as the device counter."""
         d_ids, d_rows, d_cnt = self._buf
         a, b = int(self.bounds[s]), int(self.bounds[s + 1])
         d_cnt.zero_()
         if b > a:
             self.model.train_range(self.lu, self.li, a, b, self.params,
                                    delta=(d_ids, d_rows, d_cnt, self.cap), pair_index=self.lp)
+        if not sync:
+            return d_ids, d_rows, d_cnt
         count = int(d_cnt.item())
         if count > self.cap:
             raise RuntimeError(f"delta log overflow ({count} > {self.cap} entries); "
@@ -181,10 +197,11 @@ class ShardedTrainer:
         self.prepare_epoch(ep_users, ep_items, params, step_pairs)
         stats = []
         for s in range(self.num_steps):
-            d_ids, d_rows, count = self.local_step(s)
-            all_ids, all_rows, valid = exchange_deltas(d_ids, d_rows, count, self.group)
+            d_ids, d_rows, d_cnt = self.local_step(s, sync=False)
+            all_ids, all_rows, valid = exchange_deltas(d_ids, d_rows, d_cnt, self.group,
+                                                       capacity=self.cap)
             self.apply_ordered(all_ids, all_rows, valid)
-            stats.append(StepStats(count, count * (4 * self.model.dim + 4)))
+            stats.append(StepStats(valid.n_valid, valid.n_valid * (4 * self.model.dim + 4)))
         return stats
 
 
