@@ -65,17 +65,34 @@ void ho_sample_negatives(uint64_t *state, int64_t npairs, int n_neg, int64_t num
 }
 
 typedef struct {
-    /* per-thread scratch, trainer.py:334-363 (agg/tile buffers dropped) */
+    /* per-thread scratch, trainer.py:334-363 (tile buffers dropped) */
     int K, n_neg;
-    double *ubuf, *ugrad, *tts, *sts, *sims, *dnegs;
+    double *ubuf, *ugrad, *tts, *sts, *sims, *dnegs, *pooled, *wh;
     float *pos_buf, *neg_buf;
     int32_t *neg_ids;
 } ho_scratch;
+
+/* Behaviour aggregation (aggregator.py:30-113, in-loop copy trainer.py:148-173
+ * and 299-331).  accu (K*K f64) and counter are the per-thread state that
+ * persists across chunks of an epoch (_ThreadState.agg_accu / agg_ctr). */
+typedef struct {
+    int on;
+    float *W;                 /* K x K, input-major: W[k*K + j] */
+    const int64_t *tr_offsets;
+    const int32_t *tr_items;
+    double gamma, lr;
+    int64_t mb_size, max_history;
+    int hist_prop;
+    double *accu;
+    int64_t *counter;
+} ho_agg;
 
 static int scratch_init(ho_scratch *s, int K, int n_neg) {
     s->K = K;
     s->n_neg = n_neg;
     s->ubuf = calloc((size_t)K, sizeof(double));
+    s->pooled = calloc((size_t)K, sizeof(double));
+    s->wh = calloc((size_t)K, sizeof(double));
     s->ugrad = calloc((size_t)K, sizeof(double));
     s->tts = calloc((size_t)n_neg, sizeof(double));
     s->sts = calloc((size_t)n_neg, sizeof(double));
@@ -84,14 +101,14 @@ static int scratch_init(ho_scratch *s, int K, int n_neg) {
     s->pos_buf = calloc((size_t)K, sizeof(float));
     s->neg_buf = calloc((size_t)n_neg * K, sizeof(float));
     s->neg_ids = calloc((size_t)n_neg, sizeof(int32_t));
-    return s->ubuf && s->ugrad && s->tts && s->sts && s->sims && s->dnegs && s->pos_buf &&
+    return s->ubuf && s->pooled && s->wh && s->ugrad && s->tts && s->sts && s->sims && s->dnegs && s->pos_buf &&
                    s->neg_buf && s->neg_ids
                ? 0
                : -1;
 }
 
 static void scratch_free(ho_scratch *s) {
-    free(s->ubuf); free(s->ugrad); free(s->tts); free(s->sts); free(s->sims);
+    free(s->ubuf); free(s->pooled); free(s->wh); free(s->ugrad); free(s->tts); free(s->sts); free(s->sims);
     free(s->dnegs); free(s->pos_buf); free(s->neg_buf); free(s->neg_ids);
 }
 
@@ -103,7 +120,8 @@ static void scratch_free(ho_scratch *s) {
 static void train_chunk(float *S, float *T, const int32_t *ep_users, const int32_t *ep_items,
                         int64_t start, int64_t stop, int64_t num_items, uint64_t *rng_state,
                         int use_cosine, int n_neg, double lr, double l2, double mu, double theta,
-                        ho_scratch *s, double *loss_out, int64_t *degen_out, int64_t *active_out) {
+                        const ho_agg *ag, ho_scratch *s, double *loss_out, int64_t *degen_out,
+                        int64_t *active_out) {
     const int K = s->K;
     const double inv_n = 1.0 / n_neg;
     double *ubuf = s->ubuf, *ugrad = s->ugrad, *tts = s->tts, *sts = s->sts, *sims = s->sims,
@@ -120,7 +138,31 @@ static void train_chunk(float *S, float *T, const int32_t *ep_users, const int32
             neg_ids[j] = (int32_t)nid;
             for (int k = 0; k < K; ++k) neg_buf[(int64_t)j * K + k] = T[nid * K + k];
         }
-        for (int k = 0; k < K; ++k) ubuf[k] = (double)S[u * K + k];
+        if (!ag->on) {
+            for (int k = 0; k < K; ++k) ubuf[k] = (double)S[u * K + k];
+        }
+
+        /* aggregate forward: trainer.py:150-169 */
+        int64_t hb = 0, hist_len = 0;
+        double *pooled = s->pooled;
+        if (ag->on) {
+            hb = ag->tr_offsets[u];
+            int64_t he = ag->tr_offsets[u + 1];
+            if (he - hb > ag->max_history) he = hb + ag->max_history;
+            hist_len = he - hb;
+            for (int k = 0; k < K; ++k) pooled[k] = 0.0;
+            for (int64_t idx = hb; idx < he; ++idx) {
+                const int64_t hid = ag->tr_items[idx];
+                for (int k = 0; k < K; ++k) pooled[k] += (double)T[hid * K + k];
+            }
+            if (hist_len > 0)
+                for (int k = 0; k < K; ++k) pooled[k] /= (double)hist_len;
+            for (int j = 0; j < K; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < K; ++k) acc += pooled[k] * (double)ag->W[k * K + j];
+                ubuf[j] = ag->gamma * (double)S[u * K + j] + (1.0 - ag->gamma) * acc;
+            }
+        }
 
         /* similarity: trainer.py:176-207 */
         double ss = 0.0;
@@ -249,7 +291,45 @@ static void train_chunk(float *S, float *T, const int32_t *ep_users, const int32
             }
         }
         float *su = S + u * K;
-        for (int k = 0; k < K; ++k) su[k] = (float)((double)su[k] - lr * (ugrad[k] + l2 * (double)su[k]));
+        if (!ag->on) {
+            for (int k = 0; k < K; ++k)
+                su[k] = (float)((double)su[k] - lr * (ugrad[k] + l2 * (double)su[k]));
+        } else {
+            /* aggregate backward: trainer.py:301-328 */
+            const double gamma = ag->gamma;
+            for (int k = 0; k < K; ++k)
+                su[k] = (float)((double)su[k] - lr * (gamma * ugrad[k] + l2 * (double)su[k]));
+            for (int a = 0; a < K; ++a) {
+                const double pa = (1.0 - gamma) * pooled[a];
+                if (pa != 0.0)
+                    for (int b = 0; b < K; ++b) ag->accu[a * K + b] += pa * ugrad[b];
+            }
+            ag->counter[0] += 1;
+            if (ag->counter[0] >= ag->mb_size) {
+                const double inv_m = 1.0 / (double)ag->mb_size;
+                for (int a = 0; a < K; ++a)
+                    for (int b = 0; b < K; ++b) {
+                        float *wab = ag->W + a * K + b;
+                        *wab = (float)((double)*wab - ag->lr * ag->accu[a * K + b] * inv_m);
+                        ag->accu[a * K + b] = 0.0;
+                    }
+                ag->counter[0] = 0;
+            }
+            if (ag->hist_prop && hist_len > 0) {
+                const double scale = (1.0 - gamma) / (double)hist_len;
+                double *wh = s->wh;
+                for (int k = 0; k < K; ++k) {
+                    double acc = 0.0;
+                    for (int b = 0; b < K; ++b) acc += (double)ag->W[k * K + b] * ugrad[b];
+                    wh[k] = scale * acc;
+                }
+                for (int64_t idx = hb; idx < hb + hist_len; ++idx) {
+                    float *th = T + (int64_t)ag->tr_items[idx] * K;
+                    for (int k = 0; k < K; ++k)
+                        th[k] = (float)((double)th[k] - lr * (wh[k] + l2 * (double)th[k]));
+                }
+            }
+        }
     }
 }
 
@@ -261,14 +341,18 @@ int ho_train_range(float *S, float *T, int64_t num_items, int K, const int32_t *
                    const int32_t *ep_items, int64_t start, int64_t stop, uint64_t *rng_state,
                    int use_cosine, int n_neg, double lr, double l2, double mu, double theta,
                    double *loss_out, int64_t *degen_out, int64_t *active_out,
-                   int32_t *last_neg_ids) {
+                   int32_t *last_neg_ids, float *agg_W, const int64_t *tr_offsets,
+                   const int32_t *tr_items, double gamma, double agg_lr, int64_t mb_size,
+                   int64_t max_history, int hist_prop, double *agg_accu, int64_t *agg_counter) {
+    ho_agg ag = {agg_W != NULL, agg_W, tr_offsets, tr_items, gamma, agg_lr, mb_size, max_history,
+                 hist_prop, agg_accu, agg_counter};
     ho_scratch s;
     if (scratch_init(&s, K, n_neg)) {
         scratch_free(&s);
         return -1;
     }
     train_chunk(S, T, ep_users, ep_items, start, stop, num_items, rng_state, use_cosine, n_neg, lr,
-                l2, mu, theta, &s, loss_out, degen_out, active_out);
+                l2, mu, theta, &ag, &s, loss_out, degen_out, active_out);
     if (last_neg_ids) memcpy(last_neg_ids, s.neg_ids, sizeof(int32_t) * (size_t)n_neg);
     scratch_free(&s);
     return 0;
@@ -309,9 +393,10 @@ static void *worker_main(void *arg) {
         if (c >= sh->nchunks) break;
         int64_t start = c * sh->chunk;
         int64_t stop = start + sh->chunk < sh->npairs ? start + sh->chunk : sh->npairs;
+        const ho_agg off = {0, NULL, NULL, NULL, 0.0, 0.0, 1, 0, 0, NULL, NULL};
         train_chunk(sh->S, sh->T, sh->ep_users, sh->ep_items, start, stop, sh->num_items,
                     &w->rng_state, sh->use_cosine, sh->n_neg, sh->lr, sh->l2, sh->mu, sh->theta,
-                    &s, &w->loss, &w->degen, &w->active);
+                    &off, &s, &w->loss, &w->degen, &w->active);
     }
     scratch_free(&s);
     return NULL;

@@ -61,7 +61,8 @@ def lib():
         L.ho_sample_negatives.argtypes = [P, i64, i32, i64, P]
         L.ho_train_range.restype = i32
         L.ho_train_range.argtypes = [P, P, i64, i32, P, P, i64, i64, P, i32, i32,
-                                     f64, f64, f64, f64, P, P, P, P]
+                                     f64, f64, f64, f64, P, P, P, P,
+                                     P, P, P, f64, f64, i64, i64, i32, P, P]
         L.ho_train_epoch_threads.restype = i32
         L.ho_train_epoch_threads.argtypes = [P, P, i64, i32, P, P, i64, u64, i64, i32, i64,
                                              i32, i32, f64, f64, f64, f64, P, P, P]
@@ -99,9 +100,35 @@ class RangeResult:
     last_neg_ids: np.ndarray
 
 
+@dataclass
+class AggState:
+    """Aggregator inputs + the per-thread state of trainer.py:348-349
+    (accumulator, flush counter), carried across calls within an epoch."""
+    W: np.ndarray                 # K x K float32, updated in place
+    tr_offsets: np.ndarray
+    tr_items: np.ndarray
+    gamma: float = 0.5
+    lr: float = 0.05
+    mini_batch: int = 32
+    max_history: int = 100
+    history_grad: bool = False
+    accu: np.ndarray | None = None
+    counter: np.ndarray | None = None
+
+    def __post_init__(self):
+        K = self.W.shape[0]
+        self.tr_offsets = np.ascontiguousarray(self.tr_offsets, dtype=np.int64)
+        self.tr_items = np.ascontiguousarray(self.tr_items, dtype=np.int32)
+        if self.accu is None:
+            self.accu = np.zeros((K, K), dtype=np.float64)
+        if self.counter is None:
+            self.counter = np.zeros(1, dtype=np.int64)
+
+
 def train_range(S: np.ndarray, T: np.ndarray, ep_users, ep_items, start: int, stop: int,
                 state: int, *, n_neg: int, lr: float, l2: float = 0.0, mu: float = 1.0,
-                theta: float = 0.8, cosine: bool = True, loss0: float = 0.0) -> RangeResult:
+                theta: float = 0.8, cosine: bool = True, loss0: float = 0.0,
+                agg: AggState | None = None) -> RangeResult:
     """Sequential pairs [start, stop) in place on S, T (trainer.py:114-297).
 
     ``loss0`` seeds the running loss accumulator so a sequence of calls
@@ -116,10 +143,17 @@ def train_range(S: np.ndarray, T: np.ndarray, ep_users, ep_items, start: int, st
     degen = np.zeros(1, dtype=np.int64)
     active = np.zeros(1, dtype=np.int64)
     last = np.zeros(n_neg, dtype=np.int32)
+    if agg is not None:
+        assert agg.W.dtype == np.float32 and agg.W.flags.c_contiguous
+        ag = (_ptr(agg.W), _ptr(agg.tr_offsets), _ptr(agg.tr_items), agg.gamma, agg.lr,
+              agg.mini_batch, agg.max_history, int(bool(agg.history_grad)), _ptr(agg.accu),
+              _ptr(agg.counter))
+    else:
+        ag = (None, None, None, 0.0, 0.0, 1, 0, 0, None, None)
     rc = lib().ho_train_range(_ptr(S), _ptr(T), T.shape[0], S.shape[1], _ptr(ep_users),
                               _ptr(ep_items), start, stop, _ptr(st), int(bool(cosine)), n_neg,
                               lr, l2, mu, theta, _ptr(loss), _ptr(degen), _ptr(active),
-                              _ptr(last))
+                              _ptr(last), *ag)
     if rc != 0:
         raise MemoryError("oracle scratch allocation failed")
     return RangeResult(float(loss[0]), int(degen[0]), int(active[0]), int(st[0]), last)

@@ -287,7 +287,55 @@ def eval_golden(S_c1, T_c1):
     np.savez_compressed(os.path.join(HERE, "eval.npz"), **res)
 
 
+def agg_golden():
+    """SimpleX behaviour aggregation (trainer.py:148-173, 299-331) through the
+    reference train_epoch(num_threads=1): final S, T, W and per-epoch loss."""
+    from heatcf.aggregator import AggregatorConfig as RAgg, init_weights
+    rng = np.random.Generator(np.random.PCG64(77))
+    lists = {u: rng.integers(0, 240, size=int(rng.integers(0, 30))) for u in range(60)}
+    tr = heatcf.dataset.from_user_lists(lists, num_users=60, num_items=240)
+    cases = {}
+
+    def add(name, K, N, agg, epochs, **kw):
+        S0 = r_init(60, K, RInit(seed=1)).values
+        T0 = r_init(240, K, RInit(seed=2)).values
+        W0 = init_weights(K, 9)
+        cfg = rtrainer.TrainingConfig(emb_dim=K, num_negatives=N, aggregator=agg, **kw)
+        S, T, W = RMat(S0.copy()), RMat(T0.copy()), W0.copy()
+        ml = [rtrainer.train_epoch(S, T, tr, cfg, W, epoch=e).mean_loss for e in range(epochs)]
+        cases[name] = dict(S0=S0, T0=T0, W0=W0, S=S.values.copy(), T=T.values.copy(), W=W.copy(),
+                           mean_loss=np.array(ml), K=K, N=N, lr=cfg.learning_rate, l2=cfg.l2_reg,
+                           mu=cfg.loss.mu, theta=cfg.loss.theta,
+                           cosine=int(cfg.similarity == "cosine"), seed=cfg.seed, epochs=epochs,
+                           gamma=agg.gamma, agg_lr=agg.learning_rate or cfg.learning_rate,
+                           mb=agg.mini_batch_size, max_history=agg.max_history,
+                           hist_prop=int(agg.history_grad))
+
+    add("basic", 16, 8, RAgg(enabled=True, gamma=0.5, max_history=20, mini_batch_size=32), 2,
+        learning_rate=0.05, loss=RLoss(mu=1.0, theta=0.2), seed=7)
+    add("hist_grad_l2", 16, 8, RAgg(enabled=True, gamma=0.3, max_history=5, mini_batch_size=7,
+                                    history_grad=True, learning_rate=0.02), 2,
+        learning_rate=0.05, l2_reg=0.01, loss=RLoss(mu=2.0, theta=0.1), seed=3)
+    add("gamma0_dot", 8, 4, RAgg(enabled=True, gamma=0.0, max_history=100, mini_batch_size=1),
+        1, learning_rate=0.01, similarity="dot", loss=RLoss(mu=1.0, theta=0.5), seed=5)
+    add("gamma1", 16, 8, RAgg(enabled=True, gamma=1.0, max_history=10, mini_batch_size=3,
+                              history_grad=True), 1,
+        learning_rate=0.05, loss=RLoss(mu=1.0, theta=0.0), seed=11)
+    add("K64_N50", 64, 50, RAgg(enabled=True, gamma=0.5, max_history=100, mini_batch_size=32,
+                                history_grad=True), 1,
+        learning_rate=1e-3, loss=RLoss(mu=50.0, theta=0.3), seed=0)
+    flat = {"offsets": tr.offsets, "items": tr.items}
+    for name, d in cases.items():
+        for k, v in d.items():
+            flat[f"{name}/{k}"] = np.asarray(v)
+    np.savez_compressed(os.path.join(HERE, "agg_cases.npz"), names=np.array(list(cases)), **flat)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "agg":
+        agg_golden()
+        print("agg done")
+        sys.exit(0)
     rng_golden()
     print("rng done")
     S, T = c1_golden()
@@ -298,3 +346,5 @@ if __name__ == "__main__":
     print("c2 prefix done")
     eval_golden(S, T)
     print("eval done")
+    agg_golden()
+    print("agg done")

@@ -187,3 +187,30 @@ def test_threaded_oracle_hogwild_runs():
                                        chunk_pairs=512, n_neg=10, lr=1e-3, mu=10.0, theta=0.5)
     assert np.isfinite(loss) and np.isfinite(S).all() and np.isfinite(T).all()
     assert abs(loss / len(ep_u) - z["mean_loss"][0]) < 0.05 * abs(z["mean_loss"][0])
+
+
+def _agg_cases():
+    z = np.load(os.path.join(GOLDEN, "agg_cases.npz"))
+    for name in z["names"]:
+        g = {k.split("/", 1)[1]: z[k] for k in z.files if k.startswith(f"{name}/")}
+        yield str(name), g, z["offsets"], z["items"]
+
+
+def test_oracle_aggregator_bit_exact():
+    """trainer.py:148-173 / 299-331 (SimpleX aggregation, per-thread
+    accumulator flushed every mini_batch pairs, optional history gradient)."""
+    for name, g, offsets, items in _agg_cases():
+        S, T, W = g["S0"].copy(), g["T0"].copy(), g["W0"].copy()
+        for e in range(int(g["epochs"])):
+            u, i = O.epoch_pairs(offsets, items, 60, O.shuffle_seed(int(g["seed"]), e))
+            ag = O.AggState(W, offsets, items, gamma=float(g["gamma"]), lr=float(g["agg_lr"]),
+                            mini_batch=int(g["mb"]), max_history=int(g["max_history"]),
+                            history_grad=bool(g["hist_prop"]))  # fresh per epoch (trainer.py:398)
+            r = O.train_range(S, T, u, i, 0, len(u), O.derive_stream(int(g["seed"]), 0x45504F43, e, 0),
+                              n_neg=int(g["N"]), lr=float(g["lr"]), l2=float(g["l2"]),
+                              mu=float(g["mu"]), theta=float(g["theta"]), cosine=bool(g["cosine"]),
+                              agg=ag)
+            assert r.loss / len(u) == g["mean_loss"][e], name
+        assert S.tobytes() == g["S"].tobytes(), name
+        assert T.tobytes() == g["T"].tobytes(), name
+        assert W.tobytes() == g["W"].tobytes(), name
