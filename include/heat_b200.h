@@ -18,6 +18,7 @@
  *                             evaluator.py:140-172, _topk_from_scores 61-73
  *   heat_apply_row_deltas  <- (new) multi-GPU item-delta exchange, SURVEY.md §8(e)
  *   heat_epoch_pairs       <- dataset.epoch_pairs (host)    dataset.py:146-158
+ *   heat_aggregate_users   <- evaluator._aggregated_user_vectors evaluator.py:91-110
  */
 #ifndef HEAT_B200_H
 #define HEAT_B200_H
@@ -60,6 +61,24 @@ typedef struct heat_sgd_params {
                              partials + fp64 combine when 0)               */
 } heat_sgd_params;
 
+/* SimpleX behaviour aggregation (aggregator.py:30-113; trainer.py:148-173,
+ * 299-331): the query is h = gamma*S[u] + (1-gamma)*mean(history rows)*W.
+ * Device pointers; `accu`/`counter` are the per-epoch accumulator state
+ * (zero them at the start of every epoch, as trainer.py:348-349 does). */
+typedef struct heat_agg_params {
+    float *W;                  /* K x K float32, input-major W[k*K+j]; updated */
+    const int64_t *tr_offsets; /* train CSR: a user's history is its first   */
+    const int32_t *tr_items;   /* max_history items (trainer.py:151-155)      */
+    double gamma;              /* aggregator.gamma                            */
+    double lr;                 /* aggregator.learning_rate or the embedding lr */
+    int64_t mini_batch;        /* accumulator flush period (pairs)            */
+    int64_t max_history;
+    int32_t history_grad;      /* propagate into the history item rows        */
+    int32_t reserved;
+    double *accu;              /* K x K binary64 weight-gradient accumulator  */
+    int64_t *counter;          /* pairs since the last flush                  */
+} heat_agg_params;
+
 /* Device-resident accumulators (caller zeroes them; kernels add). */
 typedef struct heat_counters {
     double loss;        /* running sum of per-pair losses (trainer.py:222)  */
@@ -77,14 +96,16 @@ typedef struct heat_counters {
  * `pair_index` (optional, int64 per pair) is the pair's global epoch position,
  * the key of its negative draws (a user shard trains a subset of the epoch
  * and must draw the 1-GPU run's negatives); NULL means position p itself.
+ * `agg` (optional) turns on behaviour aggregation (HEAT_MODE_EXACT only in
+ * this version; other modes return HEAT_ERR_UNSUPPORTED).
  * Scratch (HEAT_MODE_EXACT): `scratch` may be NULL (internal allocation) or a
  * device buffer of at least heat_scratch_bytes(n_neg, dim) bytes. */
 int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      const int32_t *ep_users, const int32_t *ep_items, int64_t start,
                      int64_t stop, const heat_sgd_params *params, heat_counters *counters,
                      int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
-                     int64_t delta_capacity, const int64_t *pair_index, void *scratch,
-                     void *stream);
+                     int64_t delta_capacity, const int64_t *pair_index,
+                     const heat_agg_params *agg, void *scratch, void *stream);
 
 int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim);
 
@@ -107,6 +128,14 @@ int heat_eval_users(const void *S, int32_t s_f64, const float *T, int64_t t_rows
                     const int32_t *te_items, int32_t k, int32_t use_cosine,
                     const double *dcg_weights, const double *idcg, int32_t *topk,
                     double *recall, double *ndcg, void *stream);
+
+/* out[u] = gamma*S[u] + (1-gamma) * mean(first max_history train items of u).W
+ * for u < s_rows (binary64 rows, the aggregated evaluation query,
+ * evaluator.py:91-110); users without history get gamma*S[u]. */
+int heat_aggregate_users(const float *S, int64_t s_rows, const float *T, const float *W,
+                         int32_t dim, const int64_t *tr_offsets, const int32_t *tr_items,
+                         int64_t tr_num_users, double gamma, int64_t max_history, double *out,
+                         void *stream);
 
 /* T[ids[i]] += rows[i] for i < *count (device count), in index order per row
  * when `ordered` != 0 (deterministic replica update), atomically otherwise. */

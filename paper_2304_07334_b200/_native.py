@@ -22,8 +22,8 @@ MODE_HOGWILD = 1
 MODE_DELTA = 2
 
 EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
-           "heat_eval_users", "heat_apply_row_deltas", "heat_epoch_pairs", "heat_last_error",
-           "heat_version")
+           "heat_eval_users", "heat_apply_row_deltas", "heat_epoch_pairs",
+           "heat_aggregate_users", "heat_last_error", "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -39,6 +39,23 @@ class SgdParams(ctypes.Structure):
         ("stream_base", ctypes.c_uint64),
         ("window", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+    ]
+
+
+class AggParams(ctypes.Structure):
+    """heat_agg_params (include/heat_b200.h)."""
+    _fields_ = [
+        ("W", ctypes.c_void_p),
+        ("tr_offsets", ctypes.c_void_p),
+        ("tr_items", ctypes.c_void_p),
+        ("gamma", ctypes.c_double),
+        ("lr", ctypes.c_double),
+        ("mini_batch", ctypes.c_int64),
+        ("max_history", ctypes.c_int64),
+        ("history_grad", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("accu", ctypes.c_void_p),
+        ("counter", ctypes.c_void_p),
     ]
 
 
@@ -73,7 +90,7 @@ def lib():
     P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     L.heat_train_range.restype = ctypes.c_int
     L.heat_train_range.argtypes = [P, i64, P, i64, P, P, i64, i64, ctypes.POINTER(SgdParams), P,
-                                   P, P, P, i64, P, P, P]
+                                   P, P, P, i64, P, ctypes.POINTER(AggParams), P, P]
     L.heat_scratch_bytes.restype = i64
     L.heat_scratch_bytes.argtypes = [i32, i32]
     L.heat_sample_negatives.restype = ctypes.c_int
@@ -85,6 +102,8 @@ def lib():
     L.heat_apply_row_deltas.argtypes = [P, i64, i32, P, P, P, i64, i32, P]
     L.heat_epoch_pairs.restype = ctypes.c_int
     L.heat_epoch_pairs.argtypes = [P, i64, P, i64, u64, u64, u64, u64, i32, ctypes.c_uint32, P, P]
+    L.heat_aggregate_users.restype = ctypes.c_int
+    L.heat_aggregate_users.argtypes = [P, i64, P, P, i32, P, P, i64, ctypes.c_double, i64, P, P]
     L.heat_last_error.restype = ctypes.c_char_p
     L.heat_last_error.argtypes = []
     L.heat_version.restype = ctypes.c_int

@@ -144,8 +144,8 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      const int32_t *ep_users, const int32_t *ep_items, int64_t start,
                      int64_t stop, const heat_sgd_params *p, heat_counters *counters,
                      int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
-                     int64_t delta_capacity, const int64_t *pair_index, void *scratch,
-                     void *stream) {
+                     int64_t delta_capacity, const int64_t *pair_index,
+                     const heat_agg_params *agg, void *scratch, void *stream) {
     if (!p) return fail(HEAT_ERR_INVALID, "null params");
     if (!S || !T || !counters) return fail(HEAT_ERR_INVALID, "null table or counters pointer");
     if (p->dim < 1) return fail(HEAT_ERR_INVALID, "dim must be >= 1, got %d", p->dim);
@@ -160,6 +160,16 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
     if (start < 0 || stop < start) return fail(HEAT_ERR_INVALID, "bad pair range");
     if (stop > start && (!ep_users || !ep_items)) return fail(HEAT_ERR_INVALID, "null pairs");
     cudaStream_t st = (cudaStream_t)stream;
+    if (agg) {
+        if (p->mode != HEAT_MODE_EXACT)
+            return fail(HEAT_ERR_UNSUPPORTED, "aggregation is implemented in EXACT mode only");
+        if (!agg->W || !agg->tr_offsets || !agg->accu || !agg->counter)
+            return fail(HEAT_ERR_INVALID, "aggregation needs W, train CSR, accu and counter");
+        if (!(agg->gamma >= 0.0 && agg->gamma <= 1.0))
+            return fail(HEAT_ERR_INVALID, "gamma must be in [0, 1], got %g", agg->gamma);
+        if (agg->mini_batch < 1 || agg->max_history < 0)
+            return fail(HEAT_ERR_INVALID, "mini_batch_size >= 1 and max_history >= 0 required");
+    }
     if (stop == start) return HEAT_OK;
     cudaError_t e;
     switch (p->mode) {
@@ -171,7 +181,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         if (!snap) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
         e = launch_exact(S, T, ep_users, ep_items, start, stop, p->dim, p->n_neg, p->use_cosine,
                          p->lr, p->l2, p->mu, p->theta, p->stream_base, t_rows, counters,
-                         (float *)snap, pair_index, st);
+                         (float *)snap, pair_index, agg, st);
         break;
     }
     case HEAT_MODE_HOGWILD:
@@ -221,6 +231,19 @@ int heat_eval_users(const void *S, int32_t s_f64, const float *T, int64_t t_rows
     if (e == cudaErrorInvalidValue)
         return fail(HEAT_ERR_UNSUPPORTED, "eval: k=%d with dim=%d exceeds shared memory", k, dim);
     return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "eval launch");
+}
+
+int heat_aggregate_users(const float *S, int64_t s_rows, const float *T, const float *W,
+                         int32_t dim, const int64_t *tr_offsets, const int32_t *tr_items,
+                         int64_t tr_num_users, double gamma, int64_t max_history, double *out,
+                         void *stream) {
+    if (dim < 1) return fail(HEAT_ERR_INVALID, "dim must be >= 1");
+    if (!(gamma >= 0.0 && gamma <= 1.0)) return fail(HEAT_ERR_INVALID, "gamma must be in [0, 1]");
+    if (s_rows > 0 && (!S || !T || !W || !out)) return fail(HEAT_ERR_INVALID, "null pointer");
+    if (tr_num_users > 0 && (!tr_offsets || !tr_items)) return fail(HEAT_ERR_INVALID, "null CSR");
+    cudaError_t e = launch_aggregate_users(S, T, W, tr_offsets, tr_items, s_rows, tr_num_users,
+                                           dim, gamma, max_history, out, (cudaStream_t)stream);
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "aggregate_users launch");
 }
 
 int heat_apply_row_deltas(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,

@@ -272,6 +272,47 @@ cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows
     return cudaErrorInvalidValue;
 }
 
+// Aggregated query vectors for evaluation (evaluator.py:91-110):
+// out[u] = gamma*S[u] + (1-gamma) * mean(first max_history train rows) . W,
+// binary64, one CTA per user.
+__global__ void aggregate_users_kernel(const float *__restrict__ S, const float *__restrict__ T,
+                                       const float *__restrict__ W,
+                                       const int64_t *__restrict__ tr_off,
+                                       const int32_t *__restrict__ tr_items, int64_t tr_num_users,
+                                       int K, double gamma, int64_t max_history,
+                                       double *__restrict__ out) {
+    extern __shared__ double pooled[];
+    const int64_t u = blockIdx.x;
+    int64_t hb = 0, n = 0;
+    if (u < tr_num_users) {
+        hb = tr_off[u];
+        n = tr_off[u + 1] - hb;
+        if (n > max_history) n = max_history;
+    }
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        double a = 0.0;
+        for (int64_t i = 0; i < n; ++i) a += (double)T[(int64_t)tr_items[hb + i] * K + k];
+        pooled[k] = n > 0 ? a / (double)n : 0.0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < K; j += blockDim.x) {
+        double a = 0.0;
+        for (int k = 0; k < K; ++k) a = fma(pooled[k], (double)W[k * K + j], a);
+        out[u * K + j] = gamma * (double)S[u * K + j] + (1.0 - gamma) * a;
+    }
+}
+
+cudaError_t launch_aggregate_users(const float *S, const float *T, const float *W,
+                                   const int64_t *tr_off, const int32_t *tr_items,
+                                   int64_t n_users, int64_t tr_num_users, int K, double gamma,
+                                   int64_t max_history, double *out, cudaStream_t st) {
+    if (n_users == 0) return cudaSuccess;
+    int threads = K < 128 ? 64 : 128;
+    aggregate_users_kernel<<<(unsigned)n_users, threads, K * sizeof(double), st>>>(
+        S, T, W, tr_off, tr_items, tr_num_users, K, gamma, max_history, out);
+    return cudaGetLastError();
+}
+
 size_t eval_max_k_supported(int K) {
     size_t k = 1;
     while (eval_smem_bytes<8>(K, (int)(k * 2)) <= 200 * 1024 && k < (1u << 20)) k *= 2;

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                  const int32_t *__restrict__ items, int64_t start, int64_t stop, int K, int N,
                  int cosine, double lr, double l2, double mu, double theta, uint64_t s0,
                  FastMod fm, heat_counters *ctr, float *__restrict__ snap,
-                 const int64_t *__restrict__ pair_index) {
+                 const int64_t *__restrict__ pair_index, heat_agg_params ag, int agg_on) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ExactSmem &sh = *reinterpret_cast<ExactSmem *>(smem_raw);
     double *ubuf = reinterpret_cast<double *>(smem_raw + sizeof(ExactSmem) + 16 -
@@ -82,6 +82,11 @@ __global__ void __launch_bounds__(kExactThreads, 1)
     float *pos_buf = reinterpret_cast<float *>(sims + N);
     int32_t *nids = reinterpret_cast<int32_t *>(pos_buf + K);
     int32_t *list = nids + N;
+    // aggregation buffers (binary64): pooled history, h-gradient, W*grad
+    double *pooled = reinterpret_cast<double *>(
+        (reinterpret_cast<uintptr_t>(list + N) + 15) & ~uintptr_t(15));
+    double *ugs = pooled + K;
+    double *whs = ugs + K;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -91,17 +96,41 @@ __global__ void __launch_bounds__(kExactThreads, 1)
     double loss_acc = 0.0;
     if (tid == 0) loss_acc = ctr->loss;
     long long degen = 0, active = 0;
+    int64_t agg_ctr = agg_on ? *ag.counter : 0;  // uniform across the CTA
+    const double gamma = ag.gamma;
 
     for (int64_t p = start; p < stop; ++p) {
         const int64_t u = users[p];
         const int64_t pos = items[p];
         // ---- read (trainer.py:121-142): S[u] -> f64, T[pos] snapshot, ids
         for (int k = tid; k < K; k += kExactThreads) {
-            ubuf[k] = (double)S[u * K + k];
+            if (!agg_on) ubuf[k] = (double)S[u * K + k];
             pos_buf[k] = T[pos * K + k];
         }
         const int64_t pg = pair_index ? pair_index[p] : p;  // RNG key
         for (int j = tid; j < N; j += kExactThreads) nids[j] = neg_id(s0, pg, N, j, fm);
+        // ---- aggregate forward (trainer.py:150-169): pooled = mean of the
+        // first max_history history rows, h = gamma*S[u] + (1-gamma)*pooled.W
+        int64_t hb = 0, hist_len = 0;
+        if (agg_on) {
+            hb = ag.tr_offsets[u];
+            int64_t he = ag.tr_offsets[u + 1];
+            if (he - hb > ag.max_history) he = hb + ag.max_history;
+            hist_len = he - hb;
+            for (int k = tid; k < K; k += kExactThreads) {
+                double acc = 0.0;
+                for (int64_t idx = hb; idx < he; ++idx)
+                    acc = DADD(acc, (double)T[(int64_t)ag.tr_items[idx] * K + k]);
+                if (hist_len > 0) acc = DDIV(acc, (double)hist_len);
+                pooled[k] = acc;
+            }
+            __syncthreads();
+            for (int j = tid; j < K; j += kExactThreads) {
+                double acc = 0.0;
+                for (int k = 0; k < K; ++k) acc = DADD(acc, DMUL(pooled[k], (double)ag.W[k * K + j]));
+                ubuf[j] = DADD(DMUL(gamma, (double)S[u * K + j]), DMUL(DSUB(1.0, gamma), acc));
+            }
+        }
         __syncthreads();
 
         // ---- similarity (trainer.py:176-207)
@@ -267,13 +296,52 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                     }
                 }
             }
-            // S[u] (trainer.py:291-293)
+            // S[u] (trainer.py:291-293; with aggregation gamma*ugrad, 303)
             float *su = S + u * K + k;
             double s = (double)*su;
-            *su = __double2float_rn(DSUB(s, DMUL(lr, DADD(ug, DMUL(l2, s)))));
+            if (!agg_on) {
+                *su = __double2float_rn(DSUB(s, DMUL(lr, DADD(ug, DMUL(l2, s)))));
+            } else {
+                *su = __double2float_rn(DSUB(s, DMUL(lr, DADD(DMUL(gamma, ug), DMUL(l2, s)))));
+                ugs[k] = ug;
+            }
+        }
+        if (agg_on) {
+            // ---- aggregate backward (trainer.py:304-328)
+            __syncthreads();
+            const double omg = DSUB(1.0, gamma);
+            for (int e = tid; e < K * K; e += kExactThreads) {
+                const double pa = DMUL(omg, pooled[e / K]);
+                if (pa != 0.0) ag.accu[e] = DADD(ag.accu[e], DMUL(pa, ugs[e % K]));
+            }
+            agg_ctr += 1;
+            if (agg_ctr >= ag.mini_batch) {
+                const double inv_m = DDIV(1.0, (double)ag.mini_batch);
+                for (int e = tid; e < K * K; e += kExactThreads) {
+                    ag.W[e] = __double2float_rn(
+                        DSUB((double)ag.W[e], DMUL(DMUL(ag.lr, ag.accu[e]), inv_m)));
+                    ag.accu[e] = 0.0;
+                }
+                agg_ctr = 0;
+            }
+            if (ag.history_grad && hist_len > 0) {
+                __syncthreads();  // W after the flush
+                const double scale = DDIV(omg, (double)hist_len);
+                for (int k = tid; k < K; k += kExactThreads) {
+                    double acc = 0.0;
+                    for (int b = 0; b < K; ++b) acc = DADD(acc, DMUL((double)ag.W[k * K + b], ugs[b]));
+                    const double wh = DMUL(scale, acc);
+                    for (int64_t idx = hb; idx < hb + hist_len; ++idx) {
+                        float *th = T + (int64_t)ag.tr_items[idx] * K + k;
+                        const double t = (double)*th;
+                        *th = __double2float_rn(DSUB(t, DMUL(lr, DADD(wh, DMUL(l2, t)))));
+                    }
+                }
+            }
         }
         __syncthreads();
     }
+    if (agg_on && tid == 0) *ag.counter = agg_ctr;
     // telemetry (order-free integer sums)
     for (int o = 16; o > 0; o >>= 1) degen += __shfl_xor_sync(0xffffffffu, degen, o);
     if (lane == 0 && degen) atomicAdd((unsigned long long *)&ctr->degenerate, (unsigned long long)degen);
@@ -286,14 +354,15 @@ __global__ void __launch_bounds__(kExactThreads, 1)
 
 size_t exact_smem_bytes(int K, int N) {
     size_t head = sizeof(ExactSmem) + 16 - (sizeof(ExactSmem) % 16);
-    return head + (size_t)K * 8 + (size_t)N * 8 * 3 + (size_t)K * 4 + (size_t)N * 4 * 2 + 16;
+    return head + (size_t)K * 8 + (size_t)N * 8 * 3 + (size_t)K * 4 + (size_t)N * 4 * 2 + 16 +
+           (size_t)K * 8 * 3 + 16;
 }
 
 cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t *items,
                          int64_t start, int64_t stop, int K, int N, int cosine, double lr,
                          double l2, double mu, double theta, uint64_t s0, int64_t num_items,
                          heat_counters *ctr, float *snap, const int64_t *pair_index,
-                         cudaStream_t stream) {
+                         const heat_agg_params *agg, cudaStream_t stream) {
     size_t smem = exact_smem_bytes(K, N);
     cudaError_t e = cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -301,7 +370,8 @@ cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t
     exact_kernel<<<1, kExactThreads, smem, stream>>>(S, T, users, items, start, stop, K, N,
                                                      cosine, lr, l2, mu, theta, s0,
                                                      FastMod::make((uint64_t)num_items), ctr, snap,
-                                                     pair_index);
+                                                     pair_index, agg ? *agg : heat_agg_params{},
+                                                     agg != nullptr);
     return cudaGetLastError();
 }
 

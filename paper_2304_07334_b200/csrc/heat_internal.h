@@ -15,7 +15,7 @@ cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t
                          int64_t start, int64_t stop, int K, int N, int cosine, double lr,
                          double l2, double mu, double theta, uint64_t s0, int64_t num_items,
                          heat_counters *ctr, float *snap, const int64_t *pair_index,
-                         cudaStream_t stream);
+                         const heat_agg_params *agg, cudaStream_t stream);
 
 struct HogwildArgs {
     float *S;
@@ -58,6 +58,11 @@ cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows
 cudaError_t launch_apply_deltas(float *T, int64_t t_rows, int K, const int32_t *ids,
                                 const float *rows, const int64_t *count, int64_t capacity,
                                 int ordered, cudaStream_t stream);
+
+cudaError_t launch_aggregate_users(const float *S, const float *T, const float *W,
+                                   const int64_t *tr_off, const int32_t *tr_items,
+                                   int64_t n_users, int64_t tr_num_users, int K, double gamma,
+                                   int64_t max_history, double *out, cudaStream_t st);
 
 int sm_count();
 size_t eval_max_k_supported(int K);

@@ -112,7 +112,7 @@ class DeviceModel:
 
     def train_range(self, users: torch.Tensor, items: torch.Tensor, start: int, stop: int,
                     params: N.SgdParams, delta=None, pair_index: torch.Tensor | None = None,
-                    stream=None) -> None:
+                    stream=None, agg: "DeviceAggregator | None" = None) -> None:
         """Launch pairs [start, stop) on the current stream (asynchronous)."""
         scratch = self.scratch(params.n_neg) if params.mode == N.MODE_EXACT else None
         d_ids = d_rows = d_cnt = None
@@ -122,9 +122,45 @@ class DeviceModel:
         rc = N.lib().heat_train_range(
             _p(self.S), self.S.shape[0], _p(self.T), self.T.shape[0], _p(users), _p(items),
             start, stop, ctypes.byref(params), self.counters.ptr(), _p(d_ids), _p(d_rows),
-            _p(d_cnt), cap, _p(pair_index), _p(scratch),
+            _p(d_cnt), cap, _p(pair_index), ctypes.byref(agg.params()) if agg else None,
+            _p(scratch),
             _stream(self.device) if stream is None else ctypes.c_void_p(stream.cuda_stream))
         N.check(rc)
+
+
+class DeviceAggregator:
+    """Device state of the SimpleX behaviour aggregation (aggregator.py):
+    the shared K x K weights W, the train CSR that holds the histories, and
+    the per-epoch weight-gradient accumulator + flush counter
+    (_ThreadState.agg_accu / agg_ctr, trainer.py:348-349)."""
+
+    def __init__(self, W: np.ndarray, train, cfg_agg, lr: float, device):
+        K = W.shape[0]
+        self.device = device
+        self.W = torch.from_numpy(np.ascontiguousarray(W, dtype=np.float32)).to(device)
+        self.tr_offsets = torch.from_numpy(np.ascontiguousarray(train.offsets, np.int64)).to(device)
+        items = np.ascontiguousarray(train.items, np.int32)
+        self.tr_items = torch.from_numpy(items if len(items) else np.zeros(1, np.int32)).to(device)
+        self.accu = torch.zeros((K, K), dtype=torch.float64, device=device)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=device)
+        self.gamma = float(cfg_agg.gamma)
+        self.lr = float(cfg_agg.learning_rate if cfg_agg.learning_rate is not None else lr)
+        self.mini_batch = int(cfg_agg.mini_batch_size)
+        self.max_history = int(cfg_agg.max_history)
+        self.history_grad = bool(cfg_agg.history_grad)
+        self._p = None
+
+    def reset_epoch(self) -> None:
+        self.accu.zero_()
+        self.counter.zero_()
+
+    def params(self) -> N.AggParams:
+        self._p = N.AggParams(W=self.W.data_ptr(), tr_offsets=self.tr_offsets.data_ptr(),
+                              tr_items=self.tr_items.data_ptr(), gamma=self.gamma, lr=self.lr,
+                              mini_batch=self.mini_batch, max_history=self.max_history,
+                              history_grad=int(self.history_grad), reserved=0,
+                              accu=self.accu.data_ptr(), counter=self.counter.data_ptr())
+        return self._p
 
 
 def stream_base(seed: int, epoch: int) -> int:

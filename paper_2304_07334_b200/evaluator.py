@@ -59,10 +59,8 @@ def _validate(S, T, train, test, cfg, weights):
     if test.num_pairs == 0:
         raise EmptyTestSetError("no user has a test item")
     agg = getattr(cfg, "aggregator", None)
-    if agg is not None and agg.enabled:
-        if weights is None:
-            raise ValueError("aggregator enabled but no weight matrix given")
-        raise ValueError("the B200 path does not implement the aggregated query vector")
+    if agg is not None and agg.enabled and weights is None:
+        raise ValueError("aggregator enabled but no weight matrix given")
 
 
 def eval_users_device(Sdev: torch.Tensor, Tdev: torch.Tensor, users: np.ndarray, train,
@@ -96,6 +94,24 @@ def eval_users_device(Sdev: torch.Tensor, Tdev: torch.Tensor, users: np.ndarray,
     return out
 
 
+def aggregated_queries(model: DeviceModel, train, weights, gamma: float,
+                       max_history: int) -> torch.Tensor:
+    """binary64 aggregated user vectors on the device (evaluator.py:91-110)."""
+    dev = model.device
+    W = weights if torch.is_tensor(weights) else torch.from_numpy(
+        np.ascontiguousarray(weights, dtype=np.float32))
+    W = W.to(dev, dtype=torch.float32).contiguous()
+    tr_off = torch.from_numpy(np.ascontiguousarray(train.offsets, np.int64)).to(dev)
+    items = np.ascontiguousarray(train.items, np.int32)
+    tr_it = torch.from_numpy(items if len(items) else np.zeros(1, np.int32)).to(dev)
+    out = torch.empty(model.S.shape, dtype=torch.float64, device=dev)
+    rc = N.lib().heat_aggregate_users(_p(model.S), model.S.shape[0], _p(model.T), _p(W),
+                                      model.dim, _p(tr_off), _p(tr_it), train.num_users,
+                                      float(gamma), int(max_history), _p(out), _stream(dev))
+    N.check(rc)
+    return out
+
+
 def _mean_in_order(values: np.ndarray) -> float:
     acc = 0.0
     for v in values.tolist():
@@ -111,7 +127,11 @@ def evaluate_device(model: DeviceModel, S, T, train, test, cfg, weights=None, k:
     similarity = getattr(cfg, "similarity", "cosine")
     counts = np.diff(test.offsets)
     users = np.flatnonzero(counts > 0).astype(np.int32)
-    rec, nd = eval_users_device(model.S, model.T, users, train, test, k,
+    query = model.S
+    agg = getattr(cfg, "aggregator", None)
+    if agg is not None and agg.enabled:
+        query = aggregated_queries(model, train, weights, agg.gamma, agg.max_history)
+    rec, nd = eval_users_device(query, model.T, users, train, test, k,
                                 similarity == "cosine")
     n = len(users)
     return MetricsReport(recall_at_k=_mean_in_order(rec) / n, ndcg_at_k=_mean_in_order(nd) / n,

@@ -108,12 +108,25 @@ def _check_supported(cfg) -> None:
     if cfg.sampler.kind != "uniform":
         raise ValueError("the B200 path implements the uniform sampler only "
                          f"(got {cfg.sampler.kind!r}); no CPU fallback")
-    if cfg.aggregator.enabled:
-        raise ValueError("the B200 path does not implement the behaviour aggregator; "
-                         "no CPU fallback")
+    resolve_mode(cfg)  # raises for combinations the device path does not implement
+
+
+def _make_aggregator(model: DeviceModel, weights, train, cfg):
+    from .device import DeviceAggregator
+    if not cfg.aggregator.enabled:
+        return None
+    return DeviceAggregator(np.asarray(weights), train, cfg.aggregator, cfg.learning_rate,
+                            model.device)
 
 
 def resolve_mode(cfg) -> int:
+    if cfg.aggregator.enabled:
+        # shared-W aggregation is implemented in the deterministic kernel
+        # (bit-exact with the reference); an explicit Hogwild request is refused
+        if _OPTIONS.mode == "hogwild":
+            raise ValueError("behaviour aggregation is implemented in EXACT mode only; "
+                             "no CPU fallback")
+        return N.MODE_EXACT
     mode = _OPTIONS.mode or ("exact" if cfg.num_threads == 1 else "hogwild")
     return N.MODE_EXACT if mode == "exact" else N.MODE_HOGWILD
 
@@ -126,7 +139,7 @@ def sgd_params(model: DeviceModel, cfg, epoch: int, mode: int) -> N.SgdParams:
 
 
 def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int | None = None,
-                        pairs=None) -> tuple[EpochReport, dict]:
+                        pairs=None, agg=None) -> tuple[EpochReport, dict]:
     """One epoch on device-resident tables; no table transfer."""
     if mode is None:
         mode = resolve_mode(cfg)
@@ -137,11 +150,13 @@ def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int
     du, di = pairs
     npairs = int(du.shape[0])
     model.counters.reset()
+    if agg is not None:
+        agg.reset_epoch()  # per-epoch accumulator state (trainer.py:398-400)
     params = sgd_params(model, cfg, epoch, mode)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
-    model.train_range(du, di, 0, npairs, params)
+    model.train_range(du, di, 0, npairs, params, agg=agg)
     ev1.record()
     c = model.counters.read()  # synchronises
     wall = time.perf_counter() - t0
@@ -186,12 +201,15 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     di = bufs[1].to(dev, non_blocking=True)
     if collect_phases:
         stream.synchronize()
+    agg = _make_aggregator(model, weights, train, cfg)
     t_run = time.perf_counter()
-    rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=(du, di))
+    rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=(du, di), agg=agg)
     PREFETCH.release(bufs)
     t_down = time.perf_counter()
     torch.from_numpy(S.values).copy_(model.S, non_blocking=True)
     torch.from_numpy(T.values).copy_(model.T, non_blocking=True)
+    if agg is not None:  # the reference updates the shared weights in place
+        np.copyto(weights, agg.W.cpu().numpy())
     stream.synchronize()
     t_end = time.perf_counter()
     rep.wall_time = t_end - t_start
@@ -231,9 +249,11 @@ def train(S, T, train_set, test_set, cfg, weights=None, *, eval_interval: int = 
     evaluations: list = []
     best = {"recall": -1.0, "epoch": -1}
     model = DeviceModel(S.values, T.values, _OPTIONS.device)
+    agg = _make_aggregator(model, weights, train_set, cfg)
 
     def run_eval(epoch: int):
-        metrics = evaluate_device(model, S, T, train_set, test_set, cfg, k=k)
+        metrics = evaluate_device(model, S, T, train_set, test_set, cfg,
+                                  weights=agg.W if agg is not None else None, k=k)
         evaluations.append((epoch, metrics))
         if on_eval is not None:
             on_eval(epoch, metrics)
@@ -242,12 +262,14 @@ def train(S, T, train_set, test_set, cfg, weights=None, *, eval_interval: int = 
             best["epoch"] = epoch
             if out_dir is not None:
                 model.download(S.values, T.values)
-                save_model(f"{out_dir}/best.ckpt", S, T, None)
+                if agg is not None:
+                    np.copyto(weights, agg.W.cpu().numpy())
+                save_model(f"{out_dir}/best.ckpt", S, T, weights if agg is not None else None)
         return metrics
 
     for epoch in range(cfg.epochs):
         t0 = time.perf_counter()
-        rep, _ = run_epoch_on_device(model, train_set, cfg, epoch)
+        rep, _ = run_epoch_on_device(model, train_set, cfg, epoch, agg=agg)
         rep.wall_time = time.perf_counter() - t0
         reports.append(rep)
         if on_epoch is not None:
@@ -256,7 +278,9 @@ def train(S, T, train_set, test_set, cfg, weights=None, *, eval_interval: int = 
             run_eval(epoch + 1)
     final = run_eval(cfg.epochs)
     model.download(S.values, T.values)
+    if agg is not None:
+        np.copyto(weights, agg.W.cpu().numpy())
     if out_dir is not None:
-        save_model(f"{out_dir}/final.ckpt", S, T, None)
+        save_model(f"{out_dir}/final.ckpt", S, T, weights if agg is not None else None)
     return TrainResult(reports=reports, evaluations=evaluations, final_metrics=final,
                        best_recall=best["recall"], best_epoch=best["epoch"])

@@ -473,3 +473,105 @@ def test_logical_shards_keep_item_replicas_identical(torch_cuda, G):
         m.train_range(du, di, 0, len(u), p)
         ref.append(m.counters.read().loss / len(u))
     assert abs(losses[1] - ref[1]) <= 0.02 * abs(ref[1]), (losses, ref)
+
+
+def _agg_golden():
+    z = np.load(os.path.join(GOLDEN, "agg_cases.npz"))
+    for name in z["names"]:
+        g = {k.split("/", 1)[1]: z[k] for k in z.files if k.startswith(f"{name}/")}
+        yield str(name), g, z["offsets"], z["items"]
+
+
+def test_exact_aggregator_bit_exact(torch_cuda):
+    """SimpleX aggregation in EXACT mode == reference train_epoch(num_threads=1)
+    with the aggregator on: S, T, W and mean loss bit for bit
+    (trainer.py:148-173, 299-331)."""
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.config import AggregatorConfig
+    from paper_2304_07334_b200.dataset import InteractionSet, epoch_pairs
+    from paper_2304_07334_b200.device import DeviceAggregator, DeviceModel
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    for name, g, offsets, items in _agg_golden():
+        train = InteractionSet(60, 240, offsets, items)
+        S, T = g["S0"].copy(), g["T0"].copy()
+        model = DeviceModel(S, T)
+        cfg_agg = AggregatorConfig(enabled=True, gamma=float(g["gamma"]),
+                                   max_history=int(g["max_history"]),
+                                   mini_batch_size=int(g["mb"]),
+                                   history_grad=bool(g["hist_prop"]),
+                                   learning_rate=float(g["agg_lr"]))
+        agg = DeviceAggregator(g["W0"].copy(), train, cfg_agg, float(g["lr"]), model.device)
+        for e in range(int(g["epochs"])):
+            u, i = epoch_pairs(train, shuffle_seed(int(g["seed"]), e))
+            du, di = model.upload_pairs(u, i)
+            p = model.params(n_neg=int(g["N"]), lr=float(g["lr"]), l2=float(g["l2"]),
+                             mu=float(g["mu"]), theta=float(g["theta"]), cosine=bool(g["cosine"]),
+                             mode=N.MODE_EXACT, stream_base=epoch_stream(int(g["seed"]), e))
+            model.counters.reset()
+            agg.reset_epoch()
+            for s in range(0, len(u), 37):  # arbitrary step split: state carried
+                model.train_range(du, di, s, min(len(u), s + 37), p, agg=agg)
+            c = model.counters.read()
+            assert c.loss / len(u) == g["mean_loss"][e], name
+        model.download(S, T)
+        assert S.tobytes() == g["S"].tobytes(), name
+        assert T.tobytes() == g["T"].tobytes(), name
+        assert agg.W.cpu().numpy().tobytes() == g["W"].tobytes(), name
+
+
+def test_train_epoch_api_with_aggregator(torch_cuda):
+    from paper_2304_07334_b200 import LossParams, TrainingConfig
+    from paper_2304_07334_b200.config import AggregatorConfig
+    from paper_2304_07334_b200.dataset import InteractionSet
+    from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+    from paper_2304_07334_b200.trainer import train_epoch
+    name, g, offsets, items = next(_agg_golden())  # "basic"
+    train = InteractionSet(60, 240, offsets, items)
+    cfg = TrainingConfig(emb_dim=int(g["K"]), num_negatives=int(g["N"]), learning_rate=float(g["lr"]),
+                         num_threads=1, loss=LossParams(mu=float(g["mu"]), theta=float(g["theta"])),
+                         seed=int(g["seed"]),
+                         aggregator=AggregatorConfig(enabled=True, gamma=float(g["gamma"]),
+                                                     max_history=int(g["max_history"]),
+                                                     mini_batch_size=int(g["mb"])))
+    S, T, W = EmbeddingMatrix(g["S0"].copy()), EmbeddingMatrix(g["T0"].copy()), g["W0"].copy()
+    for e in range(int(g["epochs"])):
+        rep = train_epoch(S, T, train, cfg, W, epoch=e)
+        assert rep.mean_loss == g["mean_loss"][e]
+    assert S.values.tobytes() == g["S"].tobytes()
+    assert T.values.tobytes() == g["T"].tobytes()
+    assert W.tobytes() == g["W"].tobytes()  # updated in place, like the reference
+
+
+def test_aggregated_evaluation_query(torch_cuda):
+    """evaluator.py:91-110 + 113-179 with cfg.aggregator enabled."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import TrainingConfig
+    from paper_2304_07334_b200.config import AggregatorConfig
+    from paper_2304_07334_b200.dataset import from_user_lists
+    from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+    from paper_2304_07334_b200.evaluator import evaluate
+    rng = np.random.default_rng(8)
+    nu, ni, K = 40, 300, 16
+    S = EmbeddingMatrix(rng.standard_normal((nu, K)).astype(np.float32))
+    T = EmbeddingMatrix(rng.standard_normal((ni, K)).astype(np.float32))
+    W = rng.standard_normal((K, K)).astype(np.float32)
+    tr = from_user_lists({u: rng.integers(0, ni, int(rng.integers(0, 25))) for u in range(nu)},
+                         num_users=nu, num_items=ni)
+    te = from_user_lists({u: rng.integers(0, ni, 3) for u in range(nu)}, num_users=nu,
+                         num_items=ni)
+    for gamma, mh in ((0.0, 100), (0.4, 5), (1.0, 10)):
+        cfg = TrainingConfig(emb_dim=K, num_negatives=1,
+                             aggregator=AggregatorConfig(enabled=True, gamma=gamma,
+                                                         max_history=mh))
+        m = evaluate(S, T, tr, te, cfg, weights=W, k=10)
+        pooled = np.zeros((nu, K))
+        for u in range(nu):
+            h = tr.slice(u)[:mh]
+            if len(h):
+                pooled[u] = T.values[h].astype(np.float64).mean(axis=0)
+        q = gamma * S.values.astype(np.float64) + (1 - gamma) * (pooled @ W.astype(np.float64))
+        rec, nd, n = O.evaluate_ref(q, T.values, tr.offsets, tr.items, nu, te.offsets, te.items,
+                                    nu, k=10)
+        assert m.users_evaluated == n
+        assert m.recall_at_k == pytest.approx(rec, abs=1e-12)
+        assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12)

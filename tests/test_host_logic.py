@@ -41,15 +41,15 @@ def test_abi_rejects_bad_arguments_without_a_gpu():
     p = N.SgdParams(dim=0, n_neg=1, use_cosine=1, mode=0, lr=0.1, l2=0.0, mu=1.0, theta=0.5,
                     stream_base=0, window=0, flags=0)
     rc = L.heat_train_range(None, 1, None, 1, None, None, 0, 1, ctypes.byref(p), None,
-                            None, None, None, 0, None, None, None)
+                            None, None, None, 0, None, None, None, None)
     assert rc == N.HEAT_ERR_INVALID
     fake = ctypes.c_void_p(16)
     rc = L.heat_train_range(fake, 1, fake, 1, fake, fake, 0, 1, ctypes.byref(p), fake,
-                            None, None, None, 0, None, None, None)
+                            None, None, None, 0, None, None, None, None)
     assert rc == N.HEAT_ERR_INVALID and b"dim" in L.heat_last_error()
     p.dim, p.theta = 4, 1.5
     rc = L.heat_train_range(fake, 1, fake, 1, fake, fake, 0, 1, ctypes.byref(p), fake,
-                            None, None, None, 0, None, None, None)
+                            None, None, None, 0, None, None, None, None)
     assert rc == N.HEAT_ERR_INVALID and b"theta" in L.heat_last_error()
     with pytest.raises(ValueError):
         N.check(N.HEAT_ERR_INVALID)
