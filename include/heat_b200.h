@@ -99,7 +99,9 @@ typedef struct heat_counters {
  * `agg` (optional) turns on behaviour aggregation (HEAT_MODE_EXACT only in
  * this version; other modes return HEAT_ERR_UNSUPPORTED).
  * Scratch (HEAT_MODE_EXACT): `scratch` may be NULL (internal allocation) or a
- * device buffer of at least heat_scratch_bytes(n_neg, dim) bytes. */
+ * device buffer of at least heat_scratch_bytes(n_neg, dim, s_rows, t_rows)
+ * bytes (active-row snapshots and the per-row commit stamps of the parallel
+ * deterministic kernel). */
 int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      const int32_t *ep_users, const int32_t *ep_items, int64_t start,
                      int64_t stop, const heat_sgd_params *params, heat_counters *counters,
@@ -107,7 +109,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      int64_t delta_capacity, const int64_t *pair_index,
                      const heat_agg_params *agg, void *scratch, void *stream);
 
-int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim);
+int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim, int64_t s_rows, int64_t t_rows);
 
 /* out[(p - first_pair) * n_neg + j] = negative j of pair p, for
  * p in [first_pair, first_pair + npairs): the id trainer.py:136 draws. */
@@ -152,6 +154,11 @@ int heat_epoch_pairs(const int64_t *offsets, int64_t num_users, const int32_t *i
                      uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                      int32_t has_uint32, uint32_t uinteger, int32_t *out_users,
                      int32_t *out_items);
+
+/* Diagnostics of the parallel deterministic (EXACT) kernel: out[0..2] clock64
+ * totals of speculate / commit-token wait / commit, out[3..5] partial
+ * recomputes, full recomputes, pairs.  reset != 0 zeroes them. */
+int heat_exact_stats(unsigned long long *out, int reset);
 
 const char *heat_last_error(void);
 int heat_version(void);

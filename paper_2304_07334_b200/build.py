@@ -22,8 +22,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "-Xptxas", "-warn-spills"]
 # per-file extra flags: the exact kernel must never contract a*b+c into FMA
-EXTRA = {"heat_exact.cu": ["--fmad=false"]}
-SOURCES = ["heat_capi.cu", "heat_sample.cu", "heat_exact.cu", "heat_hogwild.cu", "heat_hogwild_staged.cu",
+EXTRA = {"heat_exact.cu": ["--fmad=false"], "heat_exact_spec.cu": ["--fmad=false"]}
+SOURCES = ["heat_capi.cu", "heat_sample.cu", "heat_exact.cu", "heat_exact_spec.cu",
+           "heat_hogwild.cu", "heat_hogwild_staged.cu",
            "heat_hogwild_resident.cu",
            "heat_eval.cu", "heat_host.cpp"]
 

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 
 #include "heat_common.cuh"
@@ -123,8 +124,18 @@ const char *heat_last_error(void) { return g_err.c_str(); }
 
 int heat_version(void) { return 1; }
 
-int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim) {
-    return (int64_t)n_neg * (int64_t)dim * (int64_t)sizeof(float) + 256;
+/* Diagnostics of the parallel deterministic kernel (not part of the
+ * reference interface): clock64 totals [speculate, token wait, commit],
+ * [partial recomputes, full recomputes, pairs]; `reset` zeroes them. */
+int heat_exact_stats(unsigned long long *out, int reset) {
+    exact_spec_stats(out, reset != 0);
+    return HEAT_OK;
+}
+
+int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim, int64_t s_rows, int64_t t_rows) {
+    const int64_t serial = (int64_t)n_neg * (int64_t)dim * (int64_t)sizeof(float) + 256;
+    const int64_t spec = (int64_t)exact_spec_scratch_bytes(dim, n_neg, s_rows, t_rows);
+    return serial > spec ? serial : spec;
 }
 
 int heat_sample_negatives(uint64_t stream_base, int64_t first_pair, int64_t npairs,
@@ -174,10 +185,24 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
     cudaError_t e;
     switch (p->mode) {
     case HEAT_MODE_EXACT: {
+        // speculative in-order-commit kernel (parallel, bit-identical) unless
+        // the shape or the aggregator needs the serial one
+        if (!agg && exact_spec_supported(p->dim, p->n_neg) && !getenv("HEAT_EXACT_SERIAL")) {
+            void *sc = scratch ? scratch
+                               : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim, s_rows,
+                                                                        t_rows));
+            if (!sc) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
+            e = launch_exact_spec(S, s_rows, T, t_rows, ep_users, ep_items, start, stop, p->dim,
+                                  p->n_neg, p->use_cosine, p->lr, p->l2, p->mu, p->theta,
+                                  p->stream_base, counters, sc, pair_index, st);
+            break;
+        }
         if (exact_smem_bytes(p->dim, p->n_neg) > 220 * 1024)
             return fail(HEAT_ERR_UNSUPPORTED, "exact mode: n_neg=%d dim=%d exceeds shared memory",
                         p->n_neg, p->dim);
-        void *snap = scratch ? scratch : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim));
+        void *snap = scratch ? scratch
+                             : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim, s_rows,
+                                                                      t_rows));
         if (!snap) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
         e = launch_exact(S, T, ep_users, ep_items, start, stop, p->dim, p->n_neg, p->use_cosine,
                          p->lr, p->l2, p->mu, p->theta, p->stream_base, t_rows, counters,

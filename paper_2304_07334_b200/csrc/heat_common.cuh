@@ -155,3 +155,64 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 }  // namespace heat
+
+// ---- binary64 row dots in the reference's order, loads batched ------------
+// tt = sum_k v_k*v_k and st = sum_k u_k*v_k accumulated strictly in k order
+// with separate round-to-nearest multiply and add (trainer.py:193-197), the
+// row read in bursts of up to 64 floats (16 independent 16-byte loads) so a
+// row costs one or two memory latencies instead of one per element.
+namespace heat {
+
+template <int K>
+__device__ __forceinline__ void row_dots_f64(const float *__restrict__ row, const double *ubuf,
+                                             double &tt, double &st) {
+    constexpr int C4 = K / 4;
+    constexpr int B4 = C4 < 16 ? C4 : 16;  // float4s per burst
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int c0 = 0; c0 < C4; c0 += B4) {
+        float4 v[B4];
+#pragma unroll
+        for (int c = 0; c < B4; ++c) v[c] = r4[c0 + c];
+#pragma unroll
+        for (int c = 0; c < B4; ++c) {
+            const int k = 4 * (c0 + c);
+            const double x0 = (double)v[c].x, x1 = (double)v[c].y, x2 = (double)v[c].z,
+                         x3 = (double)v[c].w;
+            a = __dadd_rn(a, __dmul_rn(x0, x0)); b = __dadd_rn(b, __dmul_rn(ubuf[k], x0));
+            a = __dadd_rn(a, __dmul_rn(x1, x1)); b = __dadd_rn(b, __dmul_rn(ubuf[k + 1], x1));
+            a = __dadd_rn(a, __dmul_rn(x2, x2)); b = __dadd_rn(b, __dmul_rn(ubuf[k + 2], x2));
+            a = __dadd_rn(a, __dmul_rn(x3, x3)); b = __dadd_rn(b, __dmul_rn(ubuf[k + 3], x3));
+        }
+    }
+    tt = a;
+    st = b;
+}
+
+// runtime-K dispatch: templated bursts for K in {16,32,64,128,256} (16-byte
+// aligned rows), a scalar sequential loop otherwise
+__device__ __forceinline__ void row_dots_any(const float *__restrict__ row, const double *ubuf,
+                                             int K, double &tt, double &st) {
+    const bool al = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+    if (al) {
+        switch (K) {
+        case 16: row_dots_f64<16>(row, ubuf, tt, st); return;
+        case 32: row_dots_f64<32>(row, ubuf, tt, st); return;
+        case 64: row_dots_f64<64>(row, ubuf, tt, st); return;
+        case 128: row_dots_f64<128>(row, ubuf, tt, st); return;
+        case 256: row_dots_f64<256>(row, ubuf, tt, st); return;
+        default: break;
+        }
+    }
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < K; ++k) {
+        const double x = (double)row[k];
+        a = __dadd_rn(a, __dmul_rn(x, x));
+        b = __dadd_rn(b, __dmul_rn(ubuf[k], x));
+    }
+    tt = a;
+    st = b;
+}
+
+}  // namespace heat

@@ -44,28 +44,6 @@ struct ExactSmem {
     int warp_cnt[kExactWarps];
 };
 
-__device__ __forceinline__ void row_dots(const float *__restrict__ row, const double *ubuf, int K,
-                                         double &tt, double &st) {
-    // trainer.py:193-197: tt += v*v; st += u*v, k ascending, binary64.
-    double a = 0.0, b = 0.0;
-    int k = 0;
-    for (; k + 4 <= K; k += 4) {
-        float v0 = row[k], v1 = row[k + 1], v2 = row[k + 2], v3 = row[k + 3];
-        double x0 = (double)v0, x1 = (double)v1, x2 = (double)v2, x3 = (double)v3;
-        a = DADD(a, DMUL(x0, x0)); b = DADD(b, DMUL(ubuf[k], x0));
-        a = DADD(a, DMUL(x1, x1)); b = DADD(b, DMUL(ubuf[k + 1], x1));
-        a = DADD(a, DMUL(x2, x2)); b = DADD(b, DMUL(ubuf[k + 2], x2));
-        a = DADD(a, DMUL(x3, x3)); b = DADD(b, DMUL(ubuf[k + 3], x3));
-    }
-    for (; k < K; ++k) {
-        double x = (double)row[k];
-        a = DADD(a, DMUL(x, x));
-        b = DADD(b, DMUL(ubuf[k], x));
-    }
-    tt = a;
-    st = b;
-}
-
 __global__ void __launch_bounds__(kExactThreads, 1)
     exact_kernel(float *__restrict__ S, float *__restrict__ T, const int32_t *__restrict__ users,
                  const int32_t *__restrict__ items, int64_t start, int64_t stop, int K, int N,
@@ -152,7 +130,7 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                 sh.tt_p = a;
                 sh.st_p = b;
             } else {
-                row_dots(T + (int64_t)nids[r - 1] * K, ubuf, K, tt, st);
+                row_dots_any(T + (int64_t)nids[r - 1] * K, ubuf, K, tt, st);
                 tts[r - 1] = tt;
                 sts[r - 1] = st;
             }

@@ -64,6 +64,15 @@ cudaError_t launch_aggregate_users(const float *S, const float *T, const float *
                                    int64_t n_users, int64_t tr_num_users, int K, double gamma,
                                    int64_t max_history, double *out, cudaStream_t st);
 
+bool exact_spec_supported(int K, int N);
+void exact_spec_stats(unsigned long long *out, bool reset);
+size_t exact_spec_scratch_bytes(int K, int N, int64_t s_rows, int64_t t_rows);
+cudaError_t launch_exact_spec(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                              const int32_t *users, const int32_t *items, int64_t start,
+                              int64_t stop, int K, int N, int cosine, double lr, double l2,
+                              double mu, double theta, uint64_t s0, heat_counters *ctr,
+                              void *scratch, const int64_t *pair_index, cudaStream_t stream);
+
 int sm_count();
 size_t eval_max_k_supported(int K);
 

@@ -98,7 +98,8 @@ class DeviceModel:
 
     # -- training ---------------------------------------------------------
     def scratch(self, n_neg: int) -> torch.Tensor:
-        need = int(N.lib().heat_scratch_bytes(n_neg, self.dim))
+        need = int(N.lib().heat_scratch_bytes(n_neg, self.dim, self.S.shape[0],
+                                              self.T.shape[0]))
         if self._scratch is None or self._scratch.numel() < need:
             self._scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._scratch

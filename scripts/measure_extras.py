@@ -48,9 +48,18 @@ def exact(cfg_name, npairs):
                  cosine=True, mode=N.MODE_EXACT, stream_base=epoch_stream(0, 0))
     m.train_range(du, di, 0, min(n, 256), p)
     torch.cuda.synchronize()
+    import ctypes
+    st = (ctypes.c_ulonglong * 8)()
+    N.lib().heat_exact_stats(st, 1)
     dt = timed(lambda: m.train_range(du, di, 0, n, p))
+    N.lib().heat_exact_stats(st, 1)
+    pairs = max(1, st[5])
     print(json.dumps({"what": "exact_mode", "config": cfg_name, "pairs": n, "seconds": dt,
-                      "samples_per_s": n / dt}), flush=True)
+                      "samples_per_s": n / dt,
+                      "cycles_per_pair": {"speculate": st[0] / pairs, "wait": st[1] / pairs,
+                                          "commit": st[2] / pairs},
+                      "recompute_frac": {"partial": st[3] / pairs, "full": st[4] / pairs}}),
+          flush=True)
 
 
 def evaluation(cfg_name):

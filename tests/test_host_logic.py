@@ -32,7 +32,7 @@ def test_abi_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert _native.lib().heat_version() == 1
-    assert _native.lib().heat_scratch_bytes(10, 32) >= 10 * 32 * 4
+    assert _native.lib().heat_scratch_bytes(10, 32, 100, 200) >= 10 * 32 * 4 + 300 * 4
 
 
 def test_abi_rejects_bad_arguments_without_a_gpu():
