@@ -19,6 +19,8 @@
  *   heat_apply_row_deltas  <- (new) multi-GPU item-delta exchange, SURVEY.md §8(e)
  *   heat_epoch_pairs       <- dataset.epoch_pairs (host)    dataset.py:146-158
  *   heat_aggregate_users   <- evaluator._aggregated_user_vectors evaluator.py:91-110
+ *   heat_train_range(agg)  <- _train_chunk agg_on branch     trainer.py:148-173, 299-331
+ *   heat_agg_scratch_bytes <- _ThreadState agg buffers      trainer.py:334-363
  */
 #ifndef HEAT_B200_H
 #define HEAT_B200_H
@@ -96,8 +98,13 @@ typedef struct heat_counters {
  * `pair_index` (optional, int64 per pair) is the pair's global epoch position,
  * the key of its negative draws (a user shard trains a subset of the epoch
  * and must draw the 1-GPU run's negatives); NULL means position p itself.
- * `agg` (optional) turns on behaviour aggregation (HEAT_MODE_EXACT only in
- * this version; other modes return HEAT_ERR_UNSUPPORTED).
+ * `agg` (optional) turns on behaviour aggregation.  HEAT_MODE_EXACT follows
+ * the reference's single thread bit for bit (accu/counter carry the flush
+ * state).  HEAT_MODE_HOGWILD runs steps of `window` pairs (4096 when <= 0)
+ * with W frozen inside a step and every pair's (agg_lr/mini_batch) *
+ * pooled (x) ugrad added to W after it (accu/counter unused); `scratch` is then
+ * NULL or at least heat_agg_scratch_bytes(dim, window) bytes.  DELTA mode
+ * returns HEAT_ERR_UNSUPPORTED.
  * Scratch (HEAT_MODE_EXACT): `scratch` may be NULL (internal allocation) or a
  * device buffer of at least heat_scratch_bytes(n_neg, dim, s_rows, t_rows)
  * bytes (active-row snapshots and the per-row commit stamps of the parallel
@@ -110,6 +117,10 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                      const heat_agg_params *agg, void *scratch, void *stream);
 
 int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim, int64_t s_rows, int64_t t_rows);
+
+/* Scratch of HEAT_MODE_HOGWILD with aggregation (per-step pooled histories,
+ * queries and user gradients). */
+int64_t heat_agg_scratch_bytes(int32_t dim, int32_t window);
 
 /* out[(p - first_pair) * n_neg + j] = negative j of pair p, for
  * p in [first_pair, first_pair + npairs): the id trainer.py:136 draws. */

@@ -23,7 +23,7 @@ MODE_DELTA = 2
 
 EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
            "heat_eval_users", "heat_apply_row_deltas", "heat_epoch_pairs",
-           "heat_aggregate_users", "heat_exact_stats", "heat_last_error", "heat_version")
+           "heat_aggregate_users", "heat_agg_scratch_bytes", "heat_exact_stats", "heat_last_error", "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -104,6 +104,8 @@ def lib():
     L.heat_epoch_pairs.argtypes = [P, i64, P, i64, u64, u64, u64, u64, i32, ctypes.c_uint32, P, P]
     L.heat_aggregate_users.restype = ctypes.c_int
     L.heat_aggregate_users.argtypes = [P, i64, P, P, i32, P, P, i64, ctypes.c_double, i64, P, P]
+    L.heat_agg_scratch_bytes.restype = i64
+    L.heat_agg_scratch_bytes.argtypes = [i32, i32]
     L.heat_exact_stats.restype = ctypes.c_int
     L.heat_exact_stats.argtypes = [P, ctypes.c_int]
     L.heat_last_error.restype = ctypes.c_char_p

@@ -138,6 +138,10 @@ int64_t heat_scratch_bytes(int32_t n_neg, int32_t dim, int64_t s_rows, int64_t t
     return serial > spec ? serial : spec;
 }
 
+int64_t heat_agg_scratch_bytes(int32_t dim, int32_t window) {
+    return (int64_t)agg_hogwild_scratch_bytes(dim, window);
+}
+
 int heat_sample_negatives(uint64_t stream_base, int64_t first_pair, int64_t npairs,
                           int32_t n_neg, int64_t num_items, int32_t *out, void *stream) {
     if (n_neg < 1) return fail(HEAT_ERR_INVALID, "num_negatives must be >= 1, got %d", n_neg);
@@ -172,10 +176,16 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
     if (stop > start && (!ep_users || !ep_items)) return fail(HEAT_ERR_INVALID, "null pairs");
     cudaStream_t st = (cudaStream_t)stream;
     if (agg) {
-        if (p->mode != HEAT_MODE_EXACT)
-            return fail(HEAT_ERR_UNSUPPORTED, "aggregation is implemented in EXACT mode only");
-        if (!agg->W || !agg->tr_offsets || !agg->accu || !agg->counter)
-            return fail(HEAT_ERR_INVALID, "aggregation needs W, train CSR, accu and counter");
+        if (p->mode == HEAT_MODE_DELTA)
+            return fail(HEAT_ERR_UNSUPPORTED, "aggregation is not implemented in DELTA mode");
+        if (!agg->W || !agg->tr_offsets || !agg->tr_items)
+            return fail(HEAT_ERR_INVALID, "aggregation needs W and the train CSR");
+        if (p->mode == HEAT_MODE_EXACT && (!agg->accu || !agg->counter))
+            return fail(HEAT_ERR_INVALID, "EXACT aggregation needs the accumulator and counter");
+        if (p->mode == HEAT_MODE_HOGWILD && p->dim != 16 && p->dim != 32 && p->dim != 64 &&
+            p->dim != 128)
+            return fail(HEAT_ERR_UNSUPPORTED,
+                        "hogwild aggregation supports dim in {16, 32, 64, 128}, got %d", p->dim);
         if (!(agg->gamma >= 0.0 && agg->gamma <= 1.0))
             return fail(HEAT_ERR_INVALID, "gamma must be in [0, 1], got %g", agg->gamma);
         if (agg->mini_batch < 1 || agg->max_history < 0)
@@ -226,6 +236,15 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         a.delta_rows = delta_rows; a.delta_count = delta_count;
         a.delta_capacity = delta_capacity;
         a.pair_index = pair_index;
+        if (agg) {
+            void *sc = scratch ? scratch
+                               : get_scratch(agg_hogwild_scratch_bytes(p->dim, p->window));
+            if (!sc) return fail(HEAT_ERR_CUDA, "aggregation: scratch allocation failed");
+            e = launch_agg_hogwild(a, *agg, sc, st);
+            if (e == cudaErrorNotSupported)
+                return fail(HEAT_ERR_UNSUPPORTED, "hogwild aggregation: unaligned tables/scratch");
+            break;
+        }
         e = launch_hogwild(a, st, nullptr);
         break;
     }

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(32)
     int ps = 0, pslot = 0, pus = 0;
     int32_t pf_u = a.users[a.start + gw];
     int32_t pf_pos = a.items[a.start + gw];
+    int64_t pf_p = a.start + gw;  // pair whose user row the producer loads next
     int32_t nx_u = 0, nx_pos = 0;
     if (my_pairs > 1) {
         nx_u = a.users[a.start + gw + n_workers];
@@ -152,6 +153,10 @@ __global__ void __launch_bounds__(32)
     // Issue stage g_next if it is below `limit`; the cp.async mover commits
     // one (possibly empty) group per call so wait_group<D-1> always targets
     // the stage being consumed.
+    // query row of a pair: S[u], or the aggregated query h (trainer.py:148-173)
+    auto qrow = [&](int64_t pp, int32_t uu_) -> const float * {
+        return a.query ? a.query + (pp - a.start) * K : a.S + (int64_t)uu_ * K;
+    };
     auto issue = [&](int64_t limit) {
         if (g_next >= limit) {
             if constexpr (!BULK) cp_async_commit();
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(32)
             if (lane == 0) {
                 if (ps == 0) {
                     mbar_arrive_expect_tx(&ubars[pus], G::ROWB);
-                    bulk_g2s(urow + pus * K, a.S + (int64_t)pf_u * K, G::ROWB, &ubars[pus]);
+                    bulk_g2s(urow + pus * K, qrow(pf_p, pf_u), G::ROWB, &ubars[pus]);
                 }
                 mbar_arrive_expect_tx(&bars[pslot], (uint32_t)(nvalid * G::ROWB));
             }
@@ -190,9 +195,11 @@ __global__ void __launch_bounds__(32)
                 if (row < nvalid)
                     cp_async16_hint(dst + i * RPI * G::SLOTF, srcb + (size_t)rid * K, pol);
             }
-            if (ps == 0)
+            if (ps == 0) {
+                const float *q = qrow(pf_p, pf_u);
                 for (int ch = lane; ch < G::CH; ch += 32)
-                    cp_async16(urow + pus * K + ch * 4, a.S + (int64_t)pf_u * K + ch * 4);
+                    cp_async16(urow + pus * K + ch * 4, q + ch * 4);
+            }
             cp_async_commit();
         }
         ++g_next;
@@ -205,6 +212,7 @@ __global__ void __launch_bounds__(32)
             pf_u = nx_u;
             pf_pos = nx_pos;
             const int64_t pn = a.start + gw + pt * n_workers;
+            pf_p = pn;
             if (pt < my_pairs)
                 rng_state = a.s0 + (rng_key(pn) * (uint64_t)N + (uint64_t)lane) * kGamma;
             if (pt + 1 < my_pairs) {
@@ -387,11 +395,29 @@ __global__ void __launch_bounds__(32)
             issue(limit);  // refill this slot with the stage D ahead
         }
         flush();
-        // user row (trainer.py:291-293): S[u] -= lr * (ugrad + l2 * S[u])
+        // user row (trainer.py:291-293): S[u] -= lr * (ugrad + l2 * S[u]); with
+        // aggregation the gamma-scaled chain (trainer.py:301-302) and the
+        // gradient kept for the weight update
         if (lane < G::ACT) {
             float d[VW];
+            if (a.query) {
+                float sv[VW];
 #pragma unroll
-            for (int i = 0; i < VW; ++i) d[i] = -a.lr * (ug[i] + a.l2 * uu[i]);
+                for (int i = 0; i < VW; ++i) sv[i] = 0.f;
+                if (a.l2 != 0.f) {
+#pragma unroll
+                    for (int i = 0; i < VW; ++i) sv[i] = a.S[u * K + lane * VW + i];
+                }
+                float *go = a.ugrad_out + (p - a.start) * K + lane * VW;
+#pragma unroll
+                for (int i = 0; i < VW; ++i) {
+                    d[i] = -a.lr * (a.ugamma * ug[i] + a.l2 * sv[i]);
+                    go[i] = ug[i];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < VW; ++i) d[i] = -a.lr * (ug[i] + a.l2 * uu[i]);
+            }
             red_add_vec<VW>(a.S + u * K + lane * VW, d);
         }
 #pragma unroll

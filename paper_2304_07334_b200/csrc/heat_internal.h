@@ -38,12 +38,22 @@ struct HogwildArgs {
     int64_t delta_capacity;
     // global epoch position of local pair p (RNG key); NULL = p itself
     const int64_t *pair_index;
+    // behaviour aggregation (throughput mode): the query of local pair p is
+    // query[(p - start) * K] instead of S[u]; the user gradient is written to
+    // ugrad_out[(p - start) * K] and S[u] -= lr * (ugamma * ugrad + l2 * S[u])
+    const float *query = nullptr;
+    float *ugrad_out = nullptr;
+    float ugamma = 1.f;
 };
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_resident(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t stream, int *workers_out,
                                   bool bulk);
+
+size_t agg_hogwild_scratch_bytes(int K, int window);
+cudaError_t launch_agg_hogwild(const HogwildArgs &base, const heat_agg_params &agg,
+                               void *scratch, cudaStream_t stream);
 
 cudaError_t launch_sample(uint64_t s0, int64_t first_pair, int64_t npairs, int N,
                           int64_t num_items, int32_t *out, cudaStream_t stream);

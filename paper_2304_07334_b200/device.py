@@ -115,7 +115,11 @@ class DeviceModel:
                     params: N.SgdParams, delta=None, pair_index: torch.Tensor | None = None,
                     stream=None, agg: "DeviceAggregator | None" = None) -> None:
         """Launch pairs [start, stop) on the current stream (asynchronous)."""
-        scratch = self.scratch(params.n_neg) if params.mode == N.MODE_EXACT else None
+        scratch = None
+        if params.mode == N.MODE_EXACT:
+            scratch = self.scratch(params.n_neg)
+        elif agg is not None:
+            scratch = agg.work(self.dim, params.window)
         d_ids = d_rows = d_cnt = None
         cap = 0
         if delta is not None:
@@ -150,6 +154,14 @@ class DeviceAggregator:
         self.max_history = int(cfg_agg.max_history)
         self.history_grad = bool(cfg_agg.history_grad)
         self._p = None
+        self._work = None
+
+    def work(self, dim: int, window: int) -> torch.Tensor:
+        """Per-step buffers of the throughput aggregator (heat_agg_scratch_bytes)."""
+        need = int(N.lib().heat_agg_scratch_bytes(dim, window))
+        if self._work is None or self._work.numel() < need:
+            self._work = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._work
 
     def reset_epoch(self) -> None:
         self.accu.zero_()

@@ -14,8 +14,10 @@ CUDA kernels of csrc/ through the C ABI:
 
 ``configure(mode=…, window=…)`` or the env vars ``HEAT_B200_MODE``
 (``exact`` | ``hogwild``) and ``HEAT_B200_WINDOW`` override the mapping.
-The tiling sampler and the aggregator are outside the built path and raise
-ValueError (no CPU fallback).
+Behaviour aggregation (SimpleX, trainer.py:148-173, 299-331) runs in both
+modes: bit-identical in EXACT, in steps of ``window`` pairs with the shared W
+frozen inside a step in Hogwild (csrc/heat_agg_hogwild.cu).  The tiling
+sampler is outside the built path and raises ValueError (no CPU fallback).
 """
 
 from __future__ import annotations
@@ -119,15 +121,18 @@ def _make_aggregator(model: DeviceModel, weights, train, cfg):
                             model.device)
 
 
+AGG_HOGWILD_DIMS = (16, 32, 64, 128)
+
+
 def resolve_mode(cfg) -> int:
-    if cfg.aggregator.enabled:
-        # shared-W aggregation is implemented in the deterministic kernel
-        # (bit-exact with the reference); an explicit Hogwild request is refused
-        if _OPTIONS.mode == "hogwild":
-            raise ValueError("behaviour aggregation is implemented in EXACT mode only; "
-                             "no CPU fallback")
-        return N.MODE_EXACT
     mode = _OPTIONS.mode or ("exact" if cfg.num_threads == 1 else "hogwild")
+    if cfg.aggregator.enabled and mode == "hogwild" and cfg.emb_dim not in AGG_HOGWILD_DIMS:
+        # the throughput aggregator is built for these widths; otherwise the
+        # deterministic kernel runs (a valid schedule of a multi-thread run)
+        if _OPTIONS.mode == "hogwild":
+            raise ValueError(f"hogwild aggregation supports emb_dim in {AGG_HOGWILD_DIMS}, "
+                             f"got {cfg.emb_dim}; no CPU fallback")
+        mode = "exact"
     return N.MODE_EXACT if mode == "exact" else N.MODE_HOGWILD
 
 

@@ -575,3 +575,104 @@ def test_aggregated_evaluation_query(torch_cuda):
         assert m.users_evaluated == n
         assert m.recall_at_k == pytest.approx(rec, abs=1e-12)
         assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12)
+
+
+def _agg_case(rng, nu, ni, K):
+    from paper_2304_07334_b200.dataset import from_user_lists
+    tr = from_user_lists({u: rng.integers(0, ni, int(rng.integers(0, 30))) for u in range(nu)},
+                         num_users=nu, num_items=ni)
+    S = (rng.standard_normal((nu, K)) * 0.1).astype(np.float32)
+    T = (rng.standard_normal((ni, K)) * 0.1).astype(np.float32)
+    W = (rng.standard_normal((K, K)) / np.sqrt(K)).astype(np.float32)
+    return tr, S, T, W
+
+
+@pytest.mark.parametrize("K,N,gamma,hist,l2,cos,mh", [
+    (16, 7, 0.5, False, 0.0, True, 100), (32, 20, 0.3, True, 0.01, True, 10),
+    (64, 50, 0.0, True, 0.0, False, 100), (128, 64, 1.0, False, 0.0, True, 100),
+    (128, 40, 0.2, True, 0.0, True, 5)])
+def test_agg_hogwild_window1_vs_oracle(torch_cuda, K, N, gamma, hist, l2, cos, mh):
+    """Throughput aggregator (csrc/heat_agg_hogwild.cu) with one pair per step
+    and mini_batch 1: the reference flushes W after every pair too, so the
+    sequence of reads and writes is the reference's (trainer.py:148-173,
+    299-331); fp32 arithmetic tracks it within 1e-4 norm-relative."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.config import AggregatorConfig
+    from paper_2304_07334_b200.device import DeviceAggregator, DeviceModel
+    rng = np.random.default_rng(K * 7 + N)
+    nu, ni, P = 40, 250, 500
+    tr, S, T, W = _agg_case(rng, nu, ni, K)
+    u = rng.integers(0, nu, P).astype(np.int32)
+    i = rng.integers(0, ni, P).astype(np.int32)
+    s0 = 0x0DDC0FFEE0DDF00D
+    S2, T2, W2 = S.copy(), T.copy(), W.copy()
+    st = O.AggState(W=W2, tr_offsets=tr.offsets, tr_items=tr.items, gamma=gamma, lr=0.02,
+                    mini_batch=1, max_history=mh, history_grad=hist)
+    r = O.train_range(S2, T2, u, i, 0, P, s0, n_neg=N, lr=0.01, l2=l2, mu=2.0, theta=0.1,
+                      cosine=cos, agg=st)
+    model = DeviceModel(S, T)
+    cfg_agg = AggregatorConfig(enabled=True, gamma=gamma, max_history=mh, mini_batch_size=1,
+                               history_grad=hist, learning_rate=0.02)
+    agg = DeviceAggregator(W.copy(), tr, cfg_agg, 0.01, model.device)
+    du, di = model.upload_pairs(u, i)
+    p = model.params(n_neg=N, lr=0.01, l2=l2, mu=2.0, theta=0.1, cosine=cos,
+                     mode=NN.MODE_HOGWILD, stream_base=s0, window=1)
+    model.counters.reset()
+    model.train_range(du, di, 0, P, p, agg=agg)
+    c = model.counters.read()
+    model.download(S, T)
+    Wg = agg.W.cpu().numpy()
+    assert c.pairs == P
+    assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss), (c.loss, r.loss)
+    assert _rel_fro(S, S2) <= 1e-4, _rel_fro(S, S2)
+    assert _rel_fro(T, T2) <= 1e-4, _rel_fro(T, T2)
+    assert _rel_fro(Wg, W2) <= 1e-4, _rel_fro(Wg, W2)
+
+
+def test_agg_hogwild_quality_matches_oracle(torch_cuda):
+    """Throughput aggregator under concurrency (256-pair steps, W frozen per
+    step): training descends and the aggregated-query recall@20 after 20
+    epochs matches the oracle's single-thread run within 0.01, the
+    reference's own thread-parity bound (test_trainer.py:199-208)."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
+    from paper_2304_07334_b200.config import AggregatorConfig
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.evaluator import evaluate
+    from paper_2304_07334_b200.rng import shuffle_seed
+    from paper_2304_07334_b200.synth import make_clustered
+    from paper_2304_07334_b200.trainer import configure, train_epoch
+    train, test = make_clustered(800, 1600, 16, 40, affinity=0.97, seed=11)
+    K, E = 32, 20
+    acfg = AggregatorConfig(enabled=True, gamma=0.5, max_history=20, mini_batch_size=32)
+    cfg = TrainingConfig(emb_dim=K, num_negatives=16, learning_rate=0.05, num_threads=8,
+                         loss=LossParams(mu=1.0, theta=0.8), seed=7, aggregator=acfg)
+    S = init_matrix(800, K, InitSpec(seed=1))
+    T = init_matrix(1600, K, InitSpec(seed=2))
+    W = np.eye(K, dtype=np.float32)
+    So, To, Wo = S.values.copy(), T.values.copy(), W.copy()
+    losses = []
+    configure(mode="hogwild", window=256)
+    try:
+        for e in range(E):
+            losses.append(train_epoch(S, T, train, cfg, W, epoch=e).mean_loss)
+    finally:
+        configure(mode=None, window=0)
+    assert np.isfinite(losses).all() and losses[-1] < losses[0], losses
+    m_gpu = evaluate(S, T, train, test, cfg, weights=W, k=20)
+    for e in range(E):
+        u, i = epoch_pairs(train, shuffle_seed(7, e))
+        st = O.AggState(W=Wo, tr_offsets=train.offsets, tr_items=train.items, gamma=0.5,
+                        lr=0.05, mini_batch=32, max_history=20)
+        O.train_range(So, To, u, i, 0, len(u), O.derive_stream(7, 0x45504F43, e, 0),
+                      n_neg=16, lr=0.05, mu=1.0, theta=0.8, agg=st)
+    pooled = np.zeros((800, K))
+    for uu in range(800):
+        h = train.slice(uu)[:20]
+        if len(h):
+            pooled[uu] = To[h].astype(np.float64).mean(axis=0)
+    q = 0.5 * So.astype(np.float64) + 0.5 * (pooled @ Wo.astype(np.float64))
+    rec_ref, _, _ = O.evaluate_ref(q, To, train.offsets, train.items, 800, test.offsets,
+                                   test.items, 800, k=20)
+    assert abs(m_gpu.recall_at_k - rec_ref) <= 0.01, (m_gpu.recall_at_k, rec_ref)
