@@ -50,17 +50,30 @@ class DeviceCounters:
 
     def __init__(self, dev: torch.device):
         self.buf = torch.zeros(N.COUNTERS_BYTES, dtype=torch.uint8, device=dev)
+        self.host = torch.zeros(N.COUNTERS_BYTES, dtype=torch.uint8).pin_memory()
 
     def reset(self, loss: float = 0.0) -> None:
+        if loss == 0.0:
+            self.buf.zero_()  # stream-ordered memset, no host round trip
+            return
         host = np.zeros(N.COUNTERS_BYTES, dtype=np.uint8)
         host[:8] = np.frombuffer(np.float64(loss).tobytes(), dtype=np.uint8)
         self.buf.copy_(torch.from_numpy(host))
 
-    def read(self) -> CounterValues:
-        h = self.buf.cpu().numpy()
+    def fetch(self) -> None:
+        """Queue the device->host copy (read with `values()` after a sync)."""
+        self.host.copy_(self.buf, non_blocking=True)
+
+    def values(self) -> CounterValues:
+        h = self.host.numpy()
         loss = float(h[:8].view(np.float64)[0])
         ints = h[8:32].view(np.int64)
         return CounterValues(loss, int(ints[0]), int(ints[1]), int(ints[2]))
+
+    def read(self) -> CounterValues:
+        self.fetch()
+        torch.cuda.current_stream(self.buf.device).synchronize()
+        return self.values()
 
     def ptr(self):
         return _p(self.buf)

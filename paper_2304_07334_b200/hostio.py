@@ -6,10 +6,11 @@ The reference's ``train_epoch`` mutates the caller's numpy tables in place
 S, T and the pair order and a device->host copy of S and T per call.  This
 module keeps that host work off the critical path:
 
-* ``PairPrefetcher`` — after epoch e's order is produced, epoch e+1's order
-  (same interaction set, same seed) is computed on a host thread by the
-  native shuffle (csrc/heat_host.cpp, GIL released) into page-locked buffers,
-  so a training loop calling train_epoch(epoch=e+1) finds it ready;
+* ``PairPrefetcher`` — after epoch e's order is produced, the orders of
+  epochs e+1 .. e+DEPTH (same interaction set, same seed) are computed on
+  host threads by the native shuffle (csrc/heat_host.cpp, GIL released) into
+  page-locked buffers, so a training loop calling train_epoch(epoch=e+1)
+  finds it ready;
 * ``pin_array`` — page-locks a caller's numpy buffer once (cudaHostRegister)
   so table copies run as async DMA at full PCIe rate; registrations are kept
   in a small LRU that also holds a reference to the array, so a registered
@@ -18,6 +19,7 @@ module keeps that host work off the critical path:
 
 from __future__ import annotations
 
+import os
 import threading
 from collections import OrderedDict
 
@@ -70,7 +72,11 @@ class PairPrefetcher:
                 return holder["bufs"]
         return self._compute(train, seed, self._buffers(train.num_pairs))
 
-    MAX_PENDING = 3
+    # epochs computed ahead, one host thread each: the shuffle is sequential
+    # (numpy's Fisher-Yates) and takes longer than a GPU epoch, so several
+    # epochs are in flight at once when the host has the cores
+    DEPTH = 4 if (os.cpu_count() or 1) >= 8 else 2
+    MAX_PENDING = DEPTH + 1
 
     def prefetch(self, train, seed: int) -> None:
         key = (_train_key(train), seed)
