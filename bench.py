@@ -198,6 +198,12 @@ def main():
     ap.add_argument("--window", type=int, default=0, help="pairs in flight (0: config batch)")
     ap.add_argument("--fp64", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="user-sharded path even at N=1")
+    ap.add_argument("--shard-driver", choices=("native", "python"), default="native",
+                    help="sharded path: step scheduler (native C++ runtime or the Python "
+                         "reference pipeline)")
+    ap.add_argument("--exchange-pairs", type=int, default=0,
+                    help="sharded path: global pairs between item-delta exchanges "
+                         "(default: the config's batch B)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -257,14 +263,16 @@ def main():
             ev1.synchronize()
             return ev0.elapsed_time(ev1) / 1e3, model.counters.read()
     else:
-        from paper_2304_07334_b200.parallel import ShardedTrainer, exchange_deltas
-        trainer = ShardedTrainer(model, world, rank)
+        from paper_2304_07334_b200.parallel import NativeShardTrainer, PipelinedShardTrainer
+        trainer = (PipelinedShardTrainer if args.shard_driver == "python"
+                   else NativeShardTrainer)(model, world, rank)
         host_pairs = [epoch_pairs(train, shuffle_seed(0, e)) for e in range(total_epochs)]
+        exchange_pairs = args.exchange_pairs or spec.batch
 
         def one_epoch(e):
             nonlocal launches_per_epoch
             u, i = host_pairs[e]
-            trainer.prepare_epoch(u, i, params(e), spec.batch)  # shard upload, untimed
+            trainer.prepare_epoch(u, i, params(e), exchange_pairs)  # shard upload, untimed
             model.counters.reset()
             flush.zero_()
             if world > 1:
@@ -272,23 +280,11 @@ def main():
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            nl = 0
-            for s in range(trainer.num_steps):
-                if world > 1:
-                    d_ids, d_rows, d_cnt = trainer.local_step(s, sync=False)
-                    nl += 1
-                    all_ids, all_rows, valid = exchange_deltas(d_ids, d_rows, d_cnt,
-                                                               capacity=trainer.cap)
-                else:
-                    d_ids, d_rows, count = trainer.local_step(s)
-                    nl += 1
-                    all_ids, all_rows = d_ids[:count], d_rows[:count]
-                    valid = torch.ones(count, dtype=torch.bool, device=dev)
-                trainer.apply_ordered(all_ids, all_rows, valid)
-                nl += 1
+            trainer.train_epoch(u, i, params(e), exchange_pairs, prepared=True)
             ev1.record(stream)
             ev1.synchronize()
-            launches_per_epoch = nl
+            # per step: the DELTA kernel + two apply kernels
+            launches_per_epoch = 3 * trainer.num_steps
             return ev0.elapsed_time(ev1) / 1e3, model.counters.read()
 
     for e in range(args.warmup):
@@ -371,7 +367,8 @@ def main():
                        "lr": spec.learning_rate, "step": "one epoch",
                        "l2_flush": "512 MiB write before every timed epoch; S+T "
                                    f"{(S.values.nbytes + T.values.nbytes) / 1e6:.1f} MB",
-                       "parallelism": (f"users sharded x{world}, item-delta all-gather"
+                       "parallelism": (f"users sharded x{world}, pipelined item-delta "
+                                       f"all-gather every {args.exchange_pairs or spec.batch} pairs"
                                        if sharded else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

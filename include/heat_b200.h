@@ -17,6 +17,9 @@
  *   heat_eval_users        <- evaluator.evaluate scoring + top-k + hits
  *                             evaluator.py:140-172, _topk_from_scores 61-73
  *   heat_apply_row_deltas  <- (new) multi-GPU item-delta exchange, SURVEY.md §8(e)
+ *   heat_apply_row_deltas_fixed <- (new) same, order-independent (pipelined exchange)
+ *   heat_shard_*           <- (new) per-rank step scheduler of the sharded epoch;
+ *                             the reference's thread pool  trainer.py:398-447
  *   heat_epoch_pairs       <- dataset.epoch_pairs (host)    dataset.py:146-158
  *   heat_aggregate_users   <- evaluator._aggregated_user_vectors evaluator.py:91-110
  *   heat_train_range(agg)  <- _train_chunk agg_on branch     trainer.py:148-173, 299-331
@@ -155,6 +158,48 @@ int heat_aggregate_users(const float *S, int64_t s_rows, const float *T, const f
 int heat_apply_row_deltas(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,
                           const float *rows, const int64_t *count, int64_t capacity,
                           int32_t ordered, void *stream);
+
+/* Order-independent variant for the pipelined exchange: the all-gathered logs
+ * of `world` ranks (rank r's entries at [r*stride, r*stride + counts[r]),
+ * counts a device array) are summed per (row, column) in 2^-40 fixed point
+ * with integer atomics, then each touched row gets T += float(sum) once; the
+ * result does not depend on atomic ordering, so replicas stay bit-identical
+ * without sorting.  acc (t_rows*dim int64) and flags (t_rows int32) are
+ * caller-owned, zero before the first call, and left zero. */
+int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,
+                                const float *rows, const int64_t *counts, int32_t world,
+                                int64_t stride, int64_t *acc, int32_t *flags, void *stream);
+
+/* ---- multi-GPU runtime --------------------------------
+ * One rank per GPU.  A heat_shard owns the rank's exchange state: two log
+ * slots, the gather buffers, the fixed-point accumulator, a comm stream and
+ * (world > 1) an NCCL communicator created from a unique id that rank 0 makes
+ * with heat_nccl_unique_id and the caller broadcasts (e.g. torch.distributed).
+ * heat_shard_epoch trains the rank's pairs of one epoch: step s covers local
+ * pairs [step_bounds[s], step_bounds[s+1]) (host array), DELTA-mode kernel on
+ * `stream`, then the item-delta all-gather + order-independent apply on the
+ * comm stream, overlapped with the next step's kernel (one-step staleness).
+ * Returns after queueing the last step; work queued later on `stream` sees
+ * every applied step. */
+typedef struct heat_shard heat_shard;
+
+typedef struct heat_shard_stats {
+    int64_t steps;           /* exchanges performed                          */
+    int64_t entries;         /* delta rows applied (sum over ranks and steps) */
+    int64_t exchanged_bytes; /* bytes all-gathered (padded to the max count)  */
+    int64_t max_entries;     /* largest per-rank log of a step               */
+} heat_shard_stats;
+
+int heat_nccl_unique_id(unsigned char *out128);
+int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id, int32_t device,
+                      heat_shard **out);
+int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t t_rows,
+                     const int32_t *local_users, const int32_t *local_items,
+                     const int64_t *pair_index, const int64_t *step_bounds, int64_t nsteps,
+                     int64_t capacity, const heat_sgd_params *params, heat_counters *counters,
+                     heat_shard_stats *stats, void *stream);
+const char *heat_shard_last_error(heat_shard *h);
+int heat_shard_destroy(heat_shard *h);
 
 /* HOST function: one epoch's (user, positive) order, bit-identical to
  * numpy Generator(PCG64(seed)).permutation applied to the CSR pairs

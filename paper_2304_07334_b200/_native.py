@@ -22,8 +22,10 @@ MODE_HOGWILD = 1
 MODE_DELTA = 2
 
 EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
-           "heat_eval_users", "heat_apply_row_deltas", "heat_epoch_pairs",
-           "heat_aggregate_users", "heat_agg_scratch_bytes", "heat_exact_stats", "heat_last_error", "heat_version")
+           "heat_eval_users", "heat_apply_row_deltas", "heat_apply_row_deltas_fixed",
+           "heat_epoch_pairs", "heat_aggregate_users", "heat_agg_scratch_bytes",
+           "heat_exact_stats", "heat_nccl_unique_id", "heat_shard_create", "heat_shard_epoch",
+           "heat_shard_last_error", "heat_shard_destroy", "heat_last_error", "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -70,6 +72,15 @@ class Counters(ctypes.Structure):
 
 COUNTERS_BYTES = ctypes.sizeof(Counters)
 
+
+class ShardStats(ctypes.Structure):
+    _fields_ = [
+        ("steps", ctypes.c_int64),
+        ("entries", ctypes.c_int64),
+        ("exchanged_bytes", ctypes.c_int64),
+        ("max_entries", ctypes.c_int64),
+    ]
+
 _lib = None
 
 
@@ -100,6 +111,19 @@ def lib():
                                   P, P, P, P]
     L.heat_apply_row_deltas.restype = ctypes.c_int
     L.heat_apply_row_deltas.argtypes = [P, i64, i32, P, P, P, i64, i32, P]
+    L.heat_apply_row_deltas_fixed.restype = ctypes.c_int
+    L.heat_apply_row_deltas_fixed.argtypes = [P, i64, i32, P, P, P, i32, i64, P, P, P]
+    L.heat_nccl_unique_id.restype = ctypes.c_int
+    L.heat_nccl_unique_id.argtypes = [P]
+    L.heat_shard_create.restype = ctypes.c_int
+    L.heat_shard_create.argtypes = [i32, i32, P, i32, ctypes.POINTER(ctypes.c_void_p)]
+    L.heat_shard_epoch.restype = ctypes.c_int
+    L.heat_shard_epoch.argtypes = [P, P, i64, P, i64, P, P, P, P, i64, i64,
+                                   ctypes.POINTER(SgdParams), P, ctypes.POINTER(ShardStats), P]
+    L.heat_shard_last_error.restype = ctypes.c_char_p
+    L.heat_shard_last_error.argtypes = [P]
+    L.heat_shard_destroy.restype = ctypes.c_int
+    L.heat_shard_destroy.argtypes = [P]
     L.heat_epoch_pairs.restype = ctypes.c_int
     L.heat_epoch_pairs.argtypes = [P, i64, P, i64, u64, u64, u64, u64, i32, ctypes.c_uint32, P, P]
     L.heat_aggregate_users.restype = ctypes.c_int

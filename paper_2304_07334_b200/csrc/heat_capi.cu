@@ -5,6 +5,7 @@
 // dataclass checks of trainer.py:55-59,79-87 and kernels.py:50-54), and
 // options outside the built path (tiling sampler, aggregator) are rejected by
 // the Python layer with ValueError — there is no CPU fallback.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -100,6 +101,73 @@ __global__ void apply_deltas_atomic(float *__restrict__ T, int K, const int32_t 
         int k = (int)(i % K);
         atomicAdd(T + (int64_t)ids[r] * K + k, rows[i]);
     }
+}
+
+// ---- order-independent (fixed-point) application ---------------------------------
+// Entries e < world*stride, valid when e % stride < counts[e / stride].  Pass 1
+// adds round(delta * 2^40) into an int64 accumulator per (row, column) —
+// integer addition commutes, so the sum is the same whatever order the
+// atomics land in — and flags the row; pass 2 converts each flagged row once:
+// T += float(acc * 2^-40), acc = 0.  Every replica that applies the same
+// gathered logs therefore computes bit-identical rows, with no sort.
+constexpr double kFixScale = 1099511627776.0;  // 2^40: resolution 9.1e-13, range +-8.4e6
+
+__global__ void apply_deltas_fixed_acc(int K, const int32_t *__restrict__ ids,
+                                       const float *__restrict__ rows,
+                                       const int64_t *__restrict__ counts, int world,
+                                       int64_t stride, long long *__restrict__ acc,
+                                       int32_t *__restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = (int64_t)world * stride;
+    for (; w < total; w += nw) {
+        if (w % stride >= counts[w / stride]) continue;
+        const int64_t id = ids[w];
+        if (lane == 0) flags[id] = 1;
+        for (int k = lane; k < K; k += 32) {
+            const long long q = __double2ll_rn((double)rows[w * K + k] * kFixScale);
+            atomicAdd(reinterpret_cast<unsigned long long *>(acc + id * K + k),
+                      (unsigned long long)q);
+        }
+    }
+}
+
+__global__ void apply_deltas_fixed_cvt(float *__restrict__ T, int K,
+                                       const int32_t *__restrict__ ids,
+                                       const int64_t *__restrict__ counts, int world,
+                                       int64_t stride, long long *__restrict__ acc,
+                                       int32_t *__restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t total = (int64_t)world * stride;
+    for (; w < total; w += nw) {
+        if (w % stride >= counts[w / stride]) continue;
+        const int64_t id = ids[w];
+        int mine = 0;
+        if (lane == 0) mine = atomicExch(flags + id, 0);
+        mine = __shfl_sync(0xffffffffu, mine, 0);
+        if (!mine) continue;  // another warp converts this row
+        for (int k = lane; k < K; k += 32) {
+            const long long q = acc[id * K + k];
+            acc[id * K + k] = 0;
+            T[id * K + k] += (float)((double)q * (1.0 / kFixScale));
+        }
+    }
+}
+
+cudaError_t launch_apply_deltas_fixed(float *T, int K, const int32_t *ids, const float *rows,
+                                      const int64_t *counts, int world, int64_t stride,
+                                      long long *acc, int32_t *flags, cudaStream_t st) {
+    const int64_t total = (int64_t)world * stride;
+    if (total <= 0) return cudaSuccess;
+    const int64_t warps = std::min<int64_t>(total, (int64_t)sm_count() * 64);
+    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    apply_deltas_fixed_acc<<<blocks, 256, 0, st>>>(K, ids, rows, counts, world, stride, acc,
+                                                   flags);
+    apply_deltas_fixed_cvt<<<blocks, 256, 0, st>>>(T, K, ids, counts, world, stride, acc, flags);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_apply_deltas(float *T, int64_t t_rows, int K, const int32_t *ids,
@@ -298,6 +366,23 @@ int heat_apply_row_deltas(float *T, int64_t t_rows, int32_t dim, const int32_t *
     cudaError_t e = launch_apply_deltas(T, t_rows, dim, ids, rows, count, capacity, ordered,
                                         (cudaStream_t)stream);
     return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "apply_row_deltas launch");
+}
+
+/* Order-independent replica update for the multi-GPU exchange: the gathered
+ * logs of `world` ranks, rank r's entries at [r*stride, r*stride+counts[r]).
+ * acc: t_rows*dim int64 and flags: t_rows int32, zero on first use and left
+ * zero on return. */
+int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int32_t *ids,
+                                const float *rows, const int64_t *counts, int32_t world,
+                                int64_t stride, int64_t *acc, int32_t *flags, void *stream) {
+    if (!T || !counts || !acc || !flags) return fail(HEAT_ERR_INVALID, "null pointer argument");
+    if (world < 1 || stride < 0) return fail(HEAT_ERR_INVALID, "bad world / stride");
+    if (stride > 0 && (!ids || !rows)) return fail(HEAT_ERR_INVALID, "null log");
+    if (dim < 1 || t_rows < 1) return fail(HEAT_ERR_INVALID, "bad table shape");
+    cudaError_t e = launch_apply_deltas_fixed(T, dim, ids, rows, counts, world, stride,
+                                              reinterpret_cast<long long *>(acc), flags,
+                                              (cudaStream_t)stream);
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "apply_row_deltas_fixed launch");
 }
 
 }  // extern "C"

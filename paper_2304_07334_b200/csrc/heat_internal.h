@@ -69,6 +69,10 @@ cudaError_t launch_apply_deltas(float *T, int64_t t_rows, int K, const int32_t *
                                 const float *rows, const int64_t *count, int64_t capacity,
                                 int ordered, cudaStream_t stream);
 
+cudaError_t launch_apply_deltas_fixed(float *T, int K, const int32_t *ids, const float *rows,
+                                      const int64_t *counts, int world, int64_t stride,
+                                      long long *acc, int32_t *flags, cudaStream_t st);
+
 cudaError_t launch_aggregate_users(const float *S, const float *T, const float *W,
                                    const int64_t *tr_off, const int32_t *tr_items,
                                    int64_t n_users, int64_t tr_num_users, int K, double gamma,

@@ -213,3 +213,238 @@ def gather_users(model: DeviceModel, world: int, rank: int, group=None) -> None:
     part = torch.where(mask, model.S, torch.zeros_like(model.S))
     dist.all_reduce(part, group=group)
     model.S.copy_(part)
+
+
+# ---- pipelined exchange ---------------------------------------------------------
+#
+# The step loop above synchronises the host once per step and applies the
+# union on the compute stream, so the GPU idles while the host sizes and
+# issues the exchange.  The pipelined driver below overlaps them:
+#
+#   compute stream:  kernel(s) -> log slot s%2                (DELTA mode)
+#   comm stream:     all-gather counts(s) -> pinned host copy
+#   host:            waits for counts(s-1) while kernel(s) runs, then issues
+#   comm stream:     all-gather logs(s-1) (cmax entries per rank), fixed-point
+#                    apply(s-1) -> T, concurrently with kernel(s)
+#
+# kernel(s) waits for apply(s-2) (its log slot and the staleness bound): it
+# reads T with every union up to s-2 applied and union s-1 possibly in flight,
+# a one-step staleness that Hogwild tolerates.  T changes
+# only through the applies, which every rank performs on the same gathered
+# logs with an order-independent sum (heat_apply_row_deltas_fixed), so the
+# replicas stay bit-identical however reads and applies interleave.
+
+@dataclass
+class GatherRequest:
+    """One all-gather of the pipeline: out = concat over ranks of inp, issued on
+    `stream` (the driver yields these; a runner executes them)."""
+    out: torch.Tensor
+    inp: torch.Tensor
+    stream: torch.cuda.Stream
+
+
+class ProcessGroupCollective:
+    """All-gathers over torch.distributed (NCCL on GPUs)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+
+    def run(self, req: GatherRequest) -> None:
+        with torch.cuda.stream(req.stream):
+            _all_gather_flat(req.out, req.inp, self.group)
+
+
+class LocalCollective:
+    """world == 1: the gather is a copy (the single-GPU sharded path)."""
+
+    world = 1
+
+    def run(self, req: GatherRequest) -> None:
+        with torch.cuda.stream(req.stream):
+            req.out.copy_(req.inp)
+
+
+def run_loopback(generators) -> None:
+    """Drive G logical ranks' pipelines on one GPU in lockstep: every yielded
+    gather is answered with the rank-order concatenation of all ranks' inputs
+    (what NCCL's all_gather returns), each rank's stream waiting for all."""
+    while True:
+        reqs = [next(g, None) for g in generators]
+        if all(r is None for r in reqs):
+            return
+        if any(r is None for r in reqs):
+            raise RuntimeError("logical ranks out of step")
+        evs = []
+        for r in reqs:
+            e = torch.cuda.Event()
+            e.record(r.stream)
+            evs.append(e)
+        for r in reqs:
+            for e in evs:
+                r.stream.wait_event(e)
+            with torch.cuda.stream(r.stream):
+                r.out.copy_(torch.cat([q.inp for q in reqs]))
+
+
+class PipelinedShardTrainer(ShardedTrainer):
+    """ShardedTrainer whose steps overlap the exchange with the next step's
+    kernel (see the note above).  `exchange_pairs` is the global step: the
+    pairs trained between two exchanges (the config's B by default)."""
+
+    def __init__(self, model: DeviceModel, world: int, rank: int, collective=None):
+        super().__init__(model, world, rank)
+        self._coll = collective
+        dev = model.device
+        self.comm = torch.cuda.Stream(dev)
+        rows, K = model.T.shape
+        self.acc = torch.zeros(rows * K, dtype=torch.int64, device=dev)
+        self.flags = torch.zeros(rows, dtype=torch.int32, device=dev)
+        self._slots = None
+        self.stats: list[StepStats] = []
+
+    @property
+    def coll(self):
+        """The collective the runner uses (created on first use, so logical
+        ranks driven by run_loopback need no process group)."""
+        if self._coll is None:
+            self._coll = LocalCollective() if self.world == 1 else ProcessGroupCollective()
+        return self._coll
+
+    def _buffers(self, cap: int):  # logs live in the two pipeline slots
+        return None
+
+    def _alloc_slots(self, cap: int) -> None:
+        K, dev, W = self.model.dim, self.model.device, self.world
+        if self._slots is not None and self._slots[0]["ids"].numel() >= cap:
+            return
+        self._slots = [{
+            "ids": torch.empty(cap, dtype=torch.int32, device=dev),
+            "rows": torch.empty((cap, K), dtype=torch.float32, device=dev),
+            "cnt": torch.zeros(1, dtype=torch.int64, device=dev),
+            "counts": torch.zeros(W, dtype=torch.int64, device=dev),
+            "host_counts": torch.zeros(W, dtype=torch.int64).pin_memory(),
+            "g_ids": torch.empty(W * cap, dtype=torch.int32, device=dev),
+            "g_rows": torch.empty((W * cap, K), dtype=torch.float32, device=dev),
+            "log_ready": torch.cuda.Event(), "cnt_ready": torch.cuda.Event(),
+            "ex_done": torch.cuda.Event(),
+        } for _ in range(2)]
+
+    def epoch_pipeline(self, ep_users: np.ndarray, ep_items: np.ndarray,
+                       params: N.SgdParams, exchange_pairs: int, prepared: bool = False):
+        """Generator of the epoch's GatherRequests (a runner executes them).
+        `prepared`: prepare_epoch already ran with these arguments."""
+        if not prepared:
+            self.prepare_epoch(ep_users, ep_items, params, exchange_pairs)
+        self._alloc_slots(self.cap)
+        compute = torch.cuda.current_stream(self.model.device)
+        self.stats = []
+        n = self.num_steps
+        for s in range(n + 1):
+            if s < n:
+                yield from self._launch(s, compute)
+            if s >= 1:
+                yield from self._exchange(s - 1)
+        if n:
+            compute.wait_event(self._slots[(n - 1) & 1]["ex_done"])
+            if n >= 2:
+                compute.wait_event(self._slots[(n - 2) & 1]["ex_done"])
+
+    def _launch(self, s: int, compute):
+        sl = self._slots[s & 1]
+        if s >= 2:
+            compute.wait_event(sl["ex_done"])  # slot free, union(s-2) applied
+        sl["cnt"].zero_()
+        a, b = int(self.bounds[s]), int(self.bounds[s + 1])
+        if b > a:
+            self.model.train_range(self.lu, self.li, a, b, self.params,
+                                   delta=(sl["ids"], sl["rows"], sl["cnt"], self.cap),
+                                   pair_index=self.lp)
+        sl["log_ready"].record(compute)
+        self.comm.wait_event(sl["log_ready"])
+        yield GatherRequest(sl["counts"], sl["cnt"], self.comm)
+        with torch.cuda.stream(self.comm):
+            sl["host_counts"].copy_(sl["counts"], non_blocking=True)
+        sl["cnt_ready"].record(self.comm)
+
+    def _exchange(self, t: int):
+        sl = self._slots[t & 1]
+        sl["cnt_ready"].synchronize()  # kernel(t+1) is already queued: the GPU stays busy
+        hc = sl["host_counts"].numpy()
+        cmax = int(hc.max())
+        if cmax > self.cap:
+            raise RuntimeError(f"delta log overflow ({cmax} > {self.cap} entries on some rank); "
+                               "raise the capacity margin")
+        W = self.world
+        if cmax > 0:
+            yield GatherRequest(sl["g_ids"][:W * cmax], sl["ids"][:cmax], self.comm)
+            yield GatherRequest(sl["g_rows"][:W * cmax], sl["rows"][:cmax], self.comm)
+            T = self.model.T
+            rc = N.lib().heat_apply_row_deltas_fixed(
+                _p(T), T.shape[0], self.model.dim, _p(sl["g_ids"]), _p(sl["g_rows"]),
+                _p(sl["counts"]), W, cmax, _p(self.acc), _p(self.flags),
+                ctypes.c_void_p(self.comm.cuda_stream))
+            N.check(rc)
+        sl["ex_done"].record(self.comm)
+        n_valid = int(hc.sum())
+        self.stats.append(StepStats(n_valid, n_valid * (4 * self.model.dim + 4)))
+
+    def train_epoch(self, ep_users: np.ndarray, ep_items: np.ndarray, params: N.SgdParams,
+                    step_pairs: int, prepared: bool = False) -> list[StepStats]:
+        for req in self.epoch_pipeline(ep_users, ep_items, params, step_pairs, prepared):
+            self.coll.run(req)
+        return self.stats
+
+
+class NativeShardTrainer(ShardedTrainer):
+    """The production multi-GPU driver: the same pipelined steps as
+    PipelinedShardTrainer, scheduled by the native runtime (csrc/heat_shard.cu)
+    with its own NCCL communicator (unique id broadcast over the default
+    torch.distributed group), so no Python runs between steps."""
+
+    def __init__(self, model: DeviceModel, world: int, rank: int, group=None):
+        super().__init__(model, world, rank, group)
+        uid = None
+        if world > 1:
+            buf = (ctypes.c_ubyte * 128)()
+            if rank == 0:
+                N.check(N.lib().heat_nccl_unique_id(buf))
+            obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = (ctypes.c_ubyte * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        N.check(N.lib().heat_shard_create(world, rank, uid, model.device.index or 0,
+                                          ctypes.byref(h)))
+        self._h = h
+        self.stats = N.ShardStats()
+
+    def _buffers(self, cap: int):  # logs live in the native runtime
+        return None
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.lib().heat_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def train_epoch(self, ep_users: np.ndarray, ep_items: np.ndarray, params: N.SgdParams,
+                    step_pairs: int, prepared: bool = False) -> N.ShardStats:
+        if not prepared:
+            self.prepare_epoch(ep_users, ep_items, params, step_pairs)
+        bounds = np.ascontiguousarray(self.bounds, dtype=np.int64)
+        m = self.model
+        rc = N.lib().heat_shard_epoch(
+            self._h, _p(m.S), m.S.shape[0], _p(m.T), m.T.shape[0], _p(self.lu), _p(self.li),
+            _p(self.lp), bounds.ctypes.data_as(ctypes.c_void_p), len(bounds) - 1, self.cap,
+            ctypes.byref(self.params), m.counters.ptr(), ctypes.byref(self.stats),
+            _stream(m.device))
+        if rc != N.HEAT_OK:
+            msg = N.lib().heat_shard_last_error(self._h).decode(errors="replace")
+            raise (ValueError if rc in (N.HEAT_ERR_INVALID, N.HEAT_ERR_UNSUPPORTED)
+                   else N.HeatError)(msg)
+        return self.stats

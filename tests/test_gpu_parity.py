@@ -676,3 +676,140 @@ def test_agg_hogwild_quality_matches_oracle(torch_cuda):
     rec_ref, _, _ = O.evaluate_ref(q, To, train.offsets, train.items, 800, test.offsets,
                                    test.items, 800, k=20)
     assert abs(m_gpu.recall_at_k - rec_ref) <= 0.01, (m_gpu.recall_at_k, rec_ref)
+
+
+def test_fixed_point_apply_is_order_independent(torch_cuda):
+    """heat_apply_row_deltas_fixed: the same gathered logs in any entry order
+    give bit-identical rows (integer accumulation), equal to the exact sum
+    within fp32 rounding; padding past each rank's count is ignored."""
+    import ctypes
+    import torch
+    from paper_2304_07334_b200 import _native as N
+    rng = np.random.default_rng(5)
+    rows_t, K, world, stride = 50, 64, 3, 400
+    counts = np.array([400, 123, 0], dtype=np.int64)
+    ids = rng.integers(0, rows_t, world * stride).astype(np.int32)
+    vals = (rng.standard_normal((world * stride, K)) * 1e-3).astype(np.float32)
+    T0 = rng.standard_normal((rows_t, K)).astype(np.float32)
+    valid = (np.arange(world * stride) % stride) < np.repeat(counts, stride)
+
+    def apply(perm_within_rank):
+        ii, vv = ids.copy(), vals.copy()
+        for r in range(world):
+            sl = slice(r * stride, r * stride + counts[r])
+            p = perm_within_rank[r]
+            ii[sl], vv[sl] = ii[sl][p], vv[sl][p]
+        T = torch.from_numpy(T0.copy()).cuda()
+        acc = torch.zeros(rows_t * K, dtype=torch.int64, device="cuda")
+        flags = torch.zeros(rows_t, dtype=torch.int32, device="cuda")
+        dc = torch.from_numpy(counts).cuda()
+        di, dv = torch.from_numpy(ii).cuda(), torch.from_numpy(vv).cuda()
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        N.check(N.lib().heat_apply_row_deltas_fixed(P(T), rows_t, K, P(di), P(dv), P(dc), world,
+                                                    stride, P(acc), P(flags), None))
+        torch.cuda.synchronize()
+        assert int(acc.abs().sum()) == 0 and int(flags.sum()) == 0  # left zero
+        return T.cpu().numpy()
+
+    a = apply([np.arange(c) for c in counts])
+    b = apply([rng.permutation(c) for c in counts])
+    assert a.tobytes() == b.tobytes()
+    want = T0.astype(np.float64)
+    np.add.at(want, ids[valid], vals[valid].astype(np.float64))
+    assert np.abs(a - want).max() <= 1e-6
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_pipelined_shards_keep_replicas_identical(torch_cuda, G):
+    """The pipelined multi-GPU step (exchange of step s overlapped with the
+    kernel of step s+1, order-independent apply) driven for G logical ranks
+    on one GPU: item replicas bit-identical, every pair trained once, loss
+    within 3 % of the 1-GPU Hogwild run at the same staleness bound (two
+    1024-pair steps of item updates in flight -> window 2048)."""
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.parallel import PipelinedShardTrainer, run_loopback
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    train, _, _ = make_dataset("c2", scale=0.05)
+    S = init_matrix(train.num_users, 64, InitSpec(seed=0)).values
+    T = init_matrix(train.num_items, 64, InitSpec(seed=0)).values
+    ranks = [PipelinedShardTrainer(DeviceModel(S, T), G, r) for r in range(G)]
+    losses = []
+    for e in range(2):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        gens = []
+        for tr in ranks:
+            p = tr.model.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                                mode=N.MODE_DELTA, stream_base=epoch_stream(0, e), window=256)
+            tr.model.counters.reset()
+            gens.append(tr.epoch_pipeline(u, i, p, 1024))
+        if G == 1:
+            for req in gens[0]:
+                ranks[0].coll.run(req)
+        else:
+            run_loopback(gens)
+        cs = [tr.model.counters.read() for tr in ranks]
+        assert sum(c.pairs for c in cs) == len(u)
+        assert sum(st.entries for st in ranks[0].stats) >= len(u)  # >= one row per pair
+        losses.append(sum(c.loss for c in cs) / len(u))
+        T0 = ranks[0].model.T.cpu().numpy()
+        for tr in ranks[1:]:
+            assert tr.model.T.cpu().numpy().tobytes() == T0.tobytes()
+    assert losses[1] < losses[0]
+    m = DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,
+                    init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
+    ref = []
+    for e in range(2):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        du, di = m.upload_pairs(u, i)
+        p = m.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                     mode=N.MODE_HOGWILD, stream_base=epoch_stream(0, e), window=2048)
+        m.counters.reset()
+        m.train_range(du, di, 0, len(u), p)
+        ref.append(m.counters.read().loss / len(u))
+    assert abs(losses[1] - ref[1]) <= 0.03 * abs(ref[1]), (losses, ref)
+
+
+def test_native_shard_runtime_world1(torch_cuda):
+    """csrc/heat_shard.cu (the production scheduler) at world 1: every pair
+    trained once per epoch, one exchange per step, training tracks the 1-GPU
+    Hogwild run at the same staleness bound (loss within 3 %)."""
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.parallel import NativeShardTrainer
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    train, _, _ = make_dataset("c2", scale=0.05)
+    mk = lambda: DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,  # noqa: E731
+                             init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
+    tr = NativeShardTrainer(mk(), 1, 0)
+    m = mk()
+    losses, ref = [], []
+    for e in range(2):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        p = tr.model.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                            mode=N.MODE_DELTA, stream_base=epoch_stream(0, e), window=256)
+        tr.model.counters.reset()
+        st = tr.train_epoch(u, i, p, 1024)
+        c = tr.model.counters.read()
+        assert c.pairs == len(u) and st.steps == tr.num_steps
+        assert st.entries >= len(u)
+        losses.append(c.loss / len(u))
+        du, di = m.upload_pairs(u, i)
+        p = m.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                     mode=N.MODE_HOGWILD, stream_base=epoch_stream(0, e), window=2048)
+        m.counters.reset()
+        m.train_range(du, di, 0, len(u), p)
+        ref.append(m.counters.read().loss / len(u))
+    assert np.isfinite(tr.model.T.cpu().numpy()).all()
+    assert abs(losses[1] - ref[1]) <= 0.03 * abs(ref[1]), (losses, ref)
+    with pytest.raises(ValueError):  # EXACT/HOGWILD params are rejected: DELTA steps only
+        p.mode = N.MODE_HOGWILD
+        tr.params = p
+        tr.train_epoch(u, i, p, 1024, prepared=True)
+    tr.close()
