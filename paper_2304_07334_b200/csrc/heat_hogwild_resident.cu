@@ -157,20 +157,23 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
         const double ss = (double)sp;
         const float rss = sp > 0.f ? rsqrtf(sp) : 0.f;
         const float *row = my_stage + lane * G::SLOTF;
-        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        // packed fp32x2 FMA (FFMA2, sm_100): half the FMA instructions of the
+        // scalar loop, four independent accumulator pairs
+        float2 ta = make_float2(0.f, 0.f), tb = ta, sa = ta, sb = ta;
         if (valid) {
 #pragma unroll
             for (int c = 0; c < G::CH; ++c) {
                 const float4 v = *reinterpret_cast<const float4 *>(row + c * 4);
                 const float4 w4 = *reinterpret_cast<const float4 *>(urow + c * 4);
-                t0 = fmaf(v.x, v.x, t0); t1 = fmaf(v.y, v.y, t1);
-                t2 = fmaf(v.z, v.z, t2); t3 = fmaf(v.w, v.w, t3);
-                s0 = fmaf(w4.x, v.x, s0); s1 = fmaf(w4.y, v.y, s1);
-                s2 = fmaf(w4.z, v.z, s2); s3 = fmaf(w4.w, v.w, s3);
+                const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
+                ta = __ffma2_rn(vlo, vlo, ta);
+                tb = __ffma2_rn(vhi, vhi, tb);
+                sa = __ffma2_rn(make_float2(w4.x, w4.y), vlo, sa);
+                sb = __ffma2_rn(make_float2(w4.z, w4.w), vhi, sb);
             }
         }
-        const float ttf = (t0 + t1) + (t2 + t3);
-        const float stf = (s0 + s1) + (s2 + s3);
+        const float ttf = (ta.x + ta.y) + (tb.x + tb.y);
+        const float stf = (sa.x + sa.y) + (sb.x + sb.y);
         bool write = false;
         double wt = 0.0, hinge = 0.0, sim = 0.0;
         if (valid) {

@@ -332,19 +332,20 @@ __global__ void __launch_bounds__(32)
                     tt = t0 + t1;
                     st = s0 + s1;
                 } else {
-                    float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
-                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                    // packed fp32x2 FMA (FFMA2, sm_100)
+                    float2 ta = make_float2(0.f, 0.f), tb = ta, sa = ta, sb = ta;
 #pragma unroll
                     for (int k = 0; k < K; k += 4) {
                         const float4 v = *reinterpret_cast<const float4 *>(row + k);
                         const float4 w4 = *reinterpret_cast<const float4 *>(up + k);
-                        t0 = fmaf(v.x, v.x, t0); t1 = fmaf(v.y, v.y, t1);
-                        t2 = fmaf(v.z, v.z, t2); t3 = fmaf(v.w, v.w, t3);
-                        s0 = fmaf(w4.x, v.x, s0); s1 = fmaf(w4.y, v.y, s1);
-                        s2 = fmaf(w4.z, v.z, s2); s3 = fmaf(w4.w, v.w, s3);
+                        const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
+                        ta = __ffma2_rn(vlo, vlo, ta);
+                        tb = __ffma2_rn(vhi, vhi, tb);
+                        sa = __ffma2_rn(make_float2(w4.x, w4.y), vlo, sa);
+                        sb = __ffma2_rn(make_float2(w4.z, w4.w), vhi, sb);
                     }
-                    tt = (double)((t0 + t1) + (t2 + t3));
-                    st = (double)((s0 + s1) + (s2 + s3));
+                    tt = (double)((ta.x + ta.y) + (tb.x + tb.y));
+                    st = (double)((sa.x + sa.y) + (sb.x + sb.y));
                 }
             }
             // similarity and loss weight (trainer.py:184-221).  fp32 screen; the

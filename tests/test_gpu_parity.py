@@ -813,3 +813,45 @@ def test_native_shard_runtime_world1(torch_cuda):
         tr.params = p
         tr.train_epoch(u, i, p, 1024, prepared=True)
     tr.close()
+
+
+def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
+    """train() (trainer.py:480-533): tables stay on the device across epochs,
+    yet the run equals the reference's epoch-by-epoch result bit for bit;
+    evaluations at every interval plus the final one; best/final checkpoints
+    in the HEATEMB1 bundle format hold the reported tables."""
+    import dataclasses
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
+    from paper_2304_07334_b200.dataset import from_user_lists
+    from paper_2304_07334_b200.embeddings import load_model
+    from paper_2304_07334_b200.synth import make_dataset
+    from paper_2304_07334_b200.trainer import train
+    z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
+    tr, _, _ = make_dataset("c1")
+    rng = np.random.default_rng(3)
+    te = from_user_lists({u: rng.integers(0, 2000, 3) for u in range(0, 1000, 3)},
+                         num_users=1000, num_items=2000)
+    cfg = TrainingConfig(emb_dim=32, num_negatives=10, learning_rate=1e-3, num_threads=1,
+                         loss=LossParams(mu=10.0, theta=0.5), seed=0)
+    cfg = dataclasses.replace(cfg, epochs=2)
+    S = init_matrix(1000, 32, InitSpec(seed=0))
+    T = init_matrix(2000, 32, InitSpec(seed=0))
+    seen = []
+    res = train(S, T, tr, te, cfg, eval_interval=1, k=20, out_dir=str(tmp_path),
+                on_epoch=lambda r: seen.append(r.epoch))
+    assert seen == [0, 1]
+    assert [r.mean_loss for r in res.reports] == list(z["mean_loss"][:2])
+    assert S.values.tobytes() == z["S_e1"].tobytes()
+    assert T.values.tobytes() == z["T_e1"].tobytes()
+    assert [e for e, _ in res.evaluations] == [1, 2, 2]
+    rec, nd, n = O.evaluate_ref(S.values, T.values, tr.offsets, tr.items, 1000, te.offsets,
+                                te.items, 1000, k=20)
+    assert res.final_metrics.recall_at_k == pytest.approx(rec, abs=1e-12)
+    assert res.final_metrics.ndcg_at_k == pytest.approx(nd, abs=1e-12)
+    assert res.best_recall == max(m.recall_at_k for _, m in res.evaluations)
+    Sf, Tf, Wf = load_model(str(tmp_path / "final.ckpt"))
+    assert Sf.values.tobytes() == S.values.tobytes() and Wf is None
+    assert Tf.values.tobytes() == T.values.tobytes()
+    Sb, Tb, _ = load_model(str(tmp_path / "best.ckpt"))
+    assert Sb.values.shape == S.values.shape and Tb.values.shape == T.values.shape
