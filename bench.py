@@ -352,6 +352,10 @@ def main():
         cpu_baseline(spec, train, S.values, T.values, 20000, threads)  # warm
         cpu = cpu_baseline(spec, train, S.values, T.values, sample, threads)
         cpu.pop("seconds", None)
+        # the single-thread figure beside it: a smaller sample
+        one = cpu_baseline(spec, train, S.values, T.values, max(2000, sample // 16), 1)
+        cpu["value_1_thread"] = one["value"]
+        cpu["sample_1_thread"] = one["sample"]
 
     if rank == 0:
         prof = _ncu_traffic(spec.name)

@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "heat_common.cuh"
@@ -39,13 +40,24 @@
 
 namespace heat {
 
-template <int K>
+// LPR lanes score one row (LPR = 2: each lane takes half of the columns and
+// a stage holds 16 rows).  The ring is shared memory's binding resource: at the
+// same rows in flight per SM, LPR = 2 halves the rows per warp and doubles the
+// warps that hide the LDS/FMA latency.  A slot stores each lane's segment of
+// HALF columns followed by 16 bytes of padding, so the lanes of a quarter-warp
+// read distinct bank groups.
+template <int K, int LPR = 1>
 struct StGeom {
     static constexpr int ROWB = K * 4;               // bytes per row
-    static constexpr int SLOTF = K + 4;              // floats per padded slot
+    static constexpr int HALF = K / LPR;             // columns per lane segment
+    static constexpr int SEGF = HALF + 4;            // floats per padded segment
+    static constexpr int SLOTF = LPR * SEGF;         // floats per padded slot
     static constexpr int CH = K / 4;                 // 16-byte chunks per row
+    static constexpr int SR = 32 / LPR;              // rows per stage
     static constexpr int VW = K >= 32 ? K / 32 : 1;  // floats per lane in row-wide ops
     static constexpr int ACT = K >= 32 ? 32 : K;     // lanes active in row-wide ops
+    // slot offset of column c
+    __host__ __device__ static constexpr int pcol(int c) { return c + (c / HALF) * 4; }
 };
 
 struct StLayout {
@@ -53,9 +65,9 @@ struct StLayout {
     size_t off_bars, off_ubars, off_ids, off_ring, off_urow, off_snap, off_ents, total;
 };
 
-template <int K, int D>
+template <int K, int D, int LPR = 1>
 __host__ __device__ inline StLayout st_layout(int snap_cap) {
-    using G = StGeom<K>;
+    using G = StGeom<K, LPR>;
     StLayout L;
     L.ucap = D + 1;
     L.snap_cap = snap_cap;
@@ -67,9 +79,9 @@ __host__ __device__ inline StLayout st_layout(int snap_cap) {
     };
     L.off_bars = take(sizeof(uint64_t) * D);
     L.off_ubars = take(sizeof(uint64_t) * L.ucap);
-    L.off_ids = take(sizeof(int32_t) * 32 * D);
-    L.off_ring = take(sizeof(float) * G::SLOTF * 32 * D);
-    L.off_urow = take(sizeof(float) * K * L.ucap);
+    L.off_ids = take(sizeof(int32_t) * G::SR * D);
+    L.off_ring = take(sizeof(float) * G::SLOTF * G::SR * D);
+    L.off_urow = take(sizeof(float) * G::SLOTF * L.ucap);
     L.off_snap = take(sizeof(float) * K * snap_cap);
     L.off_ents = take(sizeof(WriteEntry) * snap_cap);
     L.total = (o + 127) & ~size_t(127);
@@ -88,13 +100,14 @@ __device__ __forceinline__ void red_add_vec(float *p, const float (&d)[VW]) {
     }
 }
 
-template <int K, int D, bool F64, bool BULK>
+template <int K, int D, bool F64, bool BULK, int LPR>
 __global__ void __launch_bounds__(32)
     hogwild_staged(HogwildArgs a, FastMod fm, int n_workers, int snap_cap, int cross) {
-    using G = StGeom<K>;
+    using G = StGeom<K, LPR>;
     constexpr int VW = G::VW;
+    constexpr int SR = G::SR;
     extern __shared__ __align__(128) unsigned char sm[];
-    const StLayout Lo = st_layout<K, D>(snap_cap);
+    const StLayout Lo = st_layout<K, D, LPR>(snap_cap);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Lo.off_bars);
     uint64_t *ubars = reinterpret_cast<uint64_t *>(sm + Lo.off_ubars);
     int32_t *ids = reinterpret_cast<int32_t *>(sm + Lo.off_ids);
@@ -104,17 +117,26 @@ __global__ void __launch_bounds__(32)
     WriteEntry *ents = reinterpret_cast<WriteEntry *>(sm + Lo.off_ents);
 
     const int lane = threadIdx.x;
+    const int rr = lane / LPR;       // this lane's row within a stage
+    const int hs = lane % LPR;       // and its column segment
+    const bool lead = hs == 0;       // the lane that accounts for the row
     const int gw = blockIdx.x;
     const int64_t npairs = a.stop - a.start;
     if (gw >= n_workers || gw >= npairs) return;
     const int64_t my_pairs = (npairs - gw + n_workers - 1) / n_workers;
     const int N = a.N;
-    const int nb = (N + 1 + 31) / 32;  // stages per pair
+    const int nb = (N + 1 + SR - 1) / SR;  // stages per pair
     const int64_t g_total = my_pairs * nb;
     const double wneg = a.mu * (1.0 / (double)N);
     const float theta_f = (float)a.theta;
     const bool dmode = a.delta_ids != nullptr;
     const uint64_t pol = policy_evict_last();
+    float *sp_rows = a.spill ? reinterpret_cast<float *>(a.spill + (size_t)gw * a.spill_stride)
+                             : nullptr;
+    WriteEntry *sp_ents =
+        a.spill ? reinterpret_cast<WriteEntry *>(a.spill + (size_t)gw * a.spill_stride +
+                                                 (size_t)a.spill_cap * K * sizeof(float))
+                : nullptr;
 
     if constexpr (BULK) {
         if (lane == 0) {
@@ -143,10 +165,10 @@ __global__ void __launch_bounds__(32)
     auto rng_key = [&](int64_t pp) -> uint64_t {
         return (uint64_t)(a.pair_index ? a.pair_index[pp] : pp);
     };
-    uint64_t rng_state = a.s0 + (rng_key(a.start + gw) * (uint64_t)N + (uint64_t)lane) * kGamma;
+    uint64_t rng_state = a.s0 + (rng_key(a.start + gw) * (uint64_t)N + (uint64_t)rr) * kGamma;
     // this lane's fixed 16-byte chunk and row-within-instruction
     constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;  // rows per copy instruction
-    constexpr int NI = 32 / RPI;                          // copy instructions per stage
+    constexpr int NI = SR / RPI > 0 ? SR / RPI : 1;       // copy instructions per stage
     const int my_ch = lane % G::CH;
     const int my_rsub = lane / G::CH;
 
@@ -162,48 +184,51 @@ __global__ void __launch_bounds__(32)
             if constexpr (!BULK) cp_async_commit();
             return;
         }
-        const int r = ps * 32 + lane;
+        const int r = ps * SR + rr;
         const bool valid = r <= N;
         uint32_t id = (uint32_t)pf_pos;
         if (r > 0) id = (uint32_t)fm.mod(mix64(rng_state));
         if (!valid) id = 0;
-        ids[pslot * 32 + lane] = (int32_t)id;
-        const int nvalid = min(32, N + 1 - ps * 32);
-        float *dst0 = ring + (size_t)pslot * 32 * G::SLOTF;
+        if (lead) ids[pslot * SR + rr] = (int32_t)id;
+        const int nvalid = min(SR, N + 1 - ps * SR);
+        float *dst0 = ring + (size_t)pslot * SR * G::SLOTF;
         if constexpr (BULK) {
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
                 if (ps == 0) {
                     mbar_arrive_expect_tx(&ubars[pus], G::ROWB);
-                    bulk_g2s(urow + pus * K, qrow(pf_p, pf_u), G::ROWB, &ubars[pus]);
+                    for (int h = 0; h < LPR; ++h)
+                        bulk_g2s(urow + pus * G::SLOTF + h * G::SEGF, qrow(pf_p, pf_u) + h * G::HALF,
+                                 G::ROWB / LPR, &ubars[pus]);
                 }
                 mbar_arrive_expect_tx(&bars[pslot], (uint32_t)(nvalid * G::ROWB));
             }
             __syncwarp();
             if (valid)
-                bulk_g2s_hint(dst0 + lane * G::SLOTF, a.T + (int64_t)id * K, G::ROWB, &bars[pslot],
+                bulk_g2s_hint(dst0 + rr * G::SLOTF + hs * G::SEGF,
+                              a.T + (int64_t)id * K + hs * G::HALF, G::ROWB / LPR, &bars[pslot],
                               pol);
         } else {
             __syncwarp();
-            float *dst = dst0 + my_rsub * G::SLOTF + my_ch * 4;
+            float *dst = dst0 + my_rsub * G::SLOTF + G::pcol(my_ch * 4);
             const float *srcb = a.T + my_ch * 4;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 const int row = i * RPI + my_rsub;
-                const uint32_t rid = __shfl_sync(0xffffffffu, id, row & 31);
+                const uint32_t rid = __shfl_sync(0xffffffffu, id, (row * LPR) & 31);
                 if (row < nvalid)
                     cp_async16_hint(dst + i * RPI * G::SLOTF, srcb + (size_t)rid * K, pol);
             }
             if (ps == 0) {
                 const float *q = qrow(pf_p, pf_u);
                 for (int ch = lane; ch < G::CH; ch += 32)
-                    cp_async16(urow + pus * K + ch * 4, q + ch * 4);
+                    cp_async16(urow + pus * G::SLOTF + G::pcol(ch * 4), q + ch * 4);
             }
             cp_async_commit();
         }
         ++g_next;
-        rng_state += 32ull * kGamma;
+        rng_state += (uint64_t)SR * kGamma;
         if (++pslot == D) pslot = 0;
         if (++ps == nb) {  // next pair of this worker
             ps = 0;
@@ -214,7 +239,7 @@ __global__ void __launch_bounds__(32)
             const int64_t pn = a.start + gw + pt * n_workers;
             pf_p = pn;
             if (pt < my_pairs)
-                rng_state = a.s0 + (rng_key(pn) * (uint64_t)N + (uint64_t)lane) * kGamma;
+                rng_state = a.s0 + (rng_key(pn) * (uint64_t)N + (uint64_t)rr) * kGamma;
             if (pt + 1 < my_pairs) {
                 nx_u = a.users[pn + n_workers];
                 nx_pos = a.items[pn + n_workers];
@@ -238,7 +263,7 @@ __global__ void __launch_bounds__(32)
             for (int i = 0; i < D; ++i) issue(limit);
         const int us = cus;
         if (++cus == Lo.ucap) cus = 0;
-        const float *up = urow + us * K;
+        const float *up = urow + us * G::SLOTF;
         float ug[VW];
 #pragma unroll
         for (int i = 0; i < VW; ++i) ug[i] = 0.f;
@@ -248,17 +273,23 @@ __global__ void __launch_bounds__(32)
         double hinge = 0.0, sim_p = 0.0;
         int cnt = 0;
 
-        auto flush = [&]() {
-            __syncwarp();
-            for (int e = 0; e < cnt; ++e) {
-                const WriteEntry ent = ents[e];
+        int nsp = 0;  // rows of this pair parked in the global spill area
+        // apply n written rows (values in rows_, scalars in ents_)
+        auto apply = [&](const float *rows_, const WriteEntry *ents_, int n) {
+            for (int e = 0; e < n; ++e) {
+                const WriteEntry ent = ents_[e];
                 const RowCoef co = row_coef(ent, ss, rs, a.lr, a.l2, a.cosine);
-                float d[VW];
+                float d[VW], vv[VW];
+                if constexpr (VW == 4) {
+                    const float4 v4 = *reinterpret_cast<const float4 *>(rows_ + e * K + lane * 4);
+                    vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+                } else {
 #pragma unroll
-                for (int i = 0; i < VW; ++i) {
-                    const float v = lane < G::ACT ? snap[e * K + lane * VW + i] : 0.f;
-                    row_apply(co, uu[i], v, d[i], ug[i]);
+                    for (int i = 0; i < VW; ++i)
+                        vv[i] = lane < G::ACT ? rows_[e * K + lane * VW + i] : 0.f;
                 }
+#pragma unroll
+                for (int i = 0; i < VW; ++i) row_apply(co, uu[i], vv[i], d[i], ug[i]);
                 if (!dmode) {
                     if (lane < G::ACT) red_add_vec<VW>(a.T + (int64_t)ent.id * K + lane * VW, d);
                 } else {
@@ -274,6 +305,30 @@ __global__ void __launch_bounds__(32)
                         }
                     }
                 }
+            }
+        };
+        // end of the pair: every row has been read, so all writes go now
+        auto flush = [&]() {
+            __syncwarp();
+            if (nsp) apply(sp_rows, sp_ents, nsp);
+            apply(snap, ents, cnt);
+            cnt = 0;
+            nsp = 0;
+            __syncwarp();
+        };
+        // the snapshot is full mid-pair: park it in global memory (writes must
+        // wait until the pair's last row is read, trainer.py:118-146 — a later
+        // stage can hold the same row again); without a spill area, apply
+        auto spill = [&]() {
+            __syncwarp();
+            if (sp_rows && nsp + cnt <= a.spill_cap) {
+                const float4 *src4 = reinterpret_cast<const float4 *>(snap);
+                float4 *dst4 = reinterpret_cast<float4 *>(sp_rows + (size_t)nsp * K);
+                for (int x = lane; x < cnt * (K / 4); x += 32) dst4[x] = src4[x];
+                for (int e = lane; e < cnt; e += 32) sp_ents[nsp + e] = ents[e];
+                nsp += cnt;
+            } else {
+                apply(snap, ents, cnt);
             }
             cnt = 0;
             __syncwarp();
@@ -296,7 +351,7 @@ __global__ void __launch_bounds__(32)
                 double spd = 0.0;
 #pragma unroll
                 for (int i = 0; i < VW; ++i) {
-                    uu[i] = lane < G::ACT ? up[lane * VW + i] : 0.f;
+                    uu[i] = lane < G::ACT ? up[G::pcol(lane * VW + i)] : 0.f;
                     sp = fmaf(uu[i], uu[i], sp);
                     spd += (double)uu[i] * (double)uu[i];
                 }
@@ -309,17 +364,18 @@ __global__ void __launch_bounds__(32)
                 rs = ss > 0.0 ? sqrt(ss) : 0.0;
                 rss = ss > 0.0 ? rsqrtf((float)ss) : 0.f;
             }
-            const int r = s * 32 + lane;
+            const int r = s * SR + rr;
             const bool valid = r <= N;
-            const float *row = ring + ((size_t)slot * 32 + lane) * G::SLOTF;
+            const float *row = ring + ((size_t)slot * SR + rr) * G::SLOTF + hs * G::SEGF;
+            const float *uph = up + hs * G::SEGF;
             double tt = 0.0, st = 0.0;
             if (valid) {
                 if constexpr (F64) {
                     double t0 = 0, t1 = 0, s0 = 0, s1 = 0;
 #pragma unroll
-                    for (int k = 0; k < K; k += 4) {
+                    for (int k = 0; k < G::HALF; k += 4) {
                         const float4 v = *reinterpret_cast<const float4 *>(row + k);
-                        const float4 w4 = *reinterpret_cast<const float4 *>(up + k);
+                        const float4 w4 = *reinterpret_cast<const float4 *>(uph + k);
                         t0 = fma((double)v.x, (double)v.x, t0);
                         t1 = fma((double)v.y, (double)v.y, t1);
                         t0 = fma((double)v.z, (double)v.z, t0);
@@ -335,9 +391,9 @@ __global__ void __launch_bounds__(32)
                     // packed fp32x2 FMA (FFMA2, sm_100)
                     float2 ta = make_float2(0.f, 0.f), tb = ta, sa = ta, sb = ta;
 #pragma unroll
-                    for (int k = 0; k < K; k += 4) {
+                    for (int k = 0; k < G::HALF; k += 4) {
                         const float4 v = *reinterpret_cast<const float4 *>(row + k);
-                        const float4 w4 = *reinterpret_cast<const float4 *>(up + k);
+                        const float4 w4 = *reinterpret_cast<const float4 *>(uph + k);
                         const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
                         ta = __ffma2_rn(vlo, vlo, ta);
                         tb = __ffma2_rn(vhi, vhi, tb);
@@ -346,6 +402,18 @@ __global__ void __launch_bounds__(32)
                     }
                     tt = (double)((ta.x + ta.y) + (tb.x + tb.y));
                     st = (double)((sa.x + sa.y) + (sb.x + sb.y));
+                }
+            }
+            if constexpr (LPR == 2) {  // the row's two column segments
+                if constexpr (F64) {
+                    tt += __shfl_xor_sync(0xffffffffu, tt, 1);
+                    st += __shfl_xor_sync(0xffffffffu, st, 1);
+                } else {
+                    float tf = (float)tt, sf2 = (float)st;
+                    tf += __shfl_xor_sync(0xffffffffu, tf, 1);
+                    sf2 += __shfl_xor_sync(0xffffffffu, sf2, 1);
+                    tt = (double)tf;
+                    st = (double)sf2;
                 }
             }
             // similarity and loss weight (trainer.py:184-221).  fp32 screen; the
@@ -359,7 +427,7 @@ __global__ void __launch_bounds__(32)
                     if (ss <= 0.0 || tt <= 0.0) {
                         degenerate = true;
                         sim = 0.0;
-                        ++degen;
+                        if (lead) ++degen;
                     } else {
                         const float sf = (float)st * rss * rsqrtf((float)tt);
                         sim = (double)sf;
@@ -372,24 +440,25 @@ __global__ void __launch_bounds__(32)
                     write = !(a.cosine && degenerate) || a.l2 != 0.f;
                 } else {
                     if (sim - a.theta > 0.0) {
-                        hinge += sim - a.theta;
+                        if (lead) hinge += sim - a.theta;
                         w = wneg;
-                        if (w != 0.0) ++active;
+                        if (w != 0.0 && lead) ++active;
                     }
                     write = (w != 0.0 && !(a.cosine && degenerate)) || (w == 0.0 && a.l2 != 0.f);
                 }
             }
-            unsigned m = __ballot_sync(0xffffffffu, write);
+            unsigned m = __ballot_sync(0xffffffffu, write && lead);
             while (m) {
-                if (cnt == Lo.snap_cap) flush();
+                if (cnt == Lo.snap_cap) spill();
                 const int src = __ffs(m) - 1;
                 m &= m - 1;
-                const float *srow = ring + ((size_t)slot * 32 + src) * G::SLOTF;
+                const float *srow = ring + ((size_t)slot * SR + src / LPR) * G::SLOTF;
                 if (lane < G::ACT) {
 #pragma unroll
-                    for (int i = 0; i < VW; ++i) snap[cnt * K + lane * VW + i] = srow[lane * VW + i];
+                    for (int i = 0; i < VW; ++i)
+                        snap[cnt * K + lane * VW + i] = srow[G::pcol(lane * VW + i)];
                 }
-                if (lane == src) ents[cnt] = WriteEntry{tt, st, w, ids[slot * 32 + src], 0};
+                if (lane == src) ents[cnt] = WriteEntry{tt, st, w, ids[slot * SR + src / LPR], 0};
                 ++cnt;
             }
             __syncwarp();
@@ -440,40 +509,85 @@ __global__ void __launch_bounds__(32)
     }
 }
 
-template <int K, int D, bool F64, bool BULK>
+// Per-device spill area, grown on demand and kept (the launch is asynchronous,
+// so a buffer is only ever replaced after the device is idle).
+static void *spill_area(size_t bytes) {
+    static std::mutex mu;
+    static void *buf[64] = {nullptr};
+    static size_t size[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (size[dev] < bytes) {
+        cudaDeviceSynchronize();
+        if (buf[dev]) cudaFree(buf[dev]);
+        buf[dev] = nullptr;
+        size[dev] = 0;
+        if (cudaMalloc(&buf[dev], bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        size[dev] = bytes;
+    }
+    return buf[dev];
+}
+
+template <int K, int D, bool F64, bool BULK, int LPR>
 static cudaError_t launch_staged_k(const HogwildArgs &a, cudaStream_t st, int *workers_out,
                                    int cross) {
-    const int snap_cap = K <= 64 ? 16 : 8;
-    const StLayout L = st_layout<K, D>(snap_cap);
+    int snap_cap = K <= 64 ? 16 : 8;
+    if (const char *e = getenv("HEAT_SNAP")) snap_cap = atoi(e) > 0 ? atoi(e) : snap_cap;
+    const StLayout L = st_layout<K, D, LPR>(snap_cap);
     if (L.total > 200 * 1024) return cudaErrorInvalidValue;
-    auto kern = hogwild_staged<K, D, F64, BULK>;
+    auto kern = hogwild_staged<K, D, F64, BULK, LPR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)L.total);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, L.total);
     if (per_sm < 1) per_sm = 1;
-    const int nb = (a.N + 1 + 31) / 32;
+    const int nb = (a.N + 1 + StGeom<K, LPR>::SR - 1) / StGeom<K, LPR>::SR;
     const int pif = cross ? 1 + (D - 1 + nb - 1) / nb : 1;  // pairs in flight per worker
     int64_t nw = (int64_t)per_sm * sm_count();
     if (a.window > 0) nw = std::min<int64_t>(nw, std::max<int64_t>(1, a.window / pif));
     if (a.window > 0 && a.window < pif) cross = 0;  // a lone pair: never prefetch past it
     nw = std::min<int64_t>(nw, a.stop - a.start);
     if (workers_out) *workers_out = (int)nw;
-    kern<<<(unsigned)nw, 32, L.total, st>>>(a, FastMod::make((uint64_t)a.num_items), (int)nw,
+    HogwildArgs b = a;
+    // spill area: a pair writes at most N+1 rows (all of them when l2 != 0)
+    if (a.N + 1 > snap_cap) {
+        b.spill_cap = a.N + 1;
+        b.spill_stride = ((int64_t)b.spill_cap * (K * sizeof(float) + sizeof(WriteEntry)) + 255) &
+                         ~(int64_t)255;
+        b.spill = static_cast<unsigned char *>(spill_area((size_t)(b.spill_stride * nw)));
+        if (!b.spill) b.spill_cap = 0;  // no memory: mid-pair application (documented)
+    }
+    kern<<<(unsigned)nw, 32, L.total, st>>>(b, FastMod::make((uint64_t)a.num_items), (int)nw,
                                             snap_cap, cross);
     return cudaGetLastError();
 }
 
 template <int K, bool F64>
 static cudaError_t launch_staged_d(const HogwildArgs &a, cudaStream_t st, int *workers_out,
-                                   int D, int cross, bool bulk) {
-    if (bulk) return launch_staged_k<K, 2, F64, true>(a, st, workers_out, cross);
+                                   int D, int cross, bool bulk, int lpr) {
+    if constexpr (K >= 64) {
+        if (lpr == 2) {
+            if (bulk) return launch_staged_k<K, 2, F64, true, 2>(a, st, workers_out, cross);
+            switch (D) {
+            case 2: return launch_staged_k<K, 2, F64, false, 2>(a, st, workers_out, cross);
+            case 4: return launch_staged_k<K, 4, F64, false, 2>(a, st, workers_out, cross);
+            case 6: return launch_staged_k<K, 6, F64, false, 2>(a, st, workers_out, cross);
+            default: return launch_staged_k<K, 3, F64, false, 2>(a, st, workers_out, cross);
+            }
+        }
+    }
+    if (bulk) return launch_staged_k<K, 2, F64, true, 1>(a, st, workers_out, cross);
     switch (D) {
-    case 2: return launch_staged_k<K, 2, F64, false>(a, st, workers_out, cross);
-    case 4: return launch_staged_k<K, 4, F64, false>(a, st, workers_out, cross);
-    case 6: return launch_staged_k<K, 6, F64, false>(a, st, workers_out, cross);
-    default: return launch_staged_k<K, 3, F64, false>(a, st, workers_out, cross);
+    case 2: return launch_staged_k<K, 2, F64, false, 1>(a, st, workers_out, cross);
+    case 4: return launch_staged_k<K, 4, F64, false, 1>(a, st, workers_out, cross);
+    case 6: return launch_staged_k<K, 6, F64, false, 1>(a, st, workers_out, cross);
+    default: return launch_staged_k<K, 3, F64, false, 1>(a, st, workers_out, cross);
     }
 }
 
@@ -486,15 +600,20 @@ cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t st, int *wo
     // cross-pair prefetch halves the workers a window allows; measured slower
     int cross = 0;
     if (const char *e = getenv("HEAT_CROSS")) cross = atoi(e);
+    // lanes per row: 2 for K = 128 (more warps per SM at the same rows in
+    // flight; measured c4 +5 %); at K = 64 the doubled per-stage overhead
+    // outweighs it (c3 -30 %)
+    int lpr = a.K >= 128 ? 2 : 1;
+    if (const char *e = getenv("HEAT_LPR")) lpr = atoi(e) == 2 ? 2 : 1;
     switch (a.K) {
-    case 16: return a.fp64 ? launch_staged_d<16, true>(a, st, workers_out, D, cross, bulk)
-                           : launch_staged_d<16, false>(a, st, workers_out, D, cross, bulk);
-    case 32: return a.fp64 ? launch_staged_d<32, true>(a, st, workers_out, D, cross, bulk)
-                           : launch_staged_d<32, false>(a, st, workers_out, D, cross, bulk);
-    case 64: return a.fp64 ? launch_staged_d<64, true>(a, st, workers_out, D, cross, bulk)
-                           : launch_staged_d<64, false>(a, st, workers_out, D, cross, bulk);
-    case 128: return a.fp64 ? launch_staged_d<128, true>(a, st, workers_out, D, cross, bulk)
-                            : launch_staged_d<128, false>(a, st, workers_out, D, cross, bulk);
+    case 16: return a.fp64 ? launch_staged_d<16, true>(a, st, workers_out, D, cross, bulk, lpr)
+                           : launch_staged_d<16, false>(a, st, workers_out, D, cross, bulk, lpr);
+    case 32: return a.fp64 ? launch_staged_d<32, true>(a, st, workers_out, D, cross, bulk, lpr)
+                           : launch_staged_d<32, false>(a, st, workers_out, D, cross, bulk, lpr);
+    case 64: return a.fp64 ? launch_staged_d<64, true>(a, st, workers_out, D, cross, bulk, lpr)
+                           : launch_staged_d<64, false>(a, st, workers_out, D, cross, bulk, lpr);
+    case 128: return a.fp64 ? launch_staged_d<128, true>(a, st, workers_out, D, cross, bulk, lpr)
+                            : launch_staged_d<128, false>(a, st, workers_out, D, cross, bulk, lpr);
     default: return cudaErrorNotSupported;
     }
 }

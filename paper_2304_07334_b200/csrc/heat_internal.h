@@ -44,6 +44,11 @@ struct HogwildArgs {
     const float *query = nullptr;
     float *ugrad_out = nullptr;
     float ugamma = 1.f;
+    // staged kernel: per-worker overflow area for written rows beyond its
+    // shared-memory snapshot (set by the launcher)
+    unsigned char *spill = nullptr;
+    int64_t spill_stride = 0;  // bytes per worker
+    int spill_cap = 0;         // rows per worker
 };
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);

@@ -855,3 +855,45 @@ def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
     assert Tf.values.tobytes() == T.values.tobytes()
     Sb, Tb, _ = load_model(str(tmp_path / "best.ckpt"))
     assert Sb.values.shape == S.values.shape and Tb.values.shape == T.values.shape
+
+
+@pytest.mark.parametrize("K,N,lpr,fp64,stages", [(64, 100, 1, False, 2), (64, 100, 2, False, 3),
+                                                 (128, 300, 2, False, 2), (128, 300, 1, True, 4),
+                                                 (128, 64, 2, True, 2), (64, 500, 2, True, 4),
+                                                 (64, 60, 2, False, 4)])
+def test_staged_kernel_variants_window1_vs_oracle(torch_cuda, monkeypatch, K, N, lpr, fp64,
+                                                  stages):
+    """The staged throughput kernel in each row layout (one or two lanes per
+    row), fp32 and fp64 dots, several ring depths: sequential run vs the
+    oracle within 1e-4 norm-relative.  (Large-N cases use fp64 dots: with
+    fp32 dots a margin decision |sim - theta| < ~1e-6 can flip, which is the
+    fp32 mode's expected deviation, not a layout error.)"""
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.device import DeviceModel
+    monkeypatch.setenv("HEAT_HOGWILD_IMPL", "staged")
+    monkeypatch.setenv("HEAT_LPR", str(lpr))
+    monkeypatch.setenv("HEAT_STAGES", str(stages))
+    rng = np.random.default_rng(K + N + lpr)
+    nu, ni, P = 40, 250, 500
+    S = (rng.standard_normal((nu, K)) * 0.1).astype(np.float32)
+    T = (rng.standard_normal((ni, K)) * 0.1).astype(np.float32)
+    S[3] = 0.0
+    T[7] = 0.0
+    u = rng.integers(0, nu, P).astype(np.int32)
+    i = rng.integers(0, ni, P).astype(np.int32)
+    s0 = 0x0F1E2D3C4B5A6978
+    S2, T2 = S.copy(), T.copy()
+    r = O.train_range(S2, T2, u, i, 0, P, s0, n_neg=N, lr=0.01, l2=0.0, mu=2.0, theta=0.1)
+    model = DeviceModel(S, T)
+    du, di = model.upload_pairs(u, i)
+    p = model.params(n_neg=N, lr=0.01, l2=0.0, mu=2.0, theta=0.1, cosine=True,
+                     mode=NN.MODE_HOGWILD, stream_base=s0, window=1, fp64=fp64)
+    model.counters.reset()
+    model.train_range(du, di, 0, P, p)
+    c = model.counters.read()
+    model.download(S, T)
+    assert c.pairs == P and c.degenerate == r.degenerate
+    assert abs(c.active - r.active) <= max(2, r.active // 1000)
+    assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss)
+    assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
