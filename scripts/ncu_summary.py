@@ -22,7 +22,7 @@ for i, h in enumerate(hdr):
 if json_out:
     import json
     g = {h: vals[i] for i, h in enumerate(hdr)}
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     rd = float(g["dram__bytes_read.sum"]) * scale[units["dram__bytes_read.sum"]]
     wr = float(g["dram__bytes_write.sum"]) * scale[units["dram__bytes_write.sum"]]
     with open(json_out, "w") as f:
