@@ -60,11 +60,10 @@ __global__ void __launch_bounds__(kExactThreads, 1)
     float *pos_buf = reinterpret_cast<float *>(sims + N);
     int32_t *nids = reinterpret_cast<int32_t *>(pos_buf + K);
     int32_t *list = nids + N;
-    // aggregation buffers (binary64): pooled history, h-gradient, W*grad
+    // aggregation buffers (binary64): pooled history, h-gradient
     double *pooled = reinterpret_cast<double *>(
         (reinterpret_cast<uintptr_t>(list + N) + 15) & ~uintptr_t(15));
     double *ugs = pooled + K;
-    double *whs = ugs + K;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
