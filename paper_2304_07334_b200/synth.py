@@ -143,9 +143,66 @@ def _distinct_draws(rng, cdf, users_rep: np.ndarray, need: np.ndarray, num_items
     return have_u, have_r
 
 
+class _CsrBuilder:
+    """Accumulates per-block (local user, item) arrays into a CSR set."""
+
+    def __init__(self, num_users: int, num_items: int):
+        self.num_users, self.num_items = num_users, num_items
+        self.counts = np.zeros(num_users, dtype=np.int64)
+        self.items: list[np.ndarray] = []
+
+    def add_sorted(self, glob_users: np.ndarray, counts: np.ndarray, items: np.ndarray) -> None:
+        """A block's per-user counts and its items already in CSR order."""
+        if len(items):
+            self.items.append(items)
+        self.counts[glob_users] += counts
+
+    def build(self) -> InteractionSet:
+        offsets = np.zeros(self.num_users + 1, dtype=np.int64)
+        np.cumsum(self.counts, out=offsets[1:])
+        items = np.concatenate(self.items) if self.items else np.empty(0, np.int32)
+        return InteractionSet(self.num_users, self.num_items, offsets, items)
+
+
+_SHARED = None  # (cdf, rank_to_id, deg, num_items, tf) for forked block workers
+
+
+def _split_block(rng, need, cdf, rank_to_id, num_items: int, tf: float):
+    """One block of users: distinct Zipf draws, the optional per-user test
+    split, each part as (counts per local user, items in CSR order)."""
+    n_local = len(need)
+    lu, lr = _distinct_draws(rng, cdf, None, need, num_items)
+    items = rank_to_id[lr]
+
+    def part(u, it):
+        order = np.argsort(u * num_items + it, kind="stable")
+        return np.bincount(u, minlength=n_local), it[order].astype(np.int32)
+
+    if tf <= 0:
+        return part(lu, items), None
+    d = need[lu]
+    n_test = (d * tf).astype(np.int64)
+    n_test = np.where(d - n_test < 1, np.maximum(0, d - 1), n_test)
+    key = rng.random(len(lu))
+    srt = np.lexsort((key, lu))
+    lu_s = lu[srt]
+    start = np.searchsorted(lu_s, np.arange(n_local), side="left")
+    rank = np.empty(len(lu), np.int64)
+    rank[srt] = np.arange(len(lu)) - start[lu_s]
+    is_test = rank < n_test
+    return part(lu[~is_test], items[~is_test]), part(lu[is_test], items[is_test])
+
+
+def _gen_block(args):
+    b0, b1, seed = args
+    cdf, rank_to_id, deg, num_items, tf = _SHARED
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return b0, b1, _split_block(rng, deg[b0:b1], cdf, rank_to_id, num_items, tf)
+
+
 def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
                  test_fraction: float | None = None, users_per_block: int = 200_000,
-                 scale: float = 1.0, sample_users: float | None = None):
+                 scale: float = 1.0, sample_users: float | None = None, workers: int = 0):
     """(train, test, spec) for a workload.
 
     ``scale`` < 1 shrinks the user count and interaction target together
@@ -153,7 +210,9 @@ def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
     user universe (so S keeps its size and its random-access footprint) but
     generates interactions for a seeded random fraction f of the users only —
     the config-5 stand-in (10 M x 2 M tables, 5.1 GB + 1.0 GB, far beyond L2)
-    without generating all 500 M interactions on the host."""
+    without generating all 500 M interactions on the host.  ``workers`` > 1
+    generates blocks in a process pool with one seeded stream per block (the
+    full-size config 5: 500 M interactions)."""
     if isinstance(spec, str):
         spec = CONFIGS[spec]
     tf = spec.test_fraction if test_fraction is None else test_fraction
@@ -171,38 +230,42 @@ def make_dataset(spec: WorkloadSpec | str, *, gen_seed: int = GEN_SEED,
     deg = _fit_degrees(rng, spec, num_users, target)
     rank_to_id = rng.permutation(spec.num_items).astype(np.int64)
     cdf = _zipf_cdf(spec.num_items, spec.zipf_s)
-    tr_u, tr_i, te_u, te_i = [], [], [], []
-    for b0 in range(0, num_users, users_per_block):
-        b1 = min(num_users, b0 + users_per_block)
-        need = deg[b0:b1]
-        lu, lr = _distinct_draws(rng, cdf, None, need, spec.num_items)
-        users = lu + b0 if user_ids is None else user_ids[lu + b0]
-        items = rank_to_id[lr]
-        if tf > 0:
-            d = need[lu]
-            n_test = (d * tf).astype(np.int64)
-            n_test = np.where(d - n_test < 1, np.maximum(0, d - 1), n_test)
-            key = rng.random(len(lu))
-            srt = np.lexsort((key, lu))
-            lu_s = lu[srt]
-            start = np.searchsorted(lu_s, np.arange(len(need)), side="left")
-            rank = np.empty(len(lu), np.int64)
-            rank[srt] = np.arange(len(lu)) - start[lu_s]
-            is_test = rank < n_test
-            te_u.append(users[is_test])
-            te_i.append(items[is_test])
-            tr_u.append(users[~is_test])
-            tr_i.append(items[~is_test])
-        else:
-            tr_u.append(users)
-            tr_i.append(items)
     nu = num_users if universe is None else universe
-    train = from_pairs(np.concatenate(tr_u), np.concatenate(tr_i), nu, spec.num_items)
-    if tf > 0:
-        test = from_pairs(np.concatenate(te_u), np.concatenate(te_i), nu, spec.num_items)
+    # CSR built block by block: blocks cover increasing, disjoint user ranges
+    # and a user's items are distinct by construction, so sorting each block
+    # by (user, item) gives from_pairs' order without a global sort (500 M
+    # interactions for config 5)
+    tr = _CsrBuilder(nu, spec.num_items)
+    te = _CsrBuilder(nu, spec.num_items)
+    blocks = [(b0, min(num_users, b0 + users_per_block))
+              for b0 in range(0, num_users, users_per_block)]
+    if workers > 1:
+        # scale-out path (config 5 at full size): one seeded stream per block
+        # (SeedSequence.spawn), blocks generated by a process pool; a
+        # different stream from the sequential path, equally a pure function
+        # of (config, gen_seed)
+        global _SHARED
+        seeds = np.random.SeedSequence(gen_seed).spawn(len(blocks))
+        _SHARED = (cdf, rank_to_id, deg, spec.num_items, tf)
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(workers) as pool:
+            for b0, b1, parts in pool.imap(_gen_block, [(b0, b1, sd) for (b0, b1), sd in
+                                                        zip(blocks, seeds)]):
+                glob = (np.arange(b0, b1, dtype=np.int64) if user_ids is None
+                        else user_ids[b0:b1])
+                tr.add_sorted(glob, *parts[0])
+                if tf > 0:
+                    te.add_sorted(glob, *parts[1])
+        _SHARED = None
     else:
-        test = InteractionSet(nu, spec.num_items, np.zeros(nu + 1, np.int64),
-                              np.empty(0, np.int32))
+        for b0, b1 in blocks:
+            glob = (np.arange(b0, b1, dtype=np.int64) if user_ids is None else user_ids[b0:b1])
+            parts = _split_block(rng, deg[b0:b1], cdf, rank_to_id, spec.num_items, tf)
+            tr.add_sorted(glob, *parts[0])
+            if tf > 0:
+                te.add_sorted(glob, *parts[1])
+    train = tr.build()
+    test = te.build()
     return train, test, spec
 
 
