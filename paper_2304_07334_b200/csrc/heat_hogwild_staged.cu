@@ -100,12 +100,20 @@ __device__ __forceinline__ void red_add_vec(float *p, const float (&d)[VW]) {
     }
 }
 
+#ifndef UREG_MAX
+#define UREG_MAX 128
+#endif
+
 template <int K, int D, bool F64, bool BULK, int LPR>
 __global__ void __launch_bounds__(32)
     hogwild_staged(HogwildArgs a, FastMod fm, int n_workers, int snap_cap, int cross) {
     using G = StGeom<K, LPR>;
     constexpr int VW = G::VW;
     constexpr int SR = G::SR;
+    // user-row segment held in registers when it is small enough (the ring,
+    // not registers, bounds residency)
+    constexpr bool UREG = !F64 && G::HALF <= UREG_MAX;
+    float2 ureg[UREG ? G::HALF / 2 : 1];
     extern __shared__ __align__(128) unsigned char sm[];
     const StLayout Lo = st_layout<K, D, LPR>(snap_cap);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Lo.off_bars);
@@ -363,6 +371,15 @@ __global__ void __launch_bounds__(32)
                 ss = F64 ? spd : (double)sp;
                 rs = ss > 0.0 ? sqrt(ss) : 0.0;
                 rss = ss > 0.0 ? rsqrtf((float)ss) : 0.f;
+                if constexpr (UREG) {  // this lane's user-row segment, once per pair
+                    const float *uph0 = up + hs * G::SEGF;
+#pragma unroll
+                    for (int k = 0; k < G::HALF; k += 4) {
+                        const float4 w4 = *reinterpret_cast<const float4 *>(uph0 + k);
+                        ureg[k / 2] = make_float2(w4.x, w4.y);
+                        ureg[k / 2 + 1] = make_float2(w4.z, w4.w);
+                    }
+                }
             }
             const int r = s * SR + rr;
             const bool valid = r <= N;
@@ -388,20 +405,38 @@ __global__ void __launch_bounds__(32)
                     tt = t0 + t1;
                     st = s0 + s1;
                 } else {
-                    // packed fp32x2 FMA (FFMA2, sm_100)
+                    // packed fp32x2 FMA (FFMA2, sm_100); with UREG the user
+                    // segment is in registers and only the row is read from
+                    // shared memory
                     float2 ta = make_float2(0.f, 0.f), tb = ta, sa = ta, sb = ta;
+                    float2 tc = ta, td = ta, sc2 = ta, sd = ta;  // second chain set
 #pragma unroll
                     for (int k = 0; k < G::HALF; k += 4) {
                         const float4 v = *reinterpret_cast<const float4 *>(row + k);
-                        const float4 w4 = *reinterpret_cast<const float4 *>(uph + k);
+                        float2 wlo, whi;
+                        if constexpr (UREG) {
+                            wlo = ureg[k / 2];
+                            whi = ureg[k / 2 + 1];
+                        } else {
+                            const float4 w4 = *reinterpret_cast<const float4 *>(uph + k);
+                            wlo = make_float2(w4.x, w4.y);
+                            whi = make_float2(w4.z, w4.w);
+                        }
                         const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
-                        ta = __ffma2_rn(vlo, vlo, ta);
-                        tb = __ffma2_rn(vhi, vhi, tb);
-                        sa = __ffma2_rn(make_float2(w4.x, w4.y), vlo, sa);
-                        sb = __ffma2_rn(make_float2(w4.z, w4.w), vhi, sb);
+                        if ((k / 4) & 1) {
+                            tc = __ffma2_rn(vlo, vlo, tc);
+                            td = __ffma2_rn(vhi, vhi, td);
+                            sc2 = __ffma2_rn(wlo, vlo, sc2);
+                            sd = __ffma2_rn(whi, vhi, sd);
+                        } else {
+                            ta = __ffma2_rn(vlo, vlo, ta);
+                            tb = __ffma2_rn(vhi, vhi, tb);
+                            sa = __ffma2_rn(wlo, vlo, sa);
+                            sb = __ffma2_rn(whi, vhi, sb);
+                        }
                     }
-                    tt = (double)((ta.x + ta.y) + (tb.x + tb.y));
-                    st = (double)((sa.x + sa.y) + (sb.x + sb.y));
+                    tt = (double)(((ta.x + ta.y) + (tb.x + tb.y)) + ((tc.x + tc.y) + (td.x + td.y)));
+                    st = (double)(((sa.x + sa.y) + (sb.x + sb.y)) + ((sc2.x + sc2.y) + (sd.x + sd.y)));
                 }
             }
             if constexpr (LPR == 2) {  // the row's two column segments
@@ -575,6 +610,7 @@ static cudaError_t launch_staged_d(const HogwildArgs &a, cudaStream_t st, int *w
         if (lpr == 2) {
             if (bulk) return launch_staged_k<K, 2, F64, true, 2>(a, st, workers_out, cross);
             switch (D) {
+            case 1: return launch_staged_k<K, 1, F64, false, 2>(a, st, workers_out, cross);
             case 2: return launch_staged_k<K, 2, F64, false, 2>(a, st, workers_out, cross);
             case 4: return launch_staged_k<K, 4, F64, false, 2>(a, st, workers_out, cross);
             case 6: return launch_staged_k<K, 6, F64, false, 2>(a, st, workers_out, cross);
@@ -584,6 +620,7 @@ static cudaError_t launch_staged_d(const HogwildArgs &a, cudaStream_t st, int *w
     }
     if (bulk) return launch_staged_k<K, 2, F64, true, 1>(a, st, workers_out, cross);
     switch (D) {
+    case 1: return launch_staged_k<K, 1, F64, false, 1>(a, st, workers_out, cross);
     case 2: return launch_staged_k<K, 2, F64, false, 1>(a, st, workers_out, cross);
     case 4: return launch_staged_k<K, 4, F64, false, 1>(a, st, workers_out, cross);
     case 6: return launch_staged_k<K, 6, F64, false, 1>(a, st, workers_out, cross);
@@ -595,7 +632,10 @@ cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t st, int *wo
                                   bool bulk) {
     // stages in flight per warp: enough rows in flight to cover L2 latency,
     // few enough that the window's workers fit on the SMs
-    int D = a.K <= 32 ? 4 : 2;
+    // measured: K = 128 (two lanes per row) runs best with a single stage in
+    // flight per warp: 15 warps per SM hide the latency better than 9 warps
+    // with two stages each (c4 +12 %, c5 +4 %)
+    int D = a.K <= 32 ? 4 : (a.K >= 128 ? 1 : 2);
     if (const char *e = getenv("HEAT_STAGES")) D = atoi(e) > 0 ? atoi(e) : D;
     // cross-pair prefetch halves the workers a window allows; measured slower
     int cross = 0;

@@ -860,7 +860,8 @@ def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
 @pytest.mark.parametrize("K,N,lpr,fp64,stages", [(64, 100, 1, False, 2), (64, 100, 2, False, 3),
                                                  (128, 300, 2, False, 2), (128, 300, 1, True, 4),
                                                  (128, 64, 2, True, 2), (64, 500, 2, True, 4),
-                                                 (64, 60, 2, False, 4)])
+                                                 (64, 60, 2, False, 4), (128, 300, 2, False, 1),
+                                                 (64, 100, 1, False, 1)])
 def test_staged_kernel_variants_window1_vs_oracle(torch_cuda, monkeypatch, K, N, lpr, fp64,
                                                   stages):
     """The staged throughput kernel in each row layout (one or two lanes per
