@@ -9,7 +9,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <cstdlib>
 #include <string>
 
@@ -48,23 +50,34 @@ int sm_count() {
     return cached[dev];
 }
 
-// Scratch for exact-mode snapshots when the caller passes none.
-static std::mutex g_scratch_mu;
-static void *g_scratch[64] = {nullptr};
-static size_t g_scratch_size[64] = {0};
-
-static void *get_scratch(size_t bytes) {
+// Library-owned scratch when the caller passes none: one buffer per
+// (purpose, device, stream), so kernels queued on different streams never
+// share it.  Grown on demand; growth waits for the device to go idle.
+void *stream_scratch(int purpose, size_t bytes, cudaStream_t stream) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, cudaStream_t>, std::pair<void *, size_t>> bufs;
     int dev = 0;
     cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_scratch_mu);
-    if (g_scratch_size[dev] < bytes) {
-        if (g_scratch[dev]) cudaFree(g_scratch[dev]);
-        g_scratch[dev] = nullptr;
-        g_scratch_size[dev] = 0;
-        if (cudaMalloc(&g_scratch[dev], bytes) != cudaSuccess) return nullptr;
-        g_scratch_size[dev] = bytes;
+    std::lock_guard<std::mutex> lk(mu);
+    auto &b = bufs[std::make_tuple(purpose, dev, stream)];
+    if (b.second < bytes) {
+        if (b.first) {
+            cudaDeviceSynchronize();
+            cudaFree(b.first);
+        }
+        b = {nullptr, 0};
+        if (cudaMalloc(&b.first, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            b.first = nullptr;
+            return nullptr;
+        }
+        b.second = bytes;
     }
-    return g_scratch[dev];
+    return b.first;
+}
+
+static void *get_scratch(size_t bytes, cudaStream_t stream) {
+    return stream_scratch(0, bytes, stream);
 }
 
 // ---- ordered / atomic item-delta application (multi-GPU exchange) --------
@@ -268,7 +281,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         if (!agg && exact_spec_supported(p->dim, p->n_neg) && !getenv("HEAT_EXACT_SERIAL")) {
             void *sc = scratch ? scratch
                                : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim, s_rows,
-                                                                        t_rows));
+                                                                        t_rows), st);
             if (!sc) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
             e = launch_exact_spec(S, s_rows, T, t_rows, ep_users, ep_items, start, stop, p->dim,
                                   p->n_neg, p->use_cosine, p->lr, p->l2, p->mu, p->theta,
@@ -280,7 +293,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
                         p->n_neg, p->dim);
         void *snap = scratch ? scratch
                              : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim, s_rows,
-                                                                      t_rows));
+                                                                      t_rows), st);
         if (!snap) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
         e = launch_exact(S, T, ep_users, ep_items, start, stop, p->dim, p->n_neg, p->use_cosine,
                          p->lr, p->l2, p->mu, p->theta, p->stream_base, t_rows, counters,
@@ -306,7 +319,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         a.pair_index = pair_index;
         if (agg) {
             void *sc = scratch ? scratch
-                               : get_scratch(agg_hogwild_scratch_bytes(p->dim, p->window));
+                               : get_scratch(agg_hogwild_scratch_bytes(p->dim, p->window), st);
             if (!sc) return fail(HEAT_ERR_CUDA, "aggregation: scratch allocation failed");
             e = launch_agg_hogwild(a, *agg, sc, st);
             if (e == cudaErrorNotSupported)

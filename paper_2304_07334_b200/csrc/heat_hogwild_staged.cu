@@ -544,30 +544,6 @@ __global__ void __launch_bounds__(32)
     }
 }
 
-// Per-device spill area, grown on demand and kept (the launch is asynchronous,
-// so a buffer is only ever replaced after the device is idle).
-static void *spill_area(size_t bytes) {
-    static std::mutex mu;
-    static void *buf[64] = {nullptr};
-    static size_t size[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> lk(mu);
-    if (size[dev] < bytes) {
-        cudaDeviceSynchronize();
-        if (buf[dev]) cudaFree(buf[dev]);
-        buf[dev] = nullptr;
-        size[dev] = 0;
-        if (cudaMalloc(&buf[dev], bytes) != cudaSuccess) {
-            cudaGetLastError();
-            return nullptr;
-        }
-        size[dev] = bytes;
-    }
-    return buf[dev];
-}
-
 template <int K, int D, bool F64, bool BULK, int LPR>
 static cudaError_t launch_staged_k(const HogwildArgs &a, cudaStream_t st, int *workers_out,
                                    int cross) {
@@ -595,7 +571,7 @@ static cudaError_t launch_staged_k(const HogwildArgs &a, cudaStream_t st, int *w
         b.spill_cap = a.N + 1;
         b.spill_stride = ((int64_t)b.spill_cap * (K * sizeof(float) + sizeof(WriteEntry)) + 255) &
                          ~(int64_t)255;
-        b.spill = static_cast<unsigned char *>(spill_area((size_t)(b.spill_stride * nw)));
+        b.spill = static_cast<unsigned char *>(stream_scratch(1, (size_t)(b.spill_stride * nw), st));
         if (!b.spill) b.spill_cap = 0;  // no memory: mid-pair application (documented)
     }
     kern<<<(unsigned)nw, 32, L.total, st>>>(b, FastMod::make((uint64_t)a.num_items), (int)nw,

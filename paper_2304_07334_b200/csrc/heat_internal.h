@@ -93,6 +93,8 @@ cudaError_t launch_exact_spec(float *S, int64_t s_rows, float *T, int64_t t_rows
                               void *scratch, const int64_t *pair_index, cudaStream_t stream);
 
 int sm_count();
+// library-owned scratch per (purpose, device, stream); nullptr if out of memory
+void *stream_scratch(int purpose, size_t bytes, cudaStream_t stream);
 size_t eval_max_k_supported(int K);
 
 }  // namespace heat
