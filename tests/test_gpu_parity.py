@@ -898,3 +898,45 @@ def test_staged_kernel_variants_window1_vs_oracle(torch_cuda, monkeypatch, K, N,
     assert abs(c.active - r.active) <= max(2, r.active // 1000)
     assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss)
     assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
+
+
+@pytest.mark.parametrize("K,N,mode", [(512, 20, "hogwild"), (256, 255, "exact"), (64, 255, "hogwild"),
+                                      (64, 255, "hogwild32"), (32, 63, "hogwild32"),
+                                      (16, 1, "hogwild"), (1, 1, "exact"), (256, 8, "hogwild")])
+def test_boundary_shapes_vs_oracle(torch_cuda, K, N, mode):
+    """Size boundaries of every kernel family: the widest rows the ABI takes
+    (dim 512, generic kernel), the largest resident pair (N+1 = 256 rows,
+    eight 32-row stages), the largest speculative-exact row (dim 256), and
+    the smallest shapes.  EXACT is bit-identical; HOGWILD at window 1 within
+    1e-4 (fp64 dots; "hogwild32" = the fp32 resident kernel, with a margin
+    that keeps sims away from theta so fp32 cannot flip a decision)."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.device import DeviceModel
+    rng = np.random.default_rng(K * 3 + N)
+    nu, ni, P = 30, 400, 300
+    S = (rng.standard_normal((nu, K)) * 0.1).astype(np.float32)
+    T = (rng.standard_normal((ni, K)) * 0.1).astype(np.float32)
+    u = rng.integers(0, nu, P).astype(np.int32)
+    i = rng.integers(0, ni, P).astype(np.int32)
+    s0 = 0x5EED5EED5EED5EED
+    S2, T2 = S.copy(), T.copy()
+    theta = 0.6 if mode == "hogwild32" else 0.05
+    r = O.train_range(S2, T2, u, i, 0, P, s0, n_neg=N, lr=0.02, l2=0.0, mu=2.0, theta=theta)
+    model = DeviceModel(S, T)
+    du, di = model.upload_pairs(u, i)
+    exact = mode == "exact"
+    p = model.params(n_neg=N, lr=0.02, l2=0.0, mu=2.0, theta=theta, cosine=True,
+                     mode=NN.MODE_EXACT if exact else NN.MODE_HOGWILD, stream_base=s0,
+                     window=1, fp64=mode == "hogwild")
+    model.counters.reset()
+    model.train_range(du, di, 0, P, p)
+    c = model.counters.read()
+    model.download(S, T)
+    assert c.pairs == P
+    if exact:
+        assert S.tobytes() == S2.tobytes() and T.tobytes() == T2.tobytes()
+        assert c.loss == r.loss
+    else:
+        assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss)
+        assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
