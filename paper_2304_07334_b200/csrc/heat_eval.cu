@@ -16,6 +16,7 @@
 // it (the incumbent has the lower id) — exactly the reference's tie rule.
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "heat_common.cuh"
 #include "heat_internal.h"
@@ -235,6 +236,268 @@ __global__ void __launch_bounds__(kEvalThreads)
     }
 }
 
+// ---- register-blocked variant (K <= 128): warp w scores users 4w..4w+3
+// against a 128-item tile, lane owns items lane + 32 m (m < 4): 16 binary64
+// dot products per thread, 16 DFMA per 6 shared loads.  The warp merges its
+// own users straight from registers (no score buffer, two barriers per tile).
+// A candidate is screened by score * (1/unorm) * (1/inorm) against the list's
+// k-th score; only survivors get the exact s / (unorm * inorm) of
+// evaluator.py:48-58, so the list holds exactly the values the plain kernel
+// computes (and the reference's division).  The next tile is prefetched
+// into registers while the current one is scored.
+constexpr int kRbUsers = 32;
+constexpr int kRbItems = 128;
+
+__host__ __device__ inline size_t eval_rb_smem_bytes(int K, int k) {
+    size_t b = 0;
+    b += align16(sizeof(double) * K * kRbUsers);      // user vectors, transposed
+    b += align16(sizeof(float) * kRbItems * (K + 1)); // item tile (padded rows)
+    b += align16(sizeof(double) * kRbUsers * k);     // list scores
+    b += align16(sizeof(int32_t) * kRbUsers * k);    // list ids
+    b += align16(sizeof(uint32_t) * kRbUsers * 4);   // train-positive mask of the tile
+    b += align16(sizeof(double) * kRbUsers * 2);     // user norms and reciprocals
+    b += align16(sizeof(int64_t) * kRbUsers * 2);    // train cursors and ends
+    return b;
+}
+
+__global__ void item_norms_kernel(const float *__restrict__ T, int64_t t_rows, int K,
+                                  double *__restrict__ norm, double *__restrict__ rnorm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= t_rows) return;
+    double a = 0.0;
+    for (int c = 0; c < K; ++c) {
+        const double x = (double)T[i * K + c];
+        a = fma(x, x, a);
+    }
+    const double n = sqrt(a);
+    norm[i] = n;
+    rnorm[i] = n > 0.0 ? 1.0 / n : 0.0;
+}
+
+template <int KC>  // K rounded up to a multiple of 4 for the staging loads
+__global__ void __launch_bounds__(256)
+    eval_rb_kernel(const void *__restrict__ S, int s_f64, const float *__restrict__ T,
+                   int64_t t_rows, int K, const double *__restrict__ inorm_g,
+                   const double *__restrict__ rinorm_g, const int32_t *__restrict__ users,
+                   int64_t n_users, const int64_t *__restrict__ tr_off,
+                   const int32_t *__restrict__ tr_items, int64_t tr_num_users,
+                   const int64_t *__restrict__ te_off, const int32_t *__restrict__ te_items,
+                   int k, int cosine, const double *__restrict__ dcg_w,
+                   const double *__restrict__ idcg, int32_t *__restrict__ topk,
+                   double *__restrict__ recall, double *__restrict__ ndcg) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char *ptr = smem;
+    double *uT = reinterpret_cast<double *>(ptr);
+    ptr += align16(sizeof(double) * K * kRbUsers);
+    float *tile = reinterpret_cast<float *>(ptr);
+    ptr += align16(sizeof(float) * kRbItems * (K + 1));
+    double *ls = reinterpret_cast<double *>(ptr);
+    ptr += align16(sizeof(double) * kRbUsers * k);
+    int32_t *lid = reinterpret_cast<int32_t *>(ptr);
+    ptr += align16(sizeof(int32_t) * kRbUsers * k);
+    uint32_t *pmask = reinterpret_cast<uint32_t *>(ptr);
+    ptr += align16(sizeof(uint32_t) * kRbUsers * 4);
+    double *unv = reinterpret_cast<double *>(ptr);  // [0, 32) norms, [32, 64) reciprocals
+    ptr += align16(sizeof(double) * kRbUsers * 2);
+    int64_t *curv = reinterpret_cast<int64_t *>(ptr);  // [0, 32) cursors, [32, 64) ends
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ubase = (int64_t)blockIdx.x * kRbUsers;
+    const int nub = (int)imin64(kRbUsers, n_users - ubase);
+    for (int i = tid; i < kRbUsers * K; i += 256) {
+        const int b = i / K, c = i % K;
+        double v = 0.0;
+        if (b < nub) {
+            const int64_t off = (int64_t)users[ubase + b] * K + c;
+            v = s_f64 ? reinterpret_cast<const double *>(S)[off]
+                      : (double)reinterpret_cast<const float *>(S)[off];
+        }
+        uT[c * kRbUsers + b] = v;
+    }
+    __syncthreads();
+    // user norms, train cursors (shared), list sizes (registers)
+    if (tid < kRbUsers) {
+        const int b = tid;
+        double a = 0.0;
+        for (int c = 0; c < K; ++c) a = fma(uT[c * kRbUsers + b], uT[c * kRbUsers + b], a);
+        const double n = sqrt(a);
+        unv[b] = n;
+        unv[kRbUsers + b] = n > 0.0 ? 1.0 / n : 0.0;
+        const int64_t u = b < nub ? users[ubase + b] : 0;
+        const bool has = b < nub && u < tr_num_users;
+        curv[b] = has ? tr_off[u] : 0;
+        curv[kRbUsers + b] = has ? tr_off[u + 1] : 0;
+    }
+    int n_l[4] = {0, 0, 0, 0};
+    // tile staging: 128 rows x K floats, float4 loads held in registers
+    constexpr int PER = (kRbItems * KC / 4 + 255) / 256;  // float4 per thread
+    float4 pre[PER];
+    auto load_tile = [&](int64_t i0) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int f = tid + q * 256;  // float4 index within the tile
+            const int r = f / (KC / 4), c4 = f % (KC / 4);
+            const int64_t row = i0 + r;
+            pre[q] = (r < kRbItems && row < t_rows && c4 * 4 < K)
+                         ? *reinterpret_cast<const float4 *>(T + row * K + c4 * 4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto store_tile = [&]() {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int f = tid + q * 256;
+            const int r = f / (KC / 4), c = (f % (KC / 4)) * 4;
+            if (r < kRbItems && c < K) {
+                float *d = tile + r * (K + 1) + c;
+                d[0] = pre[q].x; d[1] = pre[q].y; d[2] = pre[q].z; d[3] = pre[q].w;
+            }
+        }
+    };
+    load_tile(0);
+    for (int64_t i0 = 0; i0 < t_rows; i0 += kRbItems) {
+        __syncthreads();  // previous tile consumed
+        store_tile();
+        // this tile's train positives per user -> 128-bit masks
+        if (lane < 4)
+            for (int j = 0; j < 4; ++j) pmask[(warp * 4 + j) * 4 + lane] = 0u;
+        __syncthreads();
+        if (i0 + kRbItems < t_rows) load_tile(i0 + kRbItems);  // overlaps the scoring
+        for (int j = 0; j < 4; ++j) {
+            const int b = warp * 4 + j;
+            int64_t c0 = curv[b];
+            const int64_t cend = curv[kRbUsers + b];
+            while (c0 < cend) {
+                const int64_t idx = c0 + lane;
+                const int64_t item = idx < cend ? (int64_t)tr_items[idx] : INT64_MAX;
+                const bool in_tile = item < i0 + kRbItems;
+                if (in_tile) {
+                    const int o = (int)(item - i0);
+                    atomicOr(&pmask[(warp * 4 + j) * 4 + (o >> 5)], 1u << (o & 31));
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, in_tile);
+                c0 += __popc(m);
+                if (m != 0xffffffffu) break;
+            }
+            __syncwarp();
+            if (lane == 0) curv[b] = c0;
+        }
+        __syncwarp();
+        // 4 users x 4 items of dot products
+        double acc[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[j][m] = 0.0;
+        const double *ucol = uT + warp * 4;
+        for (int c = 0; c < K; ++c) {
+            const double2 ua = *reinterpret_cast<const double2 *>(ucol + c * kRbUsers);
+            const double2 ub = *reinterpret_cast<const double2 *>(ucol + c * kRbUsers + 2);
+            const double uv[4] = {ua.x, ua.y, ub.x, ub.y};
+            double iv[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) iv[m] = (double)tile[(lane + 32 * m) * (K + 1) + c];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) acc[j][m] = fma(uv[j], iv[m], acc[j][m]);
+        }
+        __syncwarp();
+        // merge, one user at a time (items in increasing id order per lane
+        // group; the tie rule keeps the lower id, so order of arrival within
+        // equal scores does not matter: the insertion point compares ids)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int b = warp * 4 + j;
+            if (b >= nub) continue;
+            double *lsb = ls + b * k;
+            int32_t *lidb = lid + b * k;
+            int n = n_l[j];
+            for (int m = 0; m < 4; ++m) {
+                const int o = lane + 32 * m;
+                const int64_t item = i0 + o;
+                const bool valid = item < t_rows &&
+                                   !((pmask[b * 4 + (o >> 5)] >> (o & 31)) & 1u);
+                double s = acc[j][m];
+                const double kth = n == k ? lsb[k - 1] : -INFINITY;
+                bool cand = valid;
+                if (cand && n == k && cosine) {  // screen: approximate cosine
+                    const double approx = s * unv[kRbUsers + b] * rinorm_g[item];
+                    cand = approx >= kth - 1e-9;
+                }
+                double ex = s;
+                if (cand && cosine) {
+                    const double in = inorm_g[item], un = unv[b];
+                    ex = (un == 0.0 || in == 0.0) ? 0.0 : s / (un * in);
+                }
+                if (cand && n == k) cand = ex > kth || (ex == kth && false);
+                unsigned mk = __ballot_sync(0xffffffffu, cand);
+                while (mk) {
+                    const int src = __ffs(mk) - 1;
+                    mk &= mk - 1;
+                    const double cs = __shfl_sync(0xffffffffu, ex, src);
+                    const int32_t cid = (int32_t)(i0 + src + 32 * m);
+                    if (n == k && !(cs > lsb[k - 1] ||
+                                    (cs == lsb[k - 1] && cid < lidb[k - 1])))
+                        continue;
+                    int posn = 0;
+                    for (int e0 = 0; e0 < n; e0 += 32) {
+                        const int e = e0 + lane;
+                        const bool better = e < n && (lsb[e] > cs || (lsb[e] == cs && lidb[e] < cid));
+                        posn += __popc(__ballot_sync(0xffffffffu, better));
+                    }
+                    const int newn = n < k ? n + 1 : k;
+                    for (int hi = newn - 1; hi > posn; hi -= 32) {
+                        const int dst = hi - lane;
+                        const bool mv = dst > posn;
+                        double vs = 0.0;
+                        int32_t vi = 0;
+                        if (mv) { vs = lsb[dst - 1]; vi = lidb[dst - 1]; }
+                        __syncwarp();
+                        if (mv) { lsb[dst] = vs; lidb[dst] = vi; }
+                        __syncwarp();
+                    }
+                    if (lane == 0 && posn < k) { lsb[posn] = cs; lidb[posn] = cid; }
+                    __syncwarp();
+                    n = newn;
+                }
+            }
+            n_l[j] = n;
+        }
+    }
+    // hits / recall / NDCG, one lane per user of the warp; ranks in order
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int b = warp * 4 + j;
+        if (b >= nub) continue;
+        const int64_t ug = ubase + b;
+        const int64_t u = users[ug];
+        const int n = n_l[j];
+        if (topk)
+            for (int e = lane; e < k; e += 32) topk[ug * k + e] = e < n ? lid[b * k + e] : -1;
+        if (lane == 0) {
+            const int64_t tb = te_off[u], te = te_off[u + 1];
+            const int64_t nt = te - tb;
+            int hits = 0;
+            double dcg = 0.0;
+            for (int r = 0; r < n; ++r) {
+                const int32_t item = lid[b * k + r];
+                int64_t lo = tb, hi2 = te;
+                while (lo < hi2) {
+                    const int64_t mid = (lo + hi2) >> 1;
+                    if (te_items[mid] < item) lo = mid + 1; else hi2 = mid;
+                }
+                if (lo < te && te_items[lo] == item) {
+                    ++hits;
+                    dcg += dcg_w[r];
+                }
+            }
+            recall[ug] = (double)hits / (double)nt;
+            ndcg[ug] = dcg / idcg[(k < nt ? k : nt) - 1];
+        }
+    }
+}
+
 template <int UB>
 static cudaError_t launch_eval_ub(const void *S, int s_f64, const float *T, int64_t t_rows, int K,
                                   const int32_t *users, int64_t n_users, const int64_t *tr_off,
@@ -253,6 +516,29 @@ static cudaError_t launch_eval_ub(const void *S, int s_f64, const float *T, int6
     return cudaGetLastError();
 }
 
+template <int KC>
+static cudaError_t launch_eval_rb(const void *S, int s_f64, const float *T, int64_t t_rows,
+                                  int K, const int32_t *users, int64_t n_users,
+                                  const int64_t *tr_off, const int32_t *tr_items, int64_t tr_nu,
+                                  const int64_t *te_off, const int32_t *te_items, int k,
+                                  int cosine, const double *dw, const double *idcg, int32_t *topk,
+                                  double *rec, double *nd, cudaStream_t st) {
+    const size_t smem = eval_rb_smem_bytes(K, k);
+    cudaError_t e = cudaFuncSetAttribute(eval_rb_kernel<KC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // item norms and reciprocals, once per call (evaluator.py:140-141)
+    double *norms = static_cast<double *>(stream_scratch(2, (size_t)t_rows * 16, st));
+    if (!norms) return cudaErrorMemoryAllocation;
+    item_norms_kernel<<<(unsigned)((t_rows + 255) / 256), 256, 0, st>>>(T, t_rows, K, norms,
+                                                                        norms + t_rows);
+    const int64_t blocks = (n_users + kRbUsers - 1) / kRbUsers;
+    eval_rb_kernel<KC><<<(unsigned)blocks, 256, smem, st>>>(
+        S, s_f64, T, t_rows, K, norms, norms + t_rows, users, n_users, tr_off, tr_items, tr_nu,
+        te_off, te_items, k, cosine, dw, idcg, topk, rec, nd);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows, int K,
                         const int32_t *users, int64_t n_users, const int64_t *tr_offsets,
                         const int32_t *tr_items, int64_t tr_num_users, const int64_t *te_offsets,
@@ -261,6 +547,19 @@ cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows
                         cudaStream_t stream) {
     if (n_users == 0) return cudaSuccess;
     const size_t cap = 200 * 1024;
+    const bool rb_ok = K % 4 == 0 && eval_rb_smem_bytes(K, k) <= cap && !getenv("HEAT_EVAL_PLAIN");
+    if (rb_ok && K <= 32)
+        return launch_eval_rb<32>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
+                                  tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
+                                  topk, recall, ndcg, stream);
+    if (rb_ok && K <= 64)
+        return launch_eval_rb<64>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
+                                  tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
+                                  topk, recall, ndcg, stream);
+    if (rb_ok && K <= 128)
+        return launch_eval_rb<128>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
+                                   tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
+                                   topk, recall, ndcg, stream);
     if (eval_smem_bytes<32>(K, k) <= cap)
         return launch_eval_ub<32>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
                                   tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
