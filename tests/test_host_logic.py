@@ -55,6 +55,33 @@ def test_abi_rejects_bad_arguments_without_a_gpu():
         N.check(N.HEAT_ERR_INVALID)
     assert L.heat_sample_negatives(0, 0, 1, 0, 10, fake, None) == N.HEAT_ERR_INVALID
     assert L.heat_sample_negatives(0, 0, 1, 4, 0, fake, None) == N.HEAT_ERR_INVALID
+    # aggregation: DELTA mode is unsupported, odd widths in HOGWILD mode too
+    p.dim, p.theta, p.mode = 48, 0.5, N.MODE_DELTA
+    agg = N.AggParams(W=16, tr_offsets=16, tr_items=16, gamma=0.5, lr=0.1, mini_batch=4,
+                      max_history=10, history_grad=0, reserved=0, accu=None, counter=None)
+    rc = L.heat_train_range(fake, 1, fake, 1, fake, fake, 0, 1, ctypes.byref(p), fake,
+                            fake, fake, fake, 1, None, ctypes.byref(agg), None, None)
+    assert rc == N.HEAT_ERR_UNSUPPORTED
+    p.mode = N.MODE_HOGWILD
+    rc = L.heat_train_range(fake, 1, fake, 1, fake, fake, 0, 1, ctypes.byref(p), fake,
+                            None, None, None, 0, None, ctypes.byref(agg), None, None)
+    assert rc == N.HEAT_ERR_UNSUPPORTED and b"dim" in L.heat_last_error()
+    p.mode = N.MODE_EXACT  # EXACT aggregation needs the accumulator state
+    rc = L.heat_train_range(fake, 1, fake, 1, fake, fake, 0, 1, ctypes.byref(p), fake,
+                            None, None, None, 0, None, ctypes.byref(agg), None, None)
+    assert rc == N.HEAT_ERR_INVALID
+    assert L.heat_agg_scratch_bytes(128, 4096) >= 3 * 4096 * 128 * 4
+    # multi-GPU runtime and the order-independent apply reject bad arguments
+    h = ctypes.c_void_p()
+    assert L.heat_shard_create(0, 0, None, 0, ctypes.byref(h)) == N.HEAT_ERR_INVALID
+    assert L.heat_shard_create(2, 2, None, 0, ctypes.byref(h)) == N.HEAT_ERR_INVALID
+    st = N.ShardStats()
+    assert L.heat_shard_epoch(None, fake, 1, fake, 1, fake, fake, None, None, 1, 1,
+                              ctypes.byref(p), fake, ctypes.byref(st), None) == N.HEAT_ERR_INVALID
+    assert L.heat_apply_row_deltas_fixed(None, 1, 4, fake, fake, fake, 1, 1, fake, fake,
+                                         None) == N.HEAT_ERR_INVALID
+    assert L.heat_apply_row_deltas_fixed(fake, 1, 4, fake, fake, fake, 0, 1, fake, fake,
+                                         None) == N.HEAT_ERR_INVALID
 
 
 def test_config_validation_matches_reference():
@@ -154,6 +181,24 @@ def test_synthetic_workloads_hit_baseline_shapes():
     assert set(CONFIGS) == {"c1", "c2", "c3", "c4", "c5"}
     a, b = make_clustered(50, 100, 5, 10, seed=1)
     assert a.num_pairs > 0 and b.num_pairs > 0
+
+
+def test_block_parallel_generator_builds_valid_csr():
+    """The scale-out generator (process pool, one stream per block, per-block
+    CSR): exact interaction count, sorted distinct items per user, ids in
+    range, deterministic, and the sequential path is unchanged by it."""
+    tr, _, _ = make_dataset("c5", sample_users=0.0004, workers=2, users_per_block=1000)
+    tr2, _, _ = make_dataset("c5", sample_users=0.0004, workers=2, users_per_block=1000)
+    assert tr.num_pairs == round(500_000_000 * 0.0004)
+    assert (tr.offsets == tr2.offsets).all() and (tr.items == tr2.items).all()
+    assert tr.items.dtype == np.int32 and tr.items.min() >= 0 and tr.items.max() < 2_000_000
+    deg = np.diff(tr.offsets)
+    assert deg.sum() == tr.num_pairs and (deg >= 0).all()
+    for u in np.flatnonzero(deg)[::37]:
+        sl = tr.slice(u)
+        assert np.all(np.diff(sl) > 0)
+    seq, _, _ = make_dataset("c5", sample_users=0.0004, users_per_block=1000)
+    assert seq.num_pairs == tr.num_pairs and (np.diff(seq.offsets) == deg).all()
 
 
 def test_shard_epoch_partitions_pairs_by_owner():
