@@ -165,7 +165,10 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": spec.name, "users": train.num_users,
                        "items": train.num_items, "train_pairs": train.num_pairs,
-                       "dim": spec.dim, "negatives": spec.negatives, "batch": spec.batch},
+                       "dim": spec.dim, "negatives": spec.negatives, "theta": spec.theta,
+                       "mu": spec.mu, "batch": spec.batch, "mode": "hogwild (host threads)",
+                       "lr": spec.learning_rate,
+                       "step": "a bounded sample of one epoch (cpu_baseline.sample)"},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "port",
                              "sample": r["sample"]},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
