@@ -940,3 +940,40 @@ def test_boundary_shapes_vs_oracle(torch_cuda, K, N, mode):
     else:
         assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss)
         assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
+
+
+@pytest.mark.parametrize("impl", ["resident", "staged", "generic"])
+def test_hogwild_updates_are_sparse(torch_cuda, monkeypatch, impl):
+    """Sparse updates (the reference's test_trainer.py:94-107): rows that no
+    pair reads keep their exact initial bits, in every throughput kernel."""
+    import torch
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.device import DeviceModel
+    monkeypatch.setenv("HEAT_HOGWILD_IMPL", impl)
+    rng = np.random.default_rng(17)
+    nu, ni, K, NN, P = 500, 20000, 64, 40, 800
+    S = (rng.standard_normal((nu, K)) * 0.1).astype(np.float32)
+    T = (rng.standard_normal((ni, K)) * 0.1).astype(np.float32)
+    u = rng.integers(0, nu // 2, P).astype(np.int32)  # upper half of the users never trains
+    i = rng.integers(0, ni, P).astype(np.int32)
+    s0 = 0xABCDEF0123456789
+    m = DeviceModel(S.copy(), T.copy())
+    du, di = m.upload_pairs(u, i)
+    p = m.params(n_neg=NN, lr=0.05, l2=0.0, mu=2.0, theta=0.0, cosine=True,
+                 mode=N.MODE_HOGWILD, stream_base=s0, window=64)
+    m.counters.reset()
+    m.train_range(du, di, 0, P, p)
+    negs = torch.empty(P * NN, dtype=torch.int32, device="cuda")
+    N.check(N.lib().heat_sample_negatives(s0, 0, P, NN, ni, ctypes_ptr(negs), None))
+    read = np.zeros(ni, bool)
+    read[i] = True
+    read[negs.cpu().numpy()] = True
+    S2, T2 = m.S.cpu().numpy(), m.T.cpu().numpy()
+    assert S2[nu // 2:].tobytes() == S[nu // 2:].tobytes()
+    assert T2[~read].tobytes() == T[~read].tobytes()
+    assert (~read).sum() > 1000 and not np.array_equal(T2[read], T[read])
+
+
+def ctypes_ptr(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr())
