@@ -78,6 +78,13 @@ class PairPrefetcher:
     DEPTH = 4 if (os.cpu_count() or 1) >= 8 else 2
     MAX_PENDING = DEPTH + 1
 
+    @classmethod
+    def depth_for(cls, num_pairs: int) -> int:
+        """Look-ahead for an epoch of num_pairs: the full depth while the
+        pinned buffers stay small, one epoch ahead for scale-out epochs
+        (500 M pairs = 4 GB of pinned order per epoch)."""
+        return cls.DEPTH if num_pairs * 8 <= (512 << 20) else 1
+
     def prefetch(self, train, seed: int) -> None:
         key = (_train_key(train), seed)
         with self._lock:

@@ -199,7 +199,8 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     t_start = time.perf_counter()
     model = _session_model(S.values, T.values)  # raises without CUDA: no CPU fallback
     bufs = PREFETCH.get(train, shuffle_seed(cfg.seed, epoch))
-    for ahead in range(1, PREFETCH.DEPTH + 1):  # host threads keep the next orders coming
+    for ahead in range(1, PREFETCH.depth_for(train.num_pairs) + 1):  # host threads keep the
+        # next orders coming
         PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + ahead))
     dev = model.device
     stream = torch.cuda.current_stream(dev)
