@@ -117,6 +117,10 @@ def evaluation(cfg_name):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "exact":
+        exact("c1", 20000)
+        exact("c2", 50000)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "agg":
         agg_hogwild()
         sys.exit(0)
