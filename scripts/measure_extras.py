@@ -98,6 +98,41 @@ def agg_hogwild(cfg_name="c2", K=128, NN=64, H=100, mb=32, window=4096, epochs=3
           flush=True)
 
 
+def quality(cfg_name="c2", epochs=20):
+    """Statistical parity at full config-2 scale: recall@20 / NDCG@20 on the
+    held-out split after `epochs` epochs of the throughput kernel (B = 1024
+    pairs in flight) against the deterministic kernel, which is bit-identical
+    to the reference's single thread (BASELINE config 2: 20 epochs)."""
+    from paper_2304_07334_b200 import LossParams, TrainingConfig
+    from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+    tr, te, sp = make_dataset(cfg_name)
+    out = {"what": "quality", "config": cfg_name, "epochs": epochs}
+    for mode in ("hogwild", "exact"):
+        S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0))
+        T = init_matrix(tr.num_items, sp.dim, InitSpec(seed=0))
+        m = DeviceModel(S.values, T.values)
+        t0 = time.perf_counter()
+        losses = []
+        for e in range(epochs):
+            u, i = epoch_pairs(tr, shuffle_seed(0, e))
+            du, di = m.upload_pairs(u, i)
+            p = m.params(n_neg=sp.negatives, lr=sp.learning_rate, l2=0.0, mu=sp.mu,
+                         theta=sp.theta, cosine=True,
+                         mode=N.MODE_HOGWILD if mode == "hogwild" else N.MODE_EXACT,
+                         stream_base=epoch_stream(0, e), window=sp.batch)
+            m.counters.reset()
+            m.train_range(du, di, 0, len(u), p)
+            losses.append(m.counters.read().loss / len(u))
+        dt = time.perf_counter() - t0
+        cfg = TrainingConfig(emb_dim=sp.dim, num_negatives=sp.negatives,
+                             loss=LossParams(mu=sp.mu, theta=sp.theta))
+        r = evaluate_device(m, S, T, tr, te, cfg, k=20)
+        out[mode] = {"recall@20": r.recall_at_k, "ndcg@20": r.ndcg_at_k,
+                     "first_loss": losses[0], "last_loss": losses[-1], "train_seconds": dt}
+    out["recall_gap"] = abs(out["hogwild"]["recall@20"] - out["exact"]["recall@20"])
+    print(json.dumps(out), flush=True)
+
+
 def evaluation(cfg_name):
     tr, te, sp = make_dataset(cfg_name)
     S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0))
@@ -120,6 +155,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "exact":
         exact("c1", 20000)
         exact("c2", 50000)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "quality":
+        quality()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "agg":
         agg_hogwild()
