@@ -133,6 +133,44 @@ def quality(cfg_name="c2", epochs=20):
     print(json.dumps(out), flush=True)
 
 
+def agg_quality(cfg_name="c2", K=128, NN=64, H=100, mb=32, epochs=5):
+    """H-ACCL parity at full scale: aggregated-query recall@20 after `epochs`
+    epochs, throughput aggregator (4096-pair steps) vs the deterministic one
+    (bit-identical to the reference's single thread)."""
+    from paper_2304_07334_b200 import LossParams, TrainingConfig
+    from paper_2304_07334_b200.config import AggregatorConfig
+    from paper_2304_07334_b200.device import DeviceAggregator
+    tr, te, sp = make_dataset(cfg_name)
+    acfg = AggregatorConfig(enabled=True, gamma=0.5, max_history=H, mini_batch_size=mb)
+    out = {"what": "agg_quality", "config": f"{cfg_name}-shaped K{K} N{NN} H{H} mb{mb}",
+           "epochs": epochs}
+    for mode in ("hogwild", "exact"):
+        S = init_matrix(tr.num_users, K, InitSpec(seed=0))
+        T = init_matrix(tr.num_items, K, InitSpec(seed=0))
+        m = DeviceModel(S.values, T.values)
+        agg = DeviceAggregator(np.eye(K, dtype=np.float32), tr, acfg, sp.learning_rate, m.device)
+        t0 = time.perf_counter()
+        for e in range(epochs):
+            u, i = epoch_pairs(tr, shuffle_seed(0, e))
+            du, di = m.upload_pairs(u, i)
+            p = m.params(n_neg=NN, lr=sp.learning_rate, l2=0.0, mu=sp.mu, theta=sp.theta,
+                         cosine=True,
+                         mode=N.MODE_HOGWILD if mode == "hogwild" else N.MODE_EXACT,
+                         stream_base=epoch_stream(0, e), window=4096)
+            m.counters.reset()
+            agg.reset_epoch()
+            m.train_range(du, di, 0, len(u), p, agg=agg)
+            loss = m.counters.read().loss / len(u)
+        dt = time.perf_counter() - t0
+        cfg = TrainingConfig(emb_dim=K, num_negatives=NN, loss=LossParams(mu=sp.mu, theta=sp.theta),
+                             aggregator=acfg)
+        r = evaluate_device(m, S, T, tr, te, cfg, weights=agg.W, k=20)
+        out[mode] = {"recall@20": r.recall_at_k, "ndcg@20": r.ndcg_at_k, "last_loss": loss,
+                     "train_seconds": dt}
+    out["recall_gap"] = abs(out["hogwild"]["recall@20"] - out["exact"]["recall@20"])
+    print(json.dumps(out), flush=True)
+
+
 def evaluation(cfg_name):
     tr, te, sp = make_dataset(cfg_name)
     S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0))
@@ -155,6 +193,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "exact":
         exact("c1", 20000)
         exact("c2", 50000)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "agg_quality":
+        agg_quality()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "quality":
         quality()
