@@ -25,7 +25,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 EXTRA = {"heat_exact.cu": ["--fmad=false"], "heat_exact_spec.cu": ["--fmad=false"]}
 SOURCES = ["heat_capi.cu", "heat_sample.cu", "heat_exact.cu", "heat_exact_spec.cu",
            "heat_hogwild.cu", "heat_hogwild_staged.cu",
-           "heat_hogwild_resident.cu", "heat_agg_hogwild.cu", "heat_shard.cu",
+           "heat_hogwild_resident.cu", "heat_hogwild_multi.cu", "heat_agg_hogwild.cu", "heat_shard.cu",
            "heat_eval.cu", "heat_host.cpp"]
 
 

@@ -485,7 +485,17 @@ cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *worke
         cudaError_t e = launch_hogwild_resident(a, stream, workers_out);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
-    if (aligned && (!impl || impl[0] == 's' || impl[0] == 't' || (impl[0] == 'r' && impl[1] == 'e'))) {
+    // several warps per pair (large N, K <= 64: the pair does not fit the
+    // resident kernel, and one warp per pair leaves the SMs underoccupied)
+    const bool multi_forced = impl && impl[0] == 'm';
+    const bool multi_default = (!impl || (impl[0] == 'r' && impl[1] == 'e')) &&
+                               (a.K == 32 || a.K == 64) && a.N + 1 > 256;
+    if (aligned && (multi_forced || multi_default)) {
+        cudaError_t e = launch_hogwild_multi(a, stream, workers_out);
+        if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
+    }
+    if (aligned && (!impl || impl[0] == 's' || impl[0] == 't' || impl[0] == 'm' ||
+                    (impl[0] == 'r' && impl[1] == 'e'))) {
         cudaError_t e = launch_hogwild_staged(a, stream, workers_out, impl && impl[0] == 't');
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }

@@ -53,6 +53,7 @@ struct HogwildArgs {
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_resident(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
+cudaError_t launch_hogwild_multi(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t stream, int *workers_out,
                                   bool bulk);
 
