@@ -59,8 +59,12 @@ __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
 #define MULTI_UREG 0  // measured: registers cost residency more than the LDS saved
 #endif
 
+#ifndef MULTI_MINB
+#define MULTI_MINB 5  // measured: 5 CTAs (20 warps) per SM, registers <= 102
+#endif
+
 template <int K, int NW, int D>
-__global__ void __launch_bounds__(32 * NW)
+__global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     hogwild_multi(HogwildArgs a, FastMod fm, int n_workers, int snap_cap) {
     using G = MwGeom<K>;
     constexpr int VW = G::VW;
@@ -341,7 +345,8 @@ __global__ void __launch_bounds__(32 * NW)
 
 template <int K, int NW, int D>
 static cudaError_t launch_multi_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
-    const int snap_cap = 16;
+    int snap_cap = 8;  // measured on c3: 8 (77.6 M) > 16 (72 M) at 5 CTAs per SM
+    if (const char *e = getenv("HEAT_SNAP")) snap_cap = atoi(e) > 0 ? atoi(e) : snap_cap;
     const MwLayout L = mw_layout<K, D>(snap_cap);
     const size_t smem = L.per_warp * NW;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
