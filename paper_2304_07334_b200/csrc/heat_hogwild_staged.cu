@@ -104,8 +104,12 @@ __device__ __forceinline__ void red_add_vec(float *p, const float (&d)[VW]) {
 #define UREG_MAX 128
 #endif
 
+#ifndef STAGED_MINB
+#define STAGED_MINB 1
+#endif
+
 template <int K, int D, bool F64, bool BULK, int LPR>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(32, STAGED_MINB)
     hogwild_staged(HogwildArgs a, FastMod fm, int n_workers, int snap_cap, int cross) {
     using G = StGeom<K, LPR>;
     constexpr int VW = G::VW;
