@@ -1047,3 +1047,38 @@ def test_multi_warp_kernel_vs_oracle(torch_cuda, monkeypatch, K, N, window):
         assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
     else:
         assert abs(c.loss - r.loss) <= 0.02 * abs(r.loss)
+
+
+@pytest.mark.parametrize("K,N", [(64, 300), (128, 300), (32, 40)])
+def test_delta_mode_every_kernel_family(torch_cuda, K, N):
+    """DELTA mode (the multi-GPU step) through each throughput kernel family
+    the dispatcher picks (multi-warp for K 64 / N 300, staged for K 128,
+    resident for K 32 / N 40): two logical ranks on one GPU through the
+    pipelined driver keep bit-identical item replicas and train every pair."""
+    import torch
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.parallel import PipelinedShardTrainer, run_loopback
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_clustered
+    train, _ = make_clustered(600, 3000, 8, 30, seed=5)
+    S = init_matrix(600, K, InitSpec(seed=1)).values
+    T = init_matrix(3000, K, InitSpec(seed=2)).values
+    ranks = [PipelinedShardTrainer(DeviceModel(S, T), 2, r) for r in range(2)]
+    u, i = epoch_pairs(train, shuffle_seed(0, 0))
+    gens = []
+    for tr in ranks:
+        p = tr.model.params(n_neg=N, lr=0.05, l2=0.0, mu=1.0, theta=0.3, cosine=True,
+                            mode=NN.MODE_DELTA, stream_base=epoch_stream(0, 0), window=128)
+        tr.model.counters.reset()
+        gens.append(tr.epoch_pipeline(u, i, p, 512))
+    run_loopback(gens)
+    torch.cuda.synchronize()
+    cs = [tr.model.counters.read() for tr in ranks]
+    assert sum(c.pairs for c in cs) == len(u)
+    assert sum(st.entries for st in ranks[0].stats) >= len(u)
+    T0 = ranks[0].model.T.cpu().numpy()
+    assert ranks[1].model.T.cpu().numpy().tobytes() == T0.tobytes()
+    assert np.isfinite(T0).all() and not np.array_equal(T0, T)
