@@ -311,7 +311,7 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         a.start = start; a.stop = stop;
         a.K = p->dim; a.N = p->n_neg; a.cosine = p->use_cosine;
         a.lr = (float)p->lr; a.l2 = (float)p->l2; a.mu = p->mu; a.theta = p->theta;
-        a.s0 = p->stream_base; a.num_items = t_rows; a.ctr = counters;
+        a.s0 = p->stream_base; a.num_items = t_rows; a.ctr = counters; a.s_rows = s_rows;
         a.window = p->window; a.fp64 = p->flags & 1;
         a.delta_ids = p->mode == HEAT_MODE_DELTA ? delta_ids : nullptr;
         a.delta_rows = delta_rows; a.delta_count = delta_count;

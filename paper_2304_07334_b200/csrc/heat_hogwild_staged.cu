@@ -104,12 +104,8 @@ __device__ __forceinline__ void red_add_vec(float *p, const float (&d)[VW]) {
 #define UREG_MAX 128
 #endif
 
-#ifndef STAGED_MINB
-#define STAGED_MINB 1
-#endif
-
 template <int K, int D, bool F64, bool BULK, int LPR>
-__global__ void __launch_bounds__(32, STAGED_MINB)
+__global__ void __launch_bounds__(32)
     hogwild_staged(HogwildArgs a, FastMod fm, int n_workers, int snap_cap, int cross) {
     using G = StGeom<K, LPR>;
     constexpr int VW = G::VW;
@@ -612,10 +608,12 @@ cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t st, int *wo
                                   bool bulk) {
     // stages in flight per warp: enough rows in flight to cover L2 latency,
     // few enough that the window's workers fit on the SMs
-    // measured: K = 128 (two lanes per row) runs best with a single stage in
-    // flight per warp: 15 warps per SM hide the latency better than 9 warps
-    // with two stages each (c4 +12 %, c5 +4 %)
-    int D = a.K <= 32 ? 4 : (a.K >= 128 ? 1 : 2);
+    // measured, K = 128 (two lanes per row): with L2-resident tables one stage
+    // in flight per warp wins (15 warps per SM hide the latency; c4 +12 %);
+    // when the tables live in HBM two stages win (full-size c5: 12.85 M vs
+    // 10.90 M samples/s): the rows in flight, not the warps, bound it there
+    const double footprint = (double)(a.num_items + a.s_rows) * a.K * sizeof(float);
+    int D = a.K <= 32 ? 4 : (a.K >= 128 && footprint < 96e6 ? 1 : 2);
     if (const char *e = getenv("HEAT_STAGES")) D = atoi(e) > 0 ? atoi(e) : D;
     // cross-pair prefetch halves the workers a window allows; measured slower
     int cross = 0;

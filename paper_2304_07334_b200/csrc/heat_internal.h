@@ -31,6 +31,7 @@ struct HogwildArgs {
     heat_counters *ctr;
     int window;
     int fp64;
+    int64_t s_rows = 0;  // user table rows (footprint heuristics)
     // delta mode (multi-GPU): item updates logged instead of applied
     int32_t *delta_ids;
     float *delta_rows;
