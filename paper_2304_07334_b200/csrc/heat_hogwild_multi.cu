@@ -23,22 +23,28 @@
 
 namespace heat {
 
-template <int K>
+// LPR lanes per row (2 for K = 128: 16-row stages, each lane half a row,
+// half-row segments padded apart so a quarter-warp reads distinct banks)
+template <int K, int LPR>
 struct MwGeom {
-    static constexpr int SLOTF = K + 4;              // padded row slot (floats)
+    static constexpr int HALF = K / LPR;             // columns per lane segment
+    static constexpr int SEGF = HALF + 4;            // padded segment (floats)
+    static constexpr int SLOTF = LPR * SEGF;         // padded row slot (floats)
+    static constexpr int SR = 32 / LPR;              // rows per stage
     static constexpr int CH = K / 4;                 // 16-byte chunks per row
     static constexpr int VW = K >= 32 ? K / 32 : 1;  // floats per lane in row-wide ops
     static constexpr int RPI = 32 / CH > 0 ? 32 / CH : 1;  // rows per copy instruction
-    static constexpr int NI = 32 / RPI;                    // copy instructions per stage
+    static constexpr int NI = SR / RPI > 0 ? SR / RPI : 1; // copy instructions per stage
+    __host__ __device__ static constexpr int pcol(int c) { return c + (c / HALF) * 4; }
 };
 
 struct MwLayout {
     size_t ids, ring, urow, snap, ents, per_warp;
 };
 
-template <int K, int D>
+template <int K, int D, int LPR>
 __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
-    using G = MwGeom<K>;
+    using G = MwGeom<K, LPR>;
     MwLayout L;
     size_t o = 0;
     auto take = [&](size_t b) {
@@ -46,9 +52,9 @@ __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
         o = at + b;
         return at;
     };
-    L.ids = take(sizeof(int32_t) * 32 * D);
-    L.ring = take(sizeof(float) * G::SLOTF * 32 * D);
-    L.urow = take(sizeof(float) * K);
+    L.ids = take(sizeof(int32_t) * G::SR * D);
+    L.ring = take(sizeof(float) * G::SLOTF * G::SR * D);
+    L.urow = take(sizeof(float) * G::SLOTF);
     L.snap = take(sizeof(float) * K * snap_cap);
     L.ents = take(sizeof(WriteEntry) * snap_cap);
     L.per_warp = (o + 127) & ~size_t(127);
@@ -63,14 +69,17 @@ __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
 #define MULTI_MINB 5  // measured: 5 CTAs (20 warps) per SM, registers <= 102
 #endif
 
-template <int K, int NW, int D>
+template <int K, int NW, int D, int LPR>
 __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     hogwild_multi(HogwildArgs a, FastMod fm, int n_workers, int snap_cap) {
-    using G = MwGeom<K>;
+    using G = MwGeom<K, LPR>;
     constexpr int VW = G::VW;
+    constexpr int SR = G::SR;
     extern __shared__ __align__(128) unsigned char sm[];
-    const MwLayout Lo = mw_layout<K, D>(snap_cap);
+    const MwLayout Lo = mw_layout<K, D, LPR>(snap_cap);
     const int lane = threadIdx.x & 31;
+    const int rr = lane / LPR, hs = lane % LPR;  // my row in a stage, my column segment
+    const bool lead = hs == 0;                   // the lane that accounts for the row
     const int w = threadIdx.x >> 5;
     unsigned char *mine = sm + (size_t)w * Lo.per_warp;
     int32_t *ids = reinterpret_cast<int32_t *>(mine + Lo.ids);
@@ -83,7 +92,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     const int64_t npairs = a.stop - a.start;
     if (gw >= n_workers || gw >= npairs) return;  // uniform per CTA
     const int N = a.N;
-    const int nb = (N + 1 + 31) / 32;              // stages per pair
+    const int nb = (N + 1 + SR - 1) / SR;          // stages per pair
     const int nbw = nb > w ? (nb - w + NW - 1) / NW : 0;  // this warp's stages
     const double wneg = a.mu * (1.0 / (double)N);
     const float theta_f = (float)a.theta;
@@ -113,25 +122,26 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
             }
             const int s = w + NW * issued;
             const int slot = issued % D;
-            const int r = s * 32 + lane;
+            const int r = s * SR + rr;
             uint32_t id = (uint32_t)pos;
             if (r > 0 && r <= N)
                 id = (uint32_t)fm.mod(mix64(a.s0 + (key * (uint64_t)N + (uint64_t)r) * kGamma));
             if (r > N) id = 0;
-            ids[slot * 32 + lane] = (int32_t)id;
-            const int nvalid = min(32, N + 1 - s * 32);
-            float *dst = ring + (size_t)slot * 32 * G::SLOTF + my_rsub * G::SLOTF + my_ch * 4;
+            if (lead) ids[slot * SR + rr] = (int32_t)id;
+            const int nvalid = min(SR, N + 1 - s * SR);
+            float *dst = ring + (size_t)slot * SR * G::SLOTF + my_rsub * G::SLOTF +
+                         G::pcol(my_ch * 4);
             const float *srcb = a.T + my_ch * 4;
 #pragma unroll
             for (int i = 0; i < G::NI; ++i) {
                 const int row = i * G::RPI + my_rsub;
-                const uint32_t rid = __shfl_sync(0xffffffffu, id, row & 31);
+                const uint32_t rid = __shfl_sync(0xffffffffu, id, (row * LPR) & 31);
                 if (row < nvalid)
                     cp_async16_hint(dst + i * G::RPI * G::SLOTF, srcb + (size_t)rid * K, pol);
             }
             if (issued == 0)  // the user row rides with the warp's first stage
                 for (int ch = lane; ch < G::CH; ch += 32)
-                    cp_async16(urow + ch * 4, a.S + u * K + ch * 4);
+                    cp_async16(urow + G::pcol(ch * 4), a.S + u * K + ch * 4);
             cp_async_commit();
             ++issued;
         };
@@ -141,7 +151,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
 #pragma unroll
         for (int i = 0; i < VW; ++i) ug[i] = uu[i] = 0.f;
         constexpr bool UREG = MULTI_UREG != 0;  // user row in registers (else broadcast LDS)
-        float2 ureg[UREG ? K / 2 : 1];
+        float2 ureg[UREG ? G::HALF / 2 : 1];
         double ss = 0.0, rs = 0.0;
         float rss = 0.f;
         double hinge = 0.0, sim_p = 0.0;
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                 float sp = 0.f;
 #pragma unroll
                 for (int v = 0; v < VW; ++v) {
-                    uu[v] = urow[lane * VW + v];
+                    uu[v] = urow[G::pcol(lane * VW + v)];
                     sp = fmaf(uu[v], uu[v], sp);
                 }
 #pragma unroll
@@ -212,21 +222,22 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                 rss = ss > 0.0 ? rsqrtf(sp) : 0.f;
                 if constexpr (UREG) {
 #pragma unroll
-                    for (int k = 0; k < K; k += 4) {
-                        const float4 w4 = *reinterpret_cast<const float4 *>(urow + k);
+                    for (int k = 0; k < G::HALF; k += 4) {
+                        const float4 w4 = *reinterpret_cast<const float4 *>(urow + hs * G::SEGF + k);
                         ureg[k / 2] = make_float2(w4.x, w4.y);
                         ureg[k / 2 + 1] = make_float2(w4.z, w4.w);
                     }
                 }
             }
-            const int r = s * 32 + lane;
+            const int r = s * SR + rr;
             const bool valid = r <= N;
-            const float *row = ring + ((size_t)slot * 32 + lane) * G::SLOTF;
+            const float *row = ring + ((size_t)slot * SR + rr) * G::SLOTF + hs * G::SEGF;
+            const float *uph = urow + hs * G::SEGF;
             float2 ta = make_float2(0.f, 0.f), tb = ta, sa = ta, sb = ta;
             float2 tc = ta, td = ta, sc = ta, sd = ta;
             if (valid) {
 #pragma unroll
-                for (int k = 0; k < K; k += 4) {
+                for (int k = 0; k < G::HALF; k += 4) {
                     const float4 v = *reinterpret_cast<const float4 *>(row + k);
                     const float2 vlo = make_float2(v.x, v.y), vhi = make_float2(v.z, v.w);
                     float2 wlo, whi;
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                         wlo = ureg[k / 2];
                         whi = ureg[k / 2 + 1];
                     } else {
-                        const float4 w4 = *reinterpret_cast<const float4 *>(urow + k);
+                        const float4 w4 = *reinterpret_cast<const float4 *>(uph + k);
                         wlo = make_float2(w4.x, w4.y);
                         whi = make_float2(w4.z, w4.w);
                     }
@@ -251,8 +262,12 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                     }
                 }
             }
-            const float ttf = ((ta.x + ta.y) + (tb.x + tb.y)) + ((tc.x + tc.y) + (td.x + td.y));
-            const float stf = ((sa.x + sa.y) + (sb.x + sb.y)) + ((sc.x + sc.y) + (sd.x + sd.y));
+            float ttf = ((ta.x + ta.y) + (tb.x + tb.y)) + ((tc.x + tc.y) + (td.x + td.y));
+            float stf = ((sa.x + sa.y) + (sb.x + sb.y)) + ((sc.x + sc.y) + (sd.x + sd.y));
+            if constexpr (LPR == 2) {  // the row's two column segments
+                ttf += __shfl_xor_sync(0xffffffffu, ttf, 1);
+                stf += __shfl_xor_sync(0xffffffffu, stf, 1);
+            }
             // similarity and loss weight (trainer.py:184-221)
             bool write = false;
             double wt = 0.0;
@@ -263,7 +278,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                     if (ss <= 0.0 || ttf <= 0.f) {
                         degenerate = true;
                         sim = 0.0;
-                        ++degen;
+                        if (lead) ++degen;
                     } else {
                         const float sf = stf * rss * rsqrtf(ttf);
                         sim = (double)sf;
@@ -277,23 +292,24 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                     write = !(a.cosine && degenerate) || a.l2 != 0.f;
                 } else {
                     if (sim - a.theta > 0.0) {
-                        hinge += sim - a.theta;
+                        if (lead) hinge += sim - a.theta;
                         wt = wneg;
-                        if (wt != 0.0) ++active;
+                        if (wt != 0.0 && lead) ++active;
                     }
                     write = (wt != 0.0 && !(a.cosine && degenerate)) || (wt == 0.0 && a.l2 != 0.f);
                 }
             }
-            unsigned m = __ballot_sync(0xffffffffu, write);
+            unsigned m = __ballot_sync(0xffffffffu, write && lead);
             while (m) {
                 if (cnt == snap_cap) spill();
                 const int src = __ffs(m) - 1;
                 m &= m - 1;
-                const float *srow = ring + ((size_t)slot * 32 + src) * G::SLOTF;
+                const float *srow = ring + ((size_t)slot * SR + src / LPR) * G::SLOTF;
 #pragma unroll
-                for (int v = 0; v < VW; ++v) snap[cnt * K + lane * VW + v] = srow[lane * VW + v];
+                for (int v = 0; v < VW; ++v)
+                    snap[cnt * K + lane * VW + v] = srow[G::pcol(lane * VW + v)];
                 if (lane == src)
-                    ents[cnt] = WriteEntry{(double)ttf, (double)stf, wt, ids[slot * 32 + src], 0};
+                    ents[cnt] = WriteEntry{(double)ttf, (double)stf, wt, ids[slot * SR + src / LPR], 0};
                 ++cnt;
             }
             __syncwarp();
@@ -343,14 +359,14 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     }
 }
 
-template <int K, int NW, int D>
+template <int K, int NW, int D, int LPR>
 static cudaError_t launch_multi_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
     int snap_cap = 8;  // measured on c3: 8 (77.6 M) > 16 (72 M) at 5 CTAs per SM
     if (const char *e = getenv("HEAT_SNAP")) snap_cap = atoi(e) > 0 ? atoi(e) : snap_cap;
-    const MwLayout L = mw_layout<K, D>(snap_cap);
+    const MwLayout L = mw_layout<K, D, LPR>(snap_cap);
     const size_t smem = L.per_warp * NW;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
-    auto kern = hogwild_multi<K, NW, D>;
+    auto kern = hogwild_multi<K, NW, D, LPR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -375,15 +391,15 @@ static cudaError_t launch_multi_k(const HogwildArgs &a, cudaStream_t st, int *wo
     return cudaGetLastError();
 }
 
-template <int K>
+template <int K, int LPR>
 static cudaError_t launch_multi_nw(const HogwildArgs &a, cudaStream_t st, int *workers_out,
                                    int nw, int d) {
-    if (nw == 2) return d == 1 ? launch_multi_k<K, 2, 1>(a, st, workers_out)
-                               : launch_multi_k<K, 2, 2>(a, st, workers_out);
-    if (nw == 8) return d == 1 ? launch_multi_k<K, 8, 1>(a, st, workers_out)
-                               : launch_multi_k<K, 8, 2>(a, st, workers_out);
-    return d == 1 ? launch_multi_k<K, 4, 1>(a, st, workers_out)
-                  : launch_multi_k<K, 4, 2>(a, st, workers_out);
+    if (nw == 2) return d == 1 ? launch_multi_k<K, 2, 1, LPR>(a, st, workers_out)
+                               : launch_multi_k<K, 2, 2, LPR>(a, st, workers_out);
+    if (nw == 8) return d == 1 ? launch_multi_k<K, 8, 1, LPR>(a, st, workers_out)
+                               : launch_multi_k<K, 8, 2, LPR>(a, st, workers_out);
+    return d == 1 ? launch_multi_k<K, 4, 1, LPR>(a, st, workers_out)
+                  : launch_multi_k<K, 4, 2, LPR>(a, st, workers_out);
 }
 
 cudaError_t launch_hogwild_multi(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
@@ -392,8 +408,9 @@ cudaError_t launch_hogwild_multi(const HogwildArgs &a, cudaStream_t st, int *wor
     if (const char *e = getenv("HEAT_MULTI_NW")) nw = atoi(e);
     if (const char *e = getenv("HEAT_MULTI_D")) d = atoi(e) == 2 ? 2 : 1;
     switch (a.K) {
-    case 32: return launch_multi_nw<32>(a, st, workers_out, nw, d);
-    case 64: return launch_multi_nw<64>(a, st, workers_out, nw, d);
+    case 32: return launch_multi_nw<32, 1>(a, st, workers_out, nw, d);
+    case 64: return launch_multi_nw<64, 1>(a, st, workers_out, nw, d);
+    case 128: return launch_multi_nw<128, 2>(a, st, workers_out, nw, d);
     default: return cudaErrorNotSupported;
     }
 }

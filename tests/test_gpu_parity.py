@@ -1013,7 +1013,8 @@ def test_c2_recall_parity_throughput_vs_deterministic(torch_cuda):
     assert abs(rec[N.MODE_HOGWILD] - rec[N.MODE_EXACT]) <= 0.005, rec
 
 
-@pytest.mark.parametrize("K,N,window", [(64, 500, 1), (32, 300, 1), (64, 100, 1), (64, 500, 64)])
+@pytest.mark.parametrize("K,N,window", [(64, 500, 1), (32, 300, 1), (64, 100, 1), (64, 500, 64),
+                                        (128, 300, 1), (128, 64, 1), (128, 500, 64)])
 def test_multi_warp_kernel_vs_oracle(torch_cuda, monkeypatch, K, N, window):
     """The several-warps-per-pair kernel (csrc/heat_hogwild_multi.cu, the
     default for K <= 64 with N + 1 > 256): window 1 tracks the oracle within
