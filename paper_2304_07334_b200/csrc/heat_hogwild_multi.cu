@@ -54,7 +54,8 @@ __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
     };
     L.ids = take(sizeof(int32_t) * G::SR * D);
     L.ring = take(sizeof(float) * G::SLOTF * G::SR * D);
-    L.urow = take(sizeof(float) * G::SLOTF);
+    // (K floats when LPR = 1: the padding would cost c3 its fifth CTA per SM)
+    L.urow = take(sizeof(float) * (LPR == 1 ? K : G::SLOTF));
     L.snap = take(sizeof(float) * K * snap_cap);
     L.ents = take(sizeof(WriteEntry) * snap_cap);
     L.per_warp = (o + 127) & ~size_t(127);
