@@ -1083,3 +1083,42 @@ def test_delta_mode_every_kernel_family(torch_cuda, K, N):
     T0 = ranks[0].model.T.cpu().numpy()
     assert ranks[1].model.T.cpu().numpy().tobytes() == T0.tobytes()
     assert np.isfinite(T0).all() and not np.array_equal(T0, T)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_properties(torch_cuda, cfg):
+    """BASELINE.json's full sizes (c4 53 k x 92 k x 128, N 1000; c5 10 M x 2 M
+    x 128 tables with a 2 % user sample), through size-independent
+    properties: every pair trained exactly once per epoch, the loss finite and
+    falling, the tables finite, and user rows that own no pair bit-identical
+    to their initial values (sparse updates, test_trainer.py:94-107)."""
+    import torch
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    kw = {"sample_users": 0.02} if cfg == "c5" else {}
+    tr, _, sp = make_dataset(cfg, **kw)
+    S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0)).values
+    T = init_matrix(tr.num_items, sp.dim, InitSpec(seed=0)).values
+    m = DeviceModel(S, T)
+    losses = []
+    for e in range(2):
+        u, i = epoch_pairs(tr, shuffle_seed(0, e))
+        du, di = m.upload_pairs(u, i)
+        p = m.params(n_neg=sp.negatives, lr=sp.learning_rate, l2=0.0, mu=sp.mu, theta=sp.theta,
+                     cosine=True, mode=N.MODE_HOGWILD, stream_base=epoch_stream(0, e),
+                     window=sp.batch)
+        m.counters.reset()
+        m.train_range(du, di, 0, len(u), p)
+        c = m.counters.read()
+        assert c.pairs == tr.num_pairs and np.isfinite(c.loss)
+        losses.append(c.loss / c.pairs)
+    assert losses[1] < losses[0]
+    idle = np.flatnonzero(np.diff(tr.offsets) == 0)  # users without a pair
+    S2 = m.S[torch.from_numpy(idle).cuda()].cpu().numpy() if len(idle) else None
+    if S2 is not None:
+        assert S2.tobytes() == S[idle].tobytes()
+    assert bool(torch.isfinite(m.S).all()) and bool(torch.isfinite(m.T).all())
