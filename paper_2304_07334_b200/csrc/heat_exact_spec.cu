@@ -42,8 +42,8 @@ namespace heat {
 #define DDIV __ddiv_rn
 #define DSQRT __dsqrt_rn
 
-constexpr int kSpecWarps = 16;
-constexpr int kSpecMaxRows = 256;  // N+1 <= 256
+constexpr int kSpecWarps = 16;     // most warps per CTA (fewer when the rows are wide)
+constexpr int kSpecMaxRows = 1024; // N+1 <= 1024: a lane's row mask is one 32-bit word
 constexpr int kSpecMaxK = 256;
 constexpr int kSpecChunk = 32767;  // pairs per launch (int16 stamps never wrap)
 
@@ -58,22 +58,24 @@ struct SpecWarp {  // per-warp shared state between speculate and commit
 struct SpecLayout {
     int wcap;  // precomputed T-row writes per warp
     int smem_stamps;
+    int warps;
     size_t off_sw, off_ubuf, off_tts, off_sts, off_sims, off_nids, off_act, off_wid, off_new,
         off_stamps, total;
 };
 
 __host__ __device__ inline SpecLayout spec_layout(int K, int N, int64_t rows_total, int wcap,
-                                                  bool smem_stamps) {
+                                                  bool smem_stamps, int warps = kSpecWarps) {
     SpecLayout L;
     L.wcap = wcap;
     L.smem_stamps = smem_stamps ? 1 : 0;
+    L.warps = warps;
     size_t o = 32;  // token, running loss
     auto take = [&](size_t b) {
         size_t at = (o + 15) & ~size_t(15);
         o = at + b;
         return at;
     };
-    const size_t W = kSpecWarps;
+    const size_t W = (size_t)warps;
     L.off_sw = take(sizeof(SpecWarp) * W);
     L.off_ubuf = take(8 * W * K);
     L.off_tts = take(8 * W * N);
@@ -407,7 +409,8 @@ __global__ void __launch_bounds__(32 * kSpecWarps, 1)
     };
 
     unsigned long long t_spec = 0, t_wait = 0, t_commit = 0, n_part = 0, n_full = 0, n_pairs = 0;
-    for (int64_t p = start + w; p < stop; p += kSpecWarps) {
+    const int nwarps = Lo.warps;
+    for (int64_t p = start + w; p < stop; p += nwarps) {
         long long c_a = clock64();
         speculate(p, 0u, true);
         long long c_b = clock64();
@@ -518,13 +521,18 @@ __global__ void __launch_bounds__(32 * kSpecWarps, 1)
 }
 
 static SpecLayout pick_layout(int K, int N, int64_t rows_total) {
+    // most speculating warps first (16 for c1/c2), then stamps in shared
+    // memory, then the widest precompute buffer; wide pairs (c3/c4: N+1 up to
+    // 1024) fall back to fewer warps with stamps in global memory
     const size_t cap = 220 * 1024;
-    for (int smem_stamps = 1; smem_stamps >= 0; --smem_stamps)
-        for (int wcap = 16; wcap >= 2; wcap /= 2) {
-            SpecLayout L = spec_layout(K, N, rows_total, wcap, smem_stamps != 0);
-            if (L.total <= cap) return L;
-        }
-    return spec_layout(K, N, rows_total, 2, false);
+    const int warp_opts[] = {16, 12, 8, 6, 4};
+    for (int warps : warp_opts)
+        for (int smem_stamps = 1; smem_stamps >= 0; --smem_stamps)
+            for (int wcap = 16; wcap >= 2; wcap /= 2) {
+                SpecLayout L = spec_layout(K, N, rows_total, wcap, smem_stamps != 0, warps);
+                if (L.total <= cap) return L;
+            }
+    return spec_layout(K, N, rows_total, 2, false, 4);
 }
 
 void exact_spec_stats(unsigned long long *out, bool reset) {
@@ -537,7 +545,7 @@ void exact_spec_stats(unsigned long long *out, bool reset) {
 
 bool exact_spec_supported(int K, int N) {
     if (K > kSpecMaxK || N + 1 > kSpecMaxRows) return false;
-    return spec_layout(K, N, 0, 2, false).total <= 220 * 1024;
+    return spec_layout(K, N, 0, 2, false, 4).total <= 220 * 1024;
 }
 
 size_t exact_spec_scratch_bytes(int K, int N, int64_t s_rows, int64_t t_rows) {
@@ -564,7 +572,7 @@ cudaError_t launch_exact_spec(float *S, int64_t s_rows, float *T, int64_t t_rows
             e = cudaMemsetAsync(gstamps, 0xff, (size_t)(s_rows + t_rows) * 4, stream);
             if (e != cudaSuccess) return e;
         }
-        exact_spec_kernel<<<1, 32 * kSpecWarps, L.total, stream>>>(
+        exact_spec_kernel<<<1, 32 * L.warps, L.total, stream>>>(
             S, T, users, items, a, b, K, N, cosine, lr, l2, mu, theta, s0, fm, ctr, snap, gstamps,
             t_rows, s_rows, pair_index, L);
         e = cudaGetLastError();
