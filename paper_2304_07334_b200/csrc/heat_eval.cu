@@ -253,10 +253,24 @@ constexpr int kRbItems = 128;
 #endif
 using TileT = std::conditional_t<EVAL_TILE_F64 != 0, double, float>;
 
+// MMA variant: the 32 x 128 x K product of a tile on the FP64 tensor path
+// (mma.sync m8n8k4 f64; tcgen05 has no binary64 kind), the user matrix and
+// the tile padded so fragment loads are bank-conflict-free, and the scores
+// through shared memory into the same merge.
+template <bool MMA>
+__host__ __device__ constexpr int rb_ldu() { return MMA ? kRbUsers + 4 : kRbUsers; }
+template <bool MMA>
+__host__ __device__ inline int rb_ldt(int K) { return MMA ? K + 4 : K + 1; }
+// tile-score rows padded by 64 B: a quarter-warp's 16-byte stores (two users,
+// four column pairs) land in distinct banks
+constexpr int kRbScoreLd = kRbItems + 8;
+
+template <bool MMA = false>
 __host__ __device__ inline size_t eval_rb_smem_bytes(int K, int k) {
     size_t b = 0;
-    b += align16(sizeof(double) * K * kRbUsers);      // user vectors, transposed
-    b += align16(sizeof(TileT) * kRbItems * (K + 1)); // item tile (padded rows)
+    b += align16(sizeof(double) * K * rb_ldu<MMA>());        // user vectors, transposed
+    b += align16(sizeof(TileT) * kRbItems * rb_ldt<MMA>(K));  // item tile (padded rows)
+    if (MMA) b += align16(sizeof(double) * kRbUsers * kRbScoreLd);  // tile scores
     b += align16(sizeof(double) * kRbUsers * k);     // list scores
     b += align16(sizeof(int32_t) * kRbUsers * k);    // list ids
     b += align16(sizeof(uint32_t) * kRbUsers * 4);   // train-positive mask of the tile
@@ -279,7 +293,7 @@ __global__ void item_norms_kernel(const float *__restrict__ T, int64_t t_rows, i
     rnorm[i] = n > 0.0 ? 1.0 / n : 0.0;
 }
 
-template <int KC>  // K rounded up to a multiple of 4 for the staging loads
+template <int KC, bool MMA>  // KC: K rounded up to a multiple of 4 for the staging loads
 __global__ void __launch_bounds__(256)
     eval_rb_kernel(const void *__restrict__ S, int s_f64, const float *__restrict__ T,
                    int64_t t_rows, int K, const double *__restrict__ inorm_g,
@@ -292,10 +306,14 @@ __global__ void __launch_bounds__(256)
                    double *__restrict__ recall, double *__restrict__ ndcg) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned char *ptr = smem;
+    constexpr int LDU = rb_ldu<MMA>();
+    const int LDT = rb_ldt<MMA>(K);
     double *uT = reinterpret_cast<double *>(ptr);
-    ptr += align16(sizeof(double) * K * kRbUsers);
+    ptr += align16(sizeof(double) * K * LDU);
     TileT *tile = reinterpret_cast<TileT *>(ptr);
-    ptr += align16(sizeof(TileT) * kRbItems * (K + 1));
+    ptr += align16(sizeof(TileT) * kRbItems * LDT);
+    double *tscore = reinterpret_cast<double *>(ptr);  // MMA: [32 users][128 items]
+    if (MMA) ptr += align16(sizeof(double) * kRbUsers * kRbScoreLd);
     double *ls = reinterpret_cast<double *>(ptr);
     ptr += align16(sizeof(double) * kRbUsers * k);
     int32_t *lid = reinterpret_cast<int32_t *>(ptr);
@@ -317,14 +335,14 @@ __global__ void __launch_bounds__(256)
             v = s_f64 ? reinterpret_cast<const double *>(S)[off]
                       : (double)reinterpret_cast<const float *>(S)[off];
         }
-        uT[c * kRbUsers + b] = v;
+        uT[c * LDU + b] = v;
     }
     __syncthreads();
     // user norms, train cursors (shared), list sizes (registers)
     if (tid < kRbUsers) {
         const int b = tid;
         double a = 0.0;
-        for (int c = 0; c < K; ++c) a = fma(uT[c * kRbUsers + b], uT[c * kRbUsers + b], a);
+        for (int c = 0; c < K; ++c) a = fma(uT[c * LDU + b], uT[c * LDU + b], a);
         const double n = sqrt(a);
         unv[b] = n;
         unv[kRbUsers + b] = n > 0.0 ? 1.0 / n : 0.0;
@@ -354,7 +372,7 @@ __global__ void __launch_bounds__(256)
             const int f = tid + q * 256;
             const int r = f / (KC / 4), c = (f % (KC / 4)) * 4;
             if (r < kRbItems && c < K) {
-                TileT *d = tile + r * (K + 1) + c;
+                TileT *d = tile + r * LDT + c;
                 d[0] = pre[q].x; d[1] = pre[q].y; d[2] = pre[q].z; d[3] = pre[q].w;
             }
         }
@@ -388,24 +406,57 @@ __global__ void __launch_bounds__(256)
             if (lane == 0) curv[b] = c0;
         }
         __syncwarp();
-        // 4 users x 4 items of dot products
+        // 4 users x 4 items of dot products per lane
         double acc[4][4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[j][m] = 0.0;
-        const double *ucol = uT + warp * 4;
-        for (int c = 0; c < K; ++c) {
-            const double2 ua = *reinterpret_cast<const double2 *>(ucol + c * kRbUsers);
-            const double2 ub = *reinterpret_cast<const double2 *>(ucol + c * kRbUsers + 2);
-            const double uv[4] = {ua.x, ua.y, ub.x, ub.y};
-            double iv[4];
+        if constexpr (MMA) {
+            // warp w: users 8*(w/2) .. +7, items 64*(w%2) .. +63 as 8 m8n8k4 tiles
+            const int g = lane >> 2, tq = lane & 3;
+            const int ub = warp >> 1, ih = warp & 1;
+            double c0[8], c1[8];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) iv[m] = (double)tile[(lane + 32 * m) * (K + 1) + c];
+            for (int ni = 0; ni < 8; ++ni) c0[ni] = c1[ni] = 0.0;
+            const double *ucol = uT + 8 * ub + g;
+            const TileT *trow = tile + (size_t)(64 * ih + g) * LDT + tq;
+            for (int k0 = 0; k0 < K; k0 += 4) {
+                const double av = ucol[(k0 + tq) * LDU];  // A[user g][k0 + tq]
+#pragma unroll
+                for (int ni = 0; ni < 8; ++ni) {
+                    const double bv = (double)trow[(size_t)8 * ni * LDT + k0];  // B[k][item]
+                    asm volatile(
+                        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+                        "{%0, %1};"
+                        : "+d"(c0[ni]), "+d"(c1[ni])
+                        : "d"(av), "d"(bv));
+                }
+            }
+            double *srow = tscore + (size_t)(8 * ub + g) * kRbScoreLd + 64 * ih + 2 * tq;
+#pragma unroll
+            for (int ni = 0; ni < 8; ++ni)
+                *reinterpret_cast<double2 *>(srow + 8 * ni) = make_double2(c0[ni], c1[ni]);
+            __syncthreads();
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
-                for (int m = 0; m < 4; ++m) acc[j][m] = fma(uv[j], iv[m], acc[j][m]);
+                for (int m = 0; m < 4; ++m)
+                    acc[j][m] = tscore[(warp * 4 + j) * kRbScoreLd + lane + 32 * m];
+        } else {
+            const double *ucol = uT + warp * 4;
+            for (int c = 0; c < K; ++c) {
+                const double2 ua = *reinterpret_cast<const double2 *>(ucol + c * LDU);
+                const double2 ub = *reinterpret_cast<const double2 *>(ucol + c * LDU + 2);
+                const double uv[4] = {ua.x, ua.y, ub.x, ub.y};
+                double iv[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) iv[m] = (double)tile[(lane + 32 * m) * LDT + c];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) acc[j][m] = fma(uv[j], iv[m], acc[j][m]);
+            }
         }
         __syncwarp();
         // merge, one user at a time (items in increasing id order per lane
@@ -521,15 +572,15 @@ static cudaError_t launch_eval_ub(const void *S, int s_f64, const float *T, int6
     return cudaGetLastError();
 }
 
-template <int KC>
+template <int KC, bool MMA>
 static cudaError_t launch_eval_rb(const void *S, int s_f64, const float *T, int64_t t_rows,
                                   int K, const int32_t *users, int64_t n_users,
                                   const int64_t *tr_off, const int32_t *tr_items, int64_t tr_nu,
                                   const int64_t *te_off, const int32_t *te_items, int k,
                                   int cosine, const double *dw, const double *idcg, int32_t *topk,
                                   double *rec, double *nd, cudaStream_t st) {
-    const size_t smem = eval_rb_smem_bytes(K, k);
-    cudaError_t e = cudaFuncSetAttribute(eval_rb_kernel<KC>,
+    const size_t smem = eval_rb_smem_bytes<MMA>(K, k);
+    cudaError_t e = cudaFuncSetAttribute(eval_rb_kernel<KC, MMA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // item norms and reciprocals, once per call (evaluator.py:140-141)
@@ -538,7 +589,7 @@ static cudaError_t launch_eval_rb(const void *S, int s_f64, const float *T, int6
     item_norms_kernel<<<(unsigned)((t_rows + 255) / 256), 256, 0, st>>>(T, t_rows, K, norms,
                                                                         norms + t_rows);
     const int64_t blocks = (n_users + kRbUsers - 1) / kRbUsers;
-    eval_rb_kernel<KC><<<(unsigned)blocks, 256, smem, st>>>(
+    eval_rb_kernel<KC, MMA><<<(unsigned)blocks, 256, smem, st>>>(
         S, s_f64, T, t_rows, K, norms, norms + t_rows, users, n_users, tr_off, tr_items, tr_nu,
         te_off, te_items, k, cosine, dw, idcg, topk, rec, nd);
     return cudaGetLastError();
@@ -552,19 +603,20 @@ cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows
                         cudaStream_t stream) {
     if (n_users == 0) return cudaSuccess;
     const size_t cap = 200 * 1024;
-    const bool rb_ok = K % 4 == 0 && eval_rb_smem_bytes(K, k) <= cap && !getenv("HEAT_EVAL_PLAIN");
-    if (rb_ok && K <= 32)
-        return launch_eval_rb<32>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
-                                  tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
-                                  topk, recall, ndcg, stream);
-    if (rb_ok && K <= 64)
-        return launch_eval_rb<64>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
-                                  tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
-                                  topk, recall, ndcg, stream);
-    if (rb_ok && K <= 128)
-        return launch_eval_rb<128>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
-                                   tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,
-                                   topk, recall, ndcg, stream);
+    const bool mma = !getenv("HEAT_EVAL_FMA") && eval_rb_smem_bytes<true>(K, k) <= cap;
+    const bool rb_ok = K % 4 == 0 && eval_rb_smem_bytes<false>(K, k) <= cap &&
+                       !getenv("HEAT_EVAL_PLAIN");
+#define HEAT_EVAL_RB(KCV)                                                                        \
+    return mma ? launch_eval_rb<KCV, true>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets,  \
+                                           tr_items, tr_num_users, te_offsets, te_items, k,     \
+                                           cosine, dcg_w, idcg, topk, recall, ndcg, stream)     \
+               : launch_eval_rb<KCV, false>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, \
+                                            tr_items, tr_num_users, te_offsets, te_items, k,    \
+                                            cosine, dcg_w, idcg, topk, recall, ndcg, stream)
+    if (rb_ok && K <= 32) HEAT_EVAL_RB(32);
+    if (rb_ok && K <= 64) HEAT_EVAL_RB(64);
+    if (rb_ok && K <= 128) HEAT_EVAL_RB(128);
+#undef HEAT_EVAL_RB
     if (eval_smem_bytes<32>(K, k) <= cap)
         return launch_eval_ub<32>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items,
                                   tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,

@@ -113,10 +113,12 @@ def aggregated_queries(model: DeviceModel, train, weights, gamma: float,
 
 
 def _mean_in_order(values: np.ndarray) -> float:
-    acc = 0.0
-    for v in values.tolist():
-        acc += v
-    return acc
+    """Left-to-right binary64 sum (the reference's running `+=`,
+    evaluator.py:171-178): np.cumsum accumulates sequentially, unlike
+    np.sum's pairwise reduction, so the last prefix is the same float."""
+    if len(values) == 0:
+        return 0.0
+    return float(np.cumsum(np.asarray(values, dtype=np.float64))[-1])
 
 
 def evaluate_device(model: DeviceModel, S, T, train, test, cfg, weights=None, k: int = 20,
