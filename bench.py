@@ -142,6 +142,35 @@ def cpu_baseline(spec, train, S0, T0, sample_pairs: int, threads: int, epoch: in
             "seconds": dt}
 
 
+def cpu_baseline_timed(spec, train, S0, T0, threads: int, seconds: float = 10.0) -> dict:
+    """cpu_baseline over a bounded sample of about `seconds` of host work:
+    a 20 k-pair probe sizes the sample, which then runs over consecutive
+    epochs (tables carried, as a training run would) until it is used up."""
+    from oracle import oracle as O
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.rng import shuffle_seed
+    probe = cpu_baseline(spec, train, S0, T0, 20000, threads)
+    target = max(20000, int(probe["value"] * seconds))
+    S, T = S0.copy(), T0.copy()
+    done, dt, e = 0, 0.0, 0
+    while done < target:
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        n = min(target - done, len(u))
+        t0 = time.perf_counter()
+        O.train_epoch_threads(S, T, u[:n], i[:n], seed=0, epoch=e, num_threads=threads,
+                              n_neg=spec.negatives, lr=spec.learning_rate, mu=spec.mu,
+                              theta=spec.theta)
+        dt += time.perf_counter() - t0
+        done += n
+        e += 1
+    full, rest = divmod(done, train.num_pairs)
+    what = (f"{full} epoch(s) + {rest} pairs" if full else f"first {rest} pairs of epoch 0")
+    return {"value": done / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"{done} pairs = {what} of {spec.name}, {dt:.1f} s "
+                      f"(oracle/heat_oracle.c, {threads} threads, chunk 2048)",
+            "seconds": dt}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -208,6 +237,8 @@ def main():
                     help="sharded path: global pairs between item-delta exchanges "
                          "(default: the config's batch B)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="host seconds for each cpu_baseline sample (16 threads, 1 thread)")
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
@@ -377,12 +408,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        sample = {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 20_000, "c5": 20_000}[spec.name]
-        cpu_baseline(spec, train, S.values, T.values, 20000, threads)  # warm
-        cpu = cpu_baseline(spec, train, S.values, T.values, sample, threads)
+        # about 10 s of host work each (bounded samples of the same workload)
+        cpu = cpu_baseline_timed(spec, train, S.values, T.values, threads, args.cpu_seconds)
         cpu.pop("seconds", None)
-        # the single-thread figure beside it: a smaller sample
-        one = cpu_baseline(spec, train, S.values, T.values, max(2000, sample // 16), 1)
+        # the single-thread figure beside it
+        one = cpu_baseline_timed(spec, train, S.values, T.values, 1, args.cpu_seconds)
         cpu["value_1_thread"] = one["value"]
         cpu["sample_1_thread"] = one["sample"]
 
