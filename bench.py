@@ -46,8 +46,8 @@ def _peaks():
 
 
 class ClockSampler:
-    """SM clock and throttle reasons polled (NVML, every 5 ms) during the
-    timed region; nvidia-smi as a fallback."""
+    """SM clock and throttle reasons polled (NVML, every 2 ms) during the
+    timed region."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
@@ -58,30 +58,39 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _poll(self):
+    def _sample(self):
         import pynvml
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-        while True:
-            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-            try:
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            except Exception:
-                rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            self.samples.append((float(sm), float(mx), int(rs)))
-            if self._stop.wait(0.005):
-                break
+        sm = pynvml.nvmlDeviceGetClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        try:
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.samples.append((float(sm), float(self._max), int(rs)))
+
+    def _poll(self):
+        while not self._stop.wait(0.002):
+            self._sample()
 
     def start(self):
+        """NVML is initialised here, and the first sample taken, before the
+        timed region begins; a thread then polls every 2 ms."""
         try:
-            import pynvml  # noqa: F401
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._sample()
             self._t = threading.Thread(target=self._poll, daemon=True)
             self._t.start()
         except Exception:
             self._t = None
 
     def stop(self) -> dict:
+        if self._t is not None:
+            try:
+                self._sample()  # the state at the end of the timed region
+            except Exception:
+                pass
         self._stop.set()
         if self._t is not None:
             self._t.join(timeout=5)
