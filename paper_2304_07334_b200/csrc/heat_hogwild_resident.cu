@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     constexpr int VW = G::VW;
     extern __shared__ __align__(128) unsigned char sm[];
     float *ring = reinterpret_cast<float *>(sm);
-    float *ubuf = ring + (size_t)G::SLOTF * (a.N + 1);
+    const int rw_all = (a.N + 1 + NB - 1) / NB;  // rows per warp (see below)
+    float *ubuf = ring + (size_t)G::SLOTF * (rw_all * NB);
 
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
@@ -86,13 +87,16 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     const float theta_f = (float)a.theta;
     const bool dmode = a.delta_ids != nullptr;
     const uint64_t pol = policy_evict_last();
-    const int r = w * 32 + lane;  // my row of every pair
-    const bool valid = r <= N;
-    const int nvalid = min(32, N + 1 - w * 32);
+    // rows spread evenly over the NB warps (c2: 26/25/25/25 instead of
+    // 32/32/32/5), so no warp's loads gate the pair barrier for long
+    const int rw = (N + 1 + NB - 1) / NB;      // rows per warp
+    const int r = w * rw + lane;               // my row of every pair
+    const bool valid = lane < rw && r <= N;
+    const int nvalid = max(0, min(rw, N + 1 - w * rw));
     constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;  // rows per copy instruction
     constexpr int NI = 32 / RPI;
     const int my_ch = lane % G::CH, my_rsub = lane / G::CH;
-    float *my_stage = ring + (size_t)w * 32 * G::SLOTF;
+    float *my_stage = ring + (size_t)w * rw * G::SLOTF;
 
     double loss = 0.0;
     long long degen = 0, active = 0, mine = 0;
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
 
 template <int K, int NB>
 static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
-    const size_t smem = rs_smem_bytes<K>(a.N + 1);
+    const size_t smem = rs_smem_bytes<K>(((a.N + 1 + NB - 1) / NB) * NB);
     if (smem > 96 * 1024) return cudaErrorNotSupported;
     auto kern = hogwild_resident<K, NB>;
     cudaError_t e =
