@@ -246,7 +246,7 @@ def main():
                          "reference pipeline)")
     ap.add_argument("--exchange-pairs", type=int, default=0,
                     help="sharded path: global pairs between item-delta exchanges "
-                         "(default: the config's batch B)")
+                         "(default: the config's batch B per rank, i.e. B * world)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="host seconds for each cpu_baseline sample (16 threads, 1 thread)")
@@ -312,7 +312,9 @@ def main():
         trainer = (PipelinedShardTrainer if args.shard_driver == "python"
                    else NativeShardTrainer)(model, world, rank)
         host_pairs = [epoch_pairs(train, shuffle_seed(0, e)) for e in range(total_epochs)]
-        exchange_pairs = args.exchange_pairs or spec.batch
+        # global step = B pairs per rank (each GPU keeps the config's batch
+        # between exchanges, as a data-parallel batch of B per GPU)
+        exchange_pairs = args.exchange_pairs or spec.batch * world
 
         def one_epoch(e):
             nonlocal launches_per_epoch
@@ -390,7 +392,7 @@ def main():
         # the multi-GPU public API keeps the tables device-resident (as train()
         # does); per epoch it takes the host epoch order: shard + H2D of the
         # rank's pairs and positions, the pipelined steps, the loss read back
-        xp = args.exchange_pairs or spec.batch
+        xp = exchange_pairs
         e2e_times = []
         h2d = 0
         for e in range(args.e2e_steps):
@@ -441,8 +443,8 @@ def main():
                        "lr": spec.learning_rate, "step": "one epoch",
                        "l2_flush": "512 MiB write before every timed epoch; S+T "
                                    f"{(S.values.nbytes + T.values.nbytes) / 1e6:.1f} MB",
-                       "parallelism": (f"users sharded x{world}, pipelined item-delta "
-                                       f"all-gather every {args.exchange_pairs or spec.batch} pairs"
+                       "parallelism": (f"users sharded x{world}, item-delta exchange every "
+                                       f"{exchange_pairs} global pairs (P2P gather+apply)"
                                        if sharded else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

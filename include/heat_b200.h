@@ -171,23 +171,28 @@ int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int
                                 int64_t stride, int64_t *acc, int32_t *flags, void *stream);
 
 /* ---- multi-GPU runtime --------------------------------
- * One rank per GPU.  A heat_shard owns the rank's exchange state: two log
- * slots, the gather buffers, the fixed-point accumulator, a comm stream and
- * (world > 1) an NCCL communicator created from a unique id that rank 0 makes
- * with heat_nccl_unique_id and the caller broadcasts (e.g. torch.distributed).
- * heat_shard_epoch trains the rank's pairs of one epoch: step s covers local
- * pairs [step_bounds[s], step_bounds[s+1]) (host array), DELTA-mode kernel on
- * `stream`, then the item-delta all-gather + order-independent apply on the
- * comm stream, overlapped with the next step's kernel (one-step staleness).
- * Returns after queueing the last step; work queued later on `stream` sees
- * every applied step. */
+ * One rank per GPU.  A heat_shard owns the rank's exchange state: rotating
+ * log slots, the fixed-point accumulator, two compute streams, a
+ * top-priority comm stream and (world > 1) an NCCL communicator created from
+ * a unique id that rank 0 makes with heat_nccl_unique_id and the caller
+ * broadcasts (e.g. torch.distributed).  heat_shard_epoch trains the rank's
+ * pairs of one epoch: step s covers local pairs [step_bounds[s],
+ * step_bounds[s+1]) (host array), DELTA-mode kernel on a compute stream;
+ * then, on the comm stream, an NCCL all-gather of the step's 8-byte entry
+ * counts (also the cross-rank fence) and the fused gather+apply kernels,
+ * which read every rank's log straight from its memory over NVLink (CUDA IPC
+ * mappings; HEAT_SHARD_EXCHANGE=gather selects an NCCL all-gather of the logs
+ * instead) and add them in order-free fixed point.  Kernel(s) waits for the
+ * apply of step s - lag (lag 2; HEAT_SHARD_LAG 1..3).  No host wait inside
+ * the epoch; it returns once the epoch is done, with `stream` ordered after
+ * it.  Every rank must pass the same nsteps; capacity is agreed (max). */
 typedef struct heat_shard heat_shard;
 
 typedef struct heat_shard_stats {
-    int64_t steps;           /* exchanges performed                          */
+    int64_t steps;           /* exchanges performed                           */
     int64_t entries;         /* delta rows applied (sum over ranks and steps) */
-    int64_t exchanged_bytes; /* bytes all-gathered (padded to the max count)  */
-    int64_t max_entries;     /* largest per-rank log of a step               */
+    int64_t exchanged_bytes; /* bytes each rank read from its peers' logs     */
+    int64_t max_entries;     /* largest per-rank log of a step                */
 } heat_shard_stats;
 
 int heat_nccl_unique_id(unsigned char *out128);

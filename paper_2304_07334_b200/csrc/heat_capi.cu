@@ -76,6 +76,36 @@ void *stream_scratch(int purpose, size_t bytes, cudaStream_t stream) {
     return b.first;
 }
 
+// Resident CTAs per SM of `kern` at `threads` and `smem` dynamic bytes, with
+// the dynamic shared-memory opt-in applied once: both calls cost microseconds
+// of host time, which a short step (the sharded runtime launches one kernel
+// per few-microsecond step) cannot afford on every launch.
+int kernel_occupancy(const void *kern, int threads, size_t smem, cudaError_t *err) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, int, size_t>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, kern, threads, smem);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *err = cudaSuccess;
+            return it->second;
+        }
+    }
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    *err = e;
+    if (e != cudaSuccess) return 0;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = per_sm;
+    return per_sm;
+}
+
 static void *get_scratch(size_t bytes, cudaStream_t stream) {
     return stream_scratch(0, bytes, stream);
 }

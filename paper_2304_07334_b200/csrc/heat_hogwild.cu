@@ -448,12 +448,9 @@ static cudaError_t launch_fast_k(const HogwildArgs &a, cudaStream_t st, int *wor
     const size_t smem = (size_t)ids_stride * sizeof(int32_t) * kHogWarps;
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
     auto kern = hogwild_fast<K, U, F64>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e;
+    const int per_sm = kernel_occupancy((const void *)kern, kHogThreads, smem, &e);
     if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHogThreads, smem);
-    if (per_sm < 1) per_sm = 1;
     int64_t nw = (int64_t)per_sm * kHogWarps * sm_count();
     if (a.window > 0 && a.window < nw) nw = a.window;
     if (a.stop - a.start < nw) nw = a.stop - a.start;

@@ -368,12 +368,9 @@ static cudaError_t launch_multi_k(const HogwildArgs &a, cudaStream_t st, int *wo
     const size_t smem = L.per_warp * NW;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
     auto kern = hogwild_multi<K, NW, D, LPR>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e;
+    const int per_sm = kernel_occupancy((const void *)kern, 32 * NW, smem, &e);
     if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NW, smem);
-    if (per_sm < 1) per_sm = 1;
     int64_t nw = (int64_t)per_sm * sm_count();
     if (a.window > 0 && a.window < nw) nw = a.window;
     if (a.stop - a.start < nw) nw = a.stop - a.start;

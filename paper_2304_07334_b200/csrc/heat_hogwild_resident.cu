@@ -286,12 +286,9 @@ static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int
     const size_t smem = rs_smem_bytes<K>(((a.N + 1 + NB - 1) / NB) * NB);
     if (smem > 96 * 1024) return cudaErrorNotSupported;
     auto kern = hogwild_resident<K, NB>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e;
+    const int per_sm = kernel_occupancy((const void *)kern, 32 * NB, smem, &e);
     if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NB, smem);
-    if (per_sm < 1) per_sm = 1;
     int64_t nw = (int64_t)per_sm * sm_count();
     if (a.window > 0 && a.window < nw) nw = a.window;
     if (a.stop - a.start < nw) nw = a.stop - a.start;

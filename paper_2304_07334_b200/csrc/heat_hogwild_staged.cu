@@ -552,12 +552,9 @@ static cudaError_t launch_staged_k(const HogwildArgs &a, cudaStream_t st, int *w
     const StLayout L = st_layout<K, D, LPR>(snap_cap);
     if (L.total > 200 * 1024) return cudaErrorInvalidValue;
     auto kern = hogwild_staged<K, D, F64, BULK, LPR>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L.total);
+    cudaError_t e;
+    const int per_sm = kernel_occupancy((const void *)kern, 32, L.total, &e);
     if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, L.total);
-    if (per_sm < 1) per_sm = 1;
     const int nb = (a.N + 1 + StGeom<K, LPR>::SR - 1) / StGeom<K, LPR>::SR;
     const int pif = cross ? 1 + (D - 1 + nb - 1) / nb : 1;  // pairs in flight per worker
     int64_t nw = (int64_t)per_sm * sm_count();

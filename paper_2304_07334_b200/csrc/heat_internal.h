@@ -95,6 +95,8 @@ cudaError_t launch_exact_spec(float *S, int64_t s_rows, float *T, int64_t t_rows
                               void *scratch, const int64_t *pair_index, cudaStream_t stream);
 
 int sm_count();
+// CTAs per SM of a kernel (dynamic smem opt-in applied), cached per device
+int kernel_occupancy(const void *kern, int threads, size_t smem, cudaError_t *err);
 // library-owned scratch per (purpose, device, stream); nullptr if out of memory
 void *stream_scratch(int purpose, size_t bytes, cudaStream_t stream);
 size_t eval_max_k_supported(int K);

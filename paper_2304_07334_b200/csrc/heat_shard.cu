@@ -2,33 +2,54 @@
 //
 // users sharded u mod G, item table replicated, per-step
 // item-delta exchange.  One process per GPU; this file is the per-rank step
-// scheduler, in C++ so the host work between steps (a few event and stream
-// calls) stays far below a step's kernel time.  Per step s, slot s%2:
+// scheduler, in C++.  Per step s (log slot s % (lag + 1), lag = 2 unless
+// HEAT_SHARD_LAG says otherwise):
 //
-//   compute stream:  [wait ex_done(s-2)] memset count; DELTA kernel -> log
-//   comm stream:     all-gather counts(s); counts -> pinned host
-//   host:            (while kernel(s+1) runs) wait counts(s), cmax = max
-//   comm stream:     all-gather logs(s) (cmax entries per rank, one NCCL
-//                    group), order-independent fixed-point apply -> T
+//   compute stream s&1: [wait ex_done(s-lag)] DELTA kernel -> log slot
+//   comm stream:        [wait log_ready(s)] NCCL all-gather of the 8-byte
+//   (top priority)      counts; fused gather+apply: the apply kernels read
+//                       every rank's log slot straight from its HBM over
+//                       NVLink (CUDA IPC mappings, P2P loads) and add the
+//                       entries in 2^-40 fixed point -> T; record ex_done(s)
 //
-// kernel(s) waits for the apply of s-2 (its log slot and the staleness bound);
-// apply(s-1) runs beside kernel(s).  T changes only through the applies, which
-// every rank performs on identical gathered logs with an integer (order-free)
-// sum, so the item replicas stay bit-identical.  NCCL is resolved at run time
-// from the copy torch already loaded (dlopen RTLD_NOLOAD), so the library has
-// no link-time NCCL dependency and shares the process's NCCL.
+// Nothing waits on the host inside an epoch: the counts stay on the device,
+// the apply grid strides over whatever the counts say.  The count all-gather
+// doubles as the cross-rank fence: it completes on a rank only once every
+// rank's comm stream has reached it, i.e. finished applying step s-1 (so no
+// peer still reads an older slot) and seen its own step-s kernel finish (so
+// the slot being read is complete).  Kernel(s) waits for ex_done(s-lag):
+//   * its slot was last read by the applies of step s-lag-1, which every
+//     rank finished before its count all-gather of s-lag could complete;
+//   * it sees every applied union up to s-lag (the staleness bound on item
+//     rows; Hogwild tolerates it).
+// Consecutive kernels alternate between two compute streams, so step s+1's
+// workers fill the SMs as step s's tail drains; pairs in flight stay bounded
+// by the resident workers.  T changes only through the applies, which every
+// rank performs on the same logs with an integer (order-free) sum, so the
+// item replicas stay bit-identical.
+//
+// Fallback exchange (HEAT_SHARD_EXCHANGE=gather, or when peer mappings are
+// unavailable): the host reads the counts of step s and NCCL all-gathers the
+// logs padded to the largest count, then the same apply runs on the gathered
+// copy.  NCCL is resolved at run time from the copy torch already loaded
+// (dlopen RTLD_NOLOAD): no link-time NCCL dependency.
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "heat_common.cuh"
 #include "heat_internal.h"
 
 namespace heat {
+
+constexpr int kSlots = 4;  // log slots allocated; lag + 1 of them in use
+constexpr int kMaxWorld = 64;
 
 struct NcclApi {
     decltype(&ncclGetUniqueId) get_unique_id = nullptr;
@@ -62,77 +83,343 @@ static const NcclApi &nccl() {
 }
 
 struct Slot {
-    int32_t *ids = nullptr;
+    int32_t *ids = nullptr;  // this rank's log (capacity entries)
     float *rows = nullptr;
     int64_t *cnt = nullptr;
-    int64_t *counts = nullptr;   // world, device
-    int64_t *hcounts = nullptr;  // world, pinned host
-    int32_t *g_ids = nullptr;
+    const int32_t **pids = nullptr;  // device [world]: every rank's ids of this slot
+    const float **prows = nullptr;   // device [world]
+    int32_t *g_ids = nullptr;        // gather fallback: world * capacity entries
     float *g_rows = nullptr;
     cudaEvent_t log_ready = nullptr, cnt_ready = nullptr, ex_done = nullptr;
+};
+
+// Where the apply reads step s's entries: per-rank pointers (own log plus
+// peers' logs mapped over NVLink), or one gathered buffer of `stride` entries
+// per rank.
+struct LogView {
+    const int32_t *const *pids;
+    const float *const *prows;
+    const int32_t *ids;
+    const float *rows;
+    int64_t stride;
 };
 
 }  // namespace heat
 
 struct heat_shard {
     int world = 1, rank = 0, device = 0;
+    bool p2p = true;
+    int lag = 2;  // kernel(s) waits for the apply of step s - lag
     ncclComm_t comm = nullptr;
     cudaStream_t comm_stream = nullptr;
-    heat::Slot slot[2];
+    cudaStream_t cstream[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_cdone[2] = {nullptr, nullptr}, ev_comm = nullptr;
+    heat::Slot slot[heat::kSlots];
+    std::vector<void *> opened;  // peer mappings to close
     int64_t cap = 0, dim = 0, acc_elems = 0, t_rows = 0;
     long long *acc = nullptr;
     int32_t *flags = nullptr;
+    int64_t *step_counts = nullptr;   // device [nsteps * world]
+    int64_t *hstep_counts = nullptr;  // pinned copy
+    int64_t step_counts_n = 0;
+    int64_t *scratch = nullptr;  // device: small collective staging (handles, agreement)
     std::string err;
 };
 
 namespace heat {
 
-// frees the log buffers of both slots (the events stay)
+// ---- fused gather + apply ---------------------------------------------------
+// Entry (q, i), i < min(counts[q], cap), of rank q's log; warp per entry,
+// flattened over ranks with a prefix of the counts in shared memory.  Pass 1
+// adds round(delta * 2^40) into an int64 accumulator per (row, column) —
+// integer addition commutes — and flags the row; pass 2 converts each flagged
+// row once, T += float(acc * 2^-40).  The same fixed point as
+// heat_apply_row_deltas_fixed.
+constexpr double kShardFixScale = 1099511627776.0;  // 2^40
+
+__device__ __forceinline__ int64_t view_prefix(const int64_t *counts, int world, int64_t cap,
+                                               int64_t *pre) {
+    if (threadIdx.x == 0) {
+        int64_t s = 0;
+        pre[0] = 0;
+        for (int q = 0; q < world; ++q) {
+            s += min(max(counts[q], (int64_t)0), cap);
+            pre[q + 1] = s;
+        }
+    }
+    __syncthreads();
+    return pre[world];
+}
+
+__device__ __forceinline__ void view_entry(const LogView &v, const int64_t *pre, int world,
+                                           int64_t w, const int32_t **id_p, const float **row_p,
+                                           int K) {
+    int q = 0;
+    while (q + 1 < world && w >= pre[q + 1]) ++q;
+    const int64_t i = w - pre[q];
+    if (v.pids) {
+        *id_p = v.pids[q] + i;
+        *row_p = v.prows[q] + i * K;
+    } else {
+        *id_p = v.ids + q * v.stride + i;
+        *row_p = v.rows + (q * v.stride + i) * K;
+    }
+}
+
+// counts: the step's per-rank counts; at world 1 the log's own counter,
+// which block 0 also records into step_counts (the gathered array otherwise)
+__global__ void shard_apply_acc(int K, LogView v, const int64_t *__restrict__ counts, int world,
+                                int64_t cap, long long *__restrict__ acc,
+                                int32_t *__restrict__ flags, int64_t *__restrict__ step_counts) {
+    __shared__ int64_t pre[kMaxWorld + 1];
+    const int64_t total = view_prefix(counts, world, cap, pre);
+    if (step_counts != counts && blockIdx.x == 0 && threadIdx.x == 0) step_counts[0] = counts[0];
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += nw) {
+        const int32_t *idp;
+        const float *rp;
+        view_entry(v, pre, world, w, &idp, &rp, K);
+        const int64_t id = *idp;
+        if (lane == 0) flags[id] = 1;
+        long long *a = acc + id * K;
+        if ((K & 3) == 0) {
+            for (int k = lane * 4; k < K; k += 128) {
+                const float4 d = *reinterpret_cast<const float4 *>(rp + k);
+                atomicAdd((unsigned long long *)(a + k),
+                          (unsigned long long)__double2ll_rn((double)d.x * kShardFixScale));
+                atomicAdd((unsigned long long *)(a + k + 1),
+                          (unsigned long long)__double2ll_rn((double)d.y * kShardFixScale));
+                atomicAdd((unsigned long long *)(a + k + 2),
+                          (unsigned long long)__double2ll_rn((double)d.z * kShardFixScale));
+                atomicAdd((unsigned long long *)(a + k + 3),
+                          (unsigned long long)__double2ll_rn((double)d.w * kShardFixScale));
+            }
+        } else {
+            for (int k = lane; k < K; k += 32)
+                atomicAdd((unsigned long long *)(a + k),
+                          (unsigned long long)__double2ll_rn((double)rp[k] * kShardFixScale));
+        }
+    }
+}
+
+// counts: the step's recorded counts; block 0 re-arms this rank's log
+// counter for the slot's next step (own_cnt; its readers are all done)
+__global__ void shard_apply_cvt(float *__restrict__ T, int K, LogView v,
+                                const int64_t *__restrict__ counts, int world, int64_t cap,
+                                long long *__restrict__ acc, int32_t *__restrict__ flags,
+                                int64_t *__restrict__ own_cnt) {
+    __shared__ int64_t pre[kMaxWorld + 1];
+    const int64_t total = view_prefix(counts, world, cap, pre);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *own_cnt = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += nw) {
+        const int32_t *idp;
+        const float *rp;
+        view_entry(v, pre, world, w, &idp, &rp, K);
+        const int64_t id = *idp;
+        int mine = 0;
+        if (lane == 0) mine = atomicExch(flags + id, 0);
+        mine = __shfl_sync(0xffffffffu, mine, 0);
+        if (!mine) continue;  // another warp converts this row
+        long long *a = acc + id * K;
+        float *t = T + id * K;
+        for (int k = lane; k < K; k += 32) {
+            const long long q = a[k];
+            a[k] = 0;
+            t[k] += (float)((double)q * (1.0 / kShardFixScale));
+        }
+    }
+}
+
+static cudaError_t launch_shard_apply(float *T, int K, const LogView &v, const int64_t *counts,
+                                      int64_t *step_counts, int64_t *own_cnt, int world,
+                                      int64_t cap, long long *acc, int32_t *flags,
+                                      cudaStream_t st) {
+    // grid sized without the counts (they live on the device): enough warps to
+    // cover a typical step, striding over the rest
+    const int64_t warps = std::min<int64_t>(std::max<int64_t>(world * cap, 1),
+                                            (int64_t)sm_count() * 16);
+    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    shard_apply_acc<<<blocks, 256, 0, st>>>(K, v, counts, world, cap, acc, flags, step_counts);
+    shard_apply_cvt<<<blocks, 256, 0, st>>>(T, K, v, step_counts, world, cap, acc, flags,
+                                            own_cnt);
+    return cudaGetLastError();
+}
+
+static void close_peers(heat_shard *h) {
+    for (void *p : h->opened) cudaIpcCloseMemHandle(p);
+    h->opened.clear();
+}
+
+// frees the log buffers of every slot (the events stay)
 static void free_slots(heat_shard *h) {
+    close_peers(h);
     for (Slot &s : h->slot) {
-        cudaFree(s.ids); cudaFree(s.rows); cudaFree(s.cnt); cudaFree(s.counts);
-        cudaFreeHost(s.hcounts);
-        if (h->world > 1) { cudaFree(s.g_ids); cudaFree(s.g_rows); }
-        s.ids = nullptr; s.rows = nullptr; s.cnt = nullptr; s.counts = nullptr;
-        s.hcounts = nullptr; s.g_ids = nullptr; s.g_rows = nullptr;
+        cudaFree(s.ids); cudaFree(s.rows); cudaFree(s.cnt);
+        cudaFree((void *)s.pids); cudaFree((void *)s.prows);
+        cudaFree(s.g_ids); cudaFree(s.g_rows);
+        s.ids = nullptr; s.rows = nullptr; s.cnt = nullptr; s.pids = nullptr;
+        s.prows = nullptr; s.g_ids = nullptr; s.g_rows = nullptr;
     }
     h->cap = 0;
 }
 
-static cudaError_t ensure_buffers(heat_shard *h, int64_t cap, int64_t dim, int64_t t_rows) {
-    cudaError_t e = cudaSuccess;
-    if (cap > h->cap || dim != h->dim) {
-        cudaDeviceSynchronize();  // buffers of a previous epoch may still be in use
-        free_slots(h);
-        for (Slot &s : h->slot) {
-            if ((e = cudaMalloc(&s.ids, cap * sizeof(int32_t)))) return e;
-            if ((e = cudaMalloc(&s.rows, cap * dim * sizeof(float)))) return e;
-            if ((e = cudaMalloc(&s.cnt, sizeof(int64_t)))) return e;
-            if ((e = cudaMalloc(&s.counts, h->world * sizeof(int64_t)))) return e;
-            if ((e = cudaMallocHost(&s.hcounts, h->world * sizeof(int64_t)))) return e;
-            if (h->world > 1) {
-                if ((e = cudaMalloc(&s.g_ids, h->world * cap * sizeof(int32_t)))) return e;
-                if ((e = cudaMalloc(&s.g_rows, h->world * cap * dim * sizeof(float)))) return e;
-            } else {  // world 1: the gathered log is the log itself
-                s.g_ids = s.ids;
-                s.g_rows = s.rows;
+struct ShardErr {
+    heat_shard *h;
+    int rc = HEAT_OK;
+    bool cuda(cudaError_t e, const char *what) {
+        if (e != cudaSuccess && rc == HEAT_OK) {
+            h->err = std::string(what) + ": " + cudaGetErrorString(e);
+            rc = HEAT_ERR_CUDA;
+        }
+        return e == cudaSuccess;
+    }
+    bool nccl(ncclResult_t r, const char *what) {
+        if (r != ncclSuccess && rc == HEAT_OK) {
+            const NcclApi &n = heat::nccl();
+            h->err = std::string(what) + ": " + (n.error_string ? n.error_string(r) : "nccl error");
+            rc = HEAT_ERR_CUDA;
+        }
+        return r == ncclSuccess;
+    }
+    bool invalid(const std::string &msg) {
+        if (rc == HEAT_OK) {
+            h->err = msg;
+            rc = HEAT_ERR_INVALID;
+        }
+        return false;
+    }
+};
+
+// world > 1: host values all-gathered through NCCL (a collective: every rank
+// calls it in the same order); out has world * n entries
+static bool host_all_gather(heat_shard *h, ShardErr &er, const int64_t *in, int64_t n,
+                            int64_t *out) {
+    const int64_t bytes = n * (int64_t)sizeof(int64_t);
+    int64_t *d = h->scratch;  // 1 + world entries of 64 B handles fit (see create)
+    if (!er.cuda(cudaMemcpyAsync(d, in, bytes, cudaMemcpyHostToDevice, h->comm_stream), "stage"))
+        return false;
+    if (!er.nccl(nccl().all_gather(d, d + n, (size_t)bytes, ncclUint8, h->comm, h->comm_stream),
+                 "all_gather (host values)"))
+        return false;
+    if (!er.cuda(cudaMemcpyAsync(out, d + n, bytes * h->world, cudaMemcpyDeviceToHost,
+                                 h->comm_stream), "unstage"))
+        return false;
+    return er.cuda(cudaStreamSynchronize(h->comm_stream), "agree");
+}
+
+// (Re)allocates the slots for `cap` entries of `dim` floats and, for the P2P
+// exchange at world > 1, maps every peer's slots (IPC handles all-gathered).
+// Every rank calls it with the same agreed cap/dim.
+static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) {
+    if (cap <= h->cap && dim == h->dim) return true;
+    cudaDeviceSynchronize();  // buffers of a previous epoch may still be in use
+    free_slots(h);
+    const int W = h->world;
+    for (Slot &s : h->slot) {
+        if (!er.cuda(cudaMalloc(&s.ids, cap * sizeof(int32_t)), "log ids")) return false;
+        if (!er.cuda(cudaMalloc(&s.rows, cap * dim * sizeof(float)), "log rows")) return false;
+        if (!er.cuda(cudaMalloc(&s.cnt, sizeof(int64_t)), "log count")) return false;
+        if (!er.cuda(cudaMalloc((void **)&s.pids, W * sizeof(void *)), "peer ids")) return false;
+        if (!er.cuda(cudaMalloc((void **)&s.prows, W * sizeof(void *)), "peer rows")) return false;
+        if (W > 1 && !h->p2p) {
+            if (!er.cuda(cudaMalloc(&s.g_ids, W * cap * sizeof(int32_t)), "gather ids")) return false;
+            if (!er.cuda(cudaMalloc(&s.g_rows, W * cap * dim * sizeof(float)), "gather rows"))
+                return false;
+        }
+    }
+    std::vector<const void *> pid(W * kSlots), prow(W * kSlots);
+    for (int k = 0; k < kSlots; ++k) {
+        pid[h->rank * kSlots + k] = h->slot[k].ids;
+        prow[h->rank * kSlots + k] = h->slot[k].rows;
+    }
+    if (W > 1 && h->p2p) {
+        // 2 * kSlots IPC handles per rank, exchanged as int64 words
+        static_assert(sizeof(cudaIpcMemHandle_t) % sizeof(int64_t) == 0, "handle size");
+        constexpr int64_t hw = sizeof(cudaIpcMemHandle_t) / sizeof(int64_t);
+        std::vector<int64_t> mine(2 * kSlots * hw), all(W * 2 * kSlots * hw);
+        for (int k = 0; k < kSlots; ++k) {
+            cudaIpcMemHandle_t a, b;
+            if (!er.cuda(cudaIpcGetMemHandle(&a, h->slot[k].ids), "ipc handle")) return false;
+            if (!er.cuda(cudaIpcGetMemHandle(&b, h->slot[k].rows), "ipc handle")) return false;
+            memcpy(&mine[(2 * k) * hw], &a, sizeof(a));
+            memcpy(&mine[(2 * k + 1) * hw], &b, sizeof(b));
+        }
+        if (!host_all_gather(h, er, mine.data(), (int64_t)mine.size(), all.data())) return false;
+        for (int q = 0; q < W; ++q) {
+            if (q == h->rank) continue;
+            for (int k = 0; k < kSlots; ++k) {
+                cudaIpcMemHandle_t a, b;
+                memcpy(&a, &all[((int64_t)q * 2 * kSlots + 2 * k) * hw], sizeof(a));
+                memcpy(&b, &all[((int64_t)q * 2 * kSlots + 2 * k + 1) * hw], sizeof(b));
+                void *pa = nullptr, *pb = nullptr;
+                if (!er.cuda(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess),
+                             "map peer log (set HEAT_SHARD_EXCHANGE=gather without peer access)"))
+                    return false;
+                h->opened.push_back(pa);
+                if (!er.cuda(cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess),
+                             "map peer log"))
+                    return false;
+                h->opened.push_back(pb);
+                pid[q * kSlots + k] = pa;
+                prow[q * kSlots + k] = pb;
             }
         }
-        h->cap = cap;
-        h->dim = dim;
     }
+    for (int k = 0; k < kSlots; ++k) {
+        std::vector<const void *> a(W), b(W);
+        for (int q = 0; q < W; ++q) {
+            a[q] = pid[q * kSlots + k];
+            b[q] = prow[q * kSlots + k];
+        }
+        if (!er.cuda(cudaMemcpy((void *)h->slot[k].pids, a.data(), W * sizeof(void *),
+                                cudaMemcpyHostToDevice), "peer table"))
+            return false;
+        if (!er.cuda(cudaMemcpy((void *)h->slot[k].prows, b.data(), W * sizeof(void *),
+                                cudaMemcpyHostToDevice), "peer table"))
+            return false;
+    }
+    h->cap = cap;
+    h->dim = dim;
+    return true;
+}
+
+static bool ensure_epoch_buffers(heat_shard *h, ShardErr &er, int64_t t_rows, int64_t dim,
+                                 int64_t nsteps) {
     if (t_rows * dim > h->acc_elems || t_rows > h->t_rows) {
         cudaDeviceSynchronize();
         cudaFree(h->acc);
         cudaFree(h->flags);
+        h->acc = nullptr;
+        h->flags = nullptr;
+        h->acc_elems = 0;
+        h->t_rows = 0;
+        if (!er.cuda(cudaMalloc(&h->acc, t_rows * dim * sizeof(long long)), "accumulator"))
+            return false;
+        if (!er.cuda(cudaMalloc(&h->flags, t_rows * sizeof(int32_t)), "row flags")) return false;
+        if (!er.cuda(cudaMemset(h->acc, 0, t_rows * dim * sizeof(long long)), "zero acc"))
+            return false;
+        if (!er.cuda(cudaMemset(h->flags, 0, t_rows * sizeof(int32_t)), "zero flags"))
+            return false;
         h->acc_elems = t_rows * dim;
-        if ((e = cudaMalloc(&h->acc, t_rows * dim * sizeof(long long)))) return e;
-        if ((e = cudaMalloc(&h->flags, t_rows * sizeof(int32_t)))) return e;
-        if ((e = cudaMemset(h->acc, 0, t_rows * dim * sizeof(long long)))) return e;
-        if ((e = cudaMemset(h->flags, 0, t_rows * sizeof(int32_t)))) return e;
         h->t_rows = t_rows;
     }
-    return e;
+    const int64_t n = std::max<int64_t>(nsteps, 1) * h->world;
+    if (n > h->step_counts_n) {
+        cudaDeviceSynchronize();
+        cudaFree(h->step_counts);
+        cudaFreeHost(h->hstep_counts);
+        h->step_counts = nullptr;
+        h->hstep_counts = nullptr;
+        h->step_counts_n = 0;
+        if (!er.cuda(cudaMalloc(&h->step_counts, n * sizeof(int64_t)), "step counts")) return false;
+        if (!er.cuda(cudaMallocHost(&h->hstep_counts, n * sizeof(int64_t)), "step counts (host)"))
+            return false;
+        h->step_counts_n = n;
+    }
+    return true;
 }
 
 }  // namespace heat
@@ -153,31 +440,51 @@ int heat_nccl_unique_id(unsigned char *out128) {
 
 int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id, int32_t device,
                       heat_shard **out) {
-    if (!out || world < 1 || rank < 0 || rank >= world) return HEAT_ERR_INVALID;
+    if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return HEAT_ERR_INVALID;
     heat_shard *h = new heat_shard();
     h->world = world;
     h->rank = rank;
     h->device = device;
+    const char *ex = getenv("HEAT_SHARD_EXCHANGE");
+    h->p2p = !(ex && strcmp(ex, "gather") == 0);
+    if (const char *l = getenv("HEAT_SHARD_LAG")) h->lag = std::min(std::max(atoi(l), 1), kSlots - 1);
     cudaSetDevice(device);
-    if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess) {
-        delete h;
-        return HEAT_ERR_CUDA;
-    }
+    // the exchange runs at the highest priority: its apply CTAs take the SM
+    // slots that the step kernels free before the next kernel's workers do
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    bool ok = cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, hi) ==
+              cudaSuccess;
+    for (int i = 0; i < 2 && ok; ++i)
+        ok = cudaStreamCreateWithFlags(&h->cstream[i], cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; ++i)
+        ok = cudaEventCreateWithFlags(&h->ev_cdone[i], cudaEventDisableTiming) == cudaSuccess;
     for (Slot &s : h->slot) {
-        cudaEventCreateWithFlags(&s.log_ready, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&s.cnt_ready, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&s.ex_done, cudaEventDisableTiming);
+        ok = ok && cudaEventCreateWithFlags(&s.log_ready, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&s.cnt_ready, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&s.ex_done, cudaEventDisableTiming) == cudaSuccess;
+    }
+    // staging for the host-value all-gathers: (1 + world) * 2 * kSlots handles
+    ok = ok && cudaMalloc(&h->scratch, (size_t)(1 + world) * 2 * kSlots *
+                                           sizeof(cudaIpcMemHandle_t)) == cudaSuccess;
+    if (!ok) {
+        heat_shard_destroy(h);
+        return HEAT_ERR_CUDA;
     }
     if (world > 1) {
         const NcclApi &n = nccl();
         if (!n.ok || !nccl_id) {
-            delete h;
+            heat_shard_destroy(h);
             return HEAT_ERR_UNSUPPORTED;
         }
         ncclUniqueId id;
         memcpy(&id, nccl_id, sizeof(id));
         if (n.comm_init_rank(&h->comm, world, id, rank) != ncclSuccess) {
-            delete h;
+            h->comm = nullptr;
+            heat_shard_destroy(h);
             return HEAT_ERR_CUDA;
         }
     }
@@ -187,17 +494,25 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
 
 int heat_shard_destroy(heat_shard *h) {
     if (!h) return HEAT_OK;
-    cudaStreamSynchronize(h->comm_stream);
+    cudaSetDevice(h->device);
+    for (cudaStream_t s : {h->comm_stream, h->cstream[0], h->cstream[1]})
+        if (s) cudaStreamSynchronize(s);
     free_slots(h);
     for (Slot &s : h->slot) {
-        cudaEventDestroy(s.log_ready);
-        cudaEventDestroy(s.cnt_ready);
-        cudaEventDestroy(s.ex_done);
+        if (s.log_ready) cudaEventDestroy(s.log_ready);
+        if (s.cnt_ready) cudaEventDestroy(s.cnt_ready);
+        if (s.ex_done) cudaEventDestroy(s.ex_done);
     }
+    for (cudaEvent_t e : {h->ev_start, h->ev_comm, h->ev_cdone[0], h->ev_cdone[1]})
+        if (e) cudaEventDestroy(e);
     cudaFree(h->acc);
     cudaFree(h->flags);
+    cudaFree(h->step_counts);
+    cudaFreeHost(h->hstep_counts);
+    cudaFree(h->scratch);
     if (h->comm) nccl().comm_destroy(h->comm);
-    cudaStreamDestroy(h->comm_stream);
+    for (cudaStream_t s : {h->comm_stream, h->cstream[0], h->cstream[1]})
+        if (s) cudaStreamDestroy(s);
     delete h;
     return HEAT_OK;
 }
@@ -214,98 +529,150 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         h->err = "heat_shard_epoch runs HEAT_MODE_DELTA steps";
         return HEAT_ERR_INVALID;
     }
-    cudaStream_t cs = (cudaStream_t)stream;
+    cudaSetDevice(h->device);
+    cudaStream_t caller = (cudaStream_t)stream;
     const int W = h->world;
     const int64_t K = p->dim;
-    cudaError_t e = ensure_buffers(h, capacity, K, t_rows);
-    if (e != cudaSuccess) {
-        h->err = std::string("buffer allocation: ") + cudaGetErrorString(e);
-        return HEAT_ERR_CUDA;
-    }
+    ShardErr er{h};
     const NcclApi &n = nccl();
-    heat_shard_stats st{};
-    int rc = HEAT_OK;
-    auto check = [&](cudaError_t ce, const char *what) {
-        if (ce != cudaSuccess && rc == HEAT_OK) {
-            h->err = std::string(what) + ": " + cudaGetErrorString(ce);
-            rc = HEAT_ERR_CUDA;
+
+    // every rank must run the same number of steps with the same log layout:
+    // agree (max capacity) and check, before any per-step collective
+    int64_t cap = capacity;
+    if (W > 1) {
+        const int64_t mine[3] = {capacity, nsteps, K};
+        std::vector<int64_t> all(3 * W);
+        if (!host_all_gather(h, er, mine, 3, all.data())) return er.rc;
+        for (int q = 0; q < W; ++q) {
+            if (all[3 * q + 1] != nsteps || all[3 * q + 2] != K) {
+                er.invalid("ranks disagree on the epoch's step count or dim (steps " +
+                           std::to_string(nsteps) + " vs " + std::to_string(all[3 * q + 1]) +
+                           " on rank " + std::to_string(q) + ")");
+                return er.rc;
+            }
+            cap = std::max(cap, all[3 * q]);
         }
-    };
-    auto nccl_check = [&](ncclResult_t r, const char *what) {
-        if (r != ncclSuccess && rc == HEAT_OK) {
-            h->err = std::string(what) + ": " + (n.error_string ? n.error_string(r) : "nccl error");
-            rc = HEAT_ERR_CUDA;
-        }
-    };
-    auto launch = [&](int64_t s) {
-        Slot &sl = h->slot[s & 1];
-        if (s >= 2) check(cudaStreamWaitEvent(cs, sl.ex_done, 0), "wait apply");
-        check(cudaMemsetAsync(sl.cnt, 0, sizeof(int64_t), cs), "memset count");
+    }
+    if (!ensure_slots(h, er, cap, K)) return er.rc;
+    if (!ensure_epoch_buffers(h, er, t_rows, K, nsteps)) return er.rc;
+    cap = h->cap;
+
+    // log counters start at zero (afterwards each step's apply re-arms its
+    // slot); the internal streams start after the caller's queued work
+    for (Slot &sl : h->slot) er.cuda(cudaMemsetAsync(sl.cnt, 0, sizeof(int64_t), caller), "zero");
+    er.cuda(cudaEventRecord(h->ev_start, caller), "record start");
+    for (cudaStream_t s : {h->cstream[0], h->cstream[1], h->comm_stream})
+        er.cuda(cudaStreamWaitEvent(s, h->ev_start, 0), "wait start");
+
+    const int lag = h->lag, nslots = h->lag + 1;
+    auto compute = [&](int64_t s) {
+        Slot &sl = h->slot[s % nslots];
+        cudaStream_t cs = h->cstream[s & 1];
+        if (s >= lag) er.cuda(cudaStreamWaitEvent(cs, h->slot[(s - lag) % nslots].ex_done, 0),
+                              "wait apply");
         const int64_t a = step_bounds[s], b = step_bounds[s + 1];
         if (b > a) {
             const int r = heat_train_range(S, s_rows, T, t_rows, local_users, local_items, a, b, p,
-                                           counters, sl.ids, sl.rows, sl.cnt, capacity,
-                                           pair_index, nullptr, nullptr, cs);
-            if (r != HEAT_OK && rc == HEAT_OK) {
+                                           counters, sl.ids, sl.rows, sl.cnt, cap, pair_index,
+                                           nullptr, nullptr, cs);
+            if (r != HEAT_OK && er.rc == HEAT_OK) {
                 h->err = std::string("train_range: ") + heat_last_error();
-                rc = r;
+                er.rc = r;
             }
         }
-        check(cudaEventRecord(sl.log_ready, cs), "record log");
-        check(cudaStreamWaitEvent(h->comm_stream, sl.log_ready, 0), "wait log");
-        if (W > 1)
-            nccl_check(n.all_gather(sl.cnt, sl.counts, 1, ncclInt64, h->comm, h->comm_stream),
-                       "all_gather counts");
-        else
-            check(cudaMemcpyAsync(sl.counts, sl.cnt, sizeof(int64_t), cudaMemcpyDeviceToDevice,
-                                  h->comm_stream), "count copy");
-        check(cudaMemcpyAsync(sl.hcounts, sl.counts, W * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                              h->comm_stream), "count to host");
-        check(cudaEventRecord(sl.cnt_ready, h->comm_stream), "record counts");
+        er.cuda(cudaEventRecord(sl.log_ready, cs), "record log");
     };
-    auto exchange = [&](int64_t t) {
-        Slot &sl = h->slot[t & 1];
-        check(cudaEventSynchronize(sl.cnt_ready), "counts");  // kernel(t+1) already queued
-        int64_t cmax = 0, total = 0;
-        for (int r = 0; r < W; ++r) {
-            cmax = std::max(cmax, sl.hcounts[r]);
-            total += sl.hcounts[r];
+    // counts of step s: the fence every rank passes before reading slot s
+    auto count = [&](int64_t s) {
+        Slot &sl = h->slot[s % nslots];
+        er.cuda(cudaStreamWaitEvent(h->comm_stream, sl.log_ready, 0), "wait log");
+        int64_t *cnts = h->step_counts + s * W;
+        if (W > 1)  // (world 1: the apply records the log's own counter)
+            er.nccl(n.all_gather(sl.cnt, cnts, 1, ncclInt64, h->comm, h->comm_stream),
+                    "all_gather counts");
+        if (!h->p2p && W > 1) {
+            er.cuda(cudaMemcpyAsync(h->hstep_counts + s * W, cnts, W * sizeof(int64_t),
+                                    cudaMemcpyDeviceToHost, h->comm_stream), "count to host");
+            er.cuda(cudaEventRecord(sl.cnt_ready, h->comm_stream), "record counts");
         }
-        if (cmax > capacity && rc == HEAT_OK) {
-            h->err = "delta log overflow (" + std::to_string(cmax) + " > " +
-                     std::to_string(capacity) + " entries on some rank); raise the capacity";
-            rc = HEAT_ERR_INVALID;
-        }
-        if (cmax > 0 && rc == HEAT_OK) {
-            if (W > 1) {
-                nccl_check(n.group_start(), "group start");
-                nccl_check(n.all_gather(sl.ids, sl.g_ids, (size_t)cmax, ncclInt32, h->comm,
-                                        h->comm_stream), "all_gather ids");
-                nccl_check(n.all_gather(sl.rows, sl.g_rows, (size_t)(cmax * K), ncclFloat32,
-                                        h->comm, h->comm_stream), "all_gather rows");
-                nccl_check(n.group_end(), "group end");
+    };
+    auto apply = [&](int64_t t) {
+        Slot &sl = h->slot[t % nslots];
+        int64_t *cnts = h->step_counts + t * W;
+        LogView v{};
+        if (h->p2p || W == 1) {
+            v.pids = sl.pids;
+            v.prows = sl.prows;
+        } else {  // gather fallback: counts read on the host, logs padded to the max
+            er.cuda(cudaEventSynchronize(sl.cnt_ready), "counts");
+            int64_t cmax = 0;
+            for (int q = 0; q < W; ++q) cmax = std::max(cmax, h->hstep_counts[t * W + q]);
+            cmax = std::min(cmax, cap);
+            if (cmax > 0 && er.rc == HEAT_OK) {
+                er.nccl(n.group_start(), "group start");
+                er.nccl(n.all_gather(sl.ids, sl.g_ids, (size_t)cmax, ncclInt32, h->comm,
+                                     h->comm_stream), "all_gather ids");
+                er.nccl(n.all_gather(sl.rows, sl.g_rows, (size_t)(cmax * K), ncclFloat32, h->comm,
+                                     h->comm_stream), "all_gather rows");
+                er.nccl(n.group_end(), "group end");
             }
-            check(launch_apply_deltas_fixed(T, (int)K, sl.g_ids, sl.g_rows, sl.counts, W, cmax,
-                                            h->acc, h->flags, h->comm_stream), "apply");
+            v.ids = sl.g_ids;
+            v.rows = sl.g_rows;
+            v.stride = cmax;
         }
-        check(cudaEventRecord(sl.ex_done, h->comm_stream), "record apply");
-        st.steps += 1;
-        st.entries += total;
-        st.exchanged_bytes += (int64_t)W * cmax * (4 * K + 4);
+        if (er.rc == HEAT_OK)
+            er.cuda(launch_shard_apply(T, (int)K, v, W > 1 ? cnts : sl.cnt, cnts, sl.cnt, W, cap,
+                                       h->acc, h->flags, h->comm_stream), "apply");
+        er.cuda(cudaEventRecord(sl.ex_done, h->comm_stream), "record apply");
+    };
+    const bool direct = h->p2p || W == 1;
+    for (int64_t s = 0; s < nsteps && er.rc == HEAT_OK; ++s) {
+        compute(s);
+        if (direct) {  // nothing waits on the host: queue the step's exchange right behind it
+            count(s);
+            apply(s);
+        } else {  // gather fallback: the host wait on the counts of s-1 overlaps kernel(s)
+            if (s >= 1) apply(s - 1);
+            count(s);
+        }
+    }
+    if (!direct && nsteps >= 1 && er.rc == HEAT_OK) apply(nsteps - 1);
+
+    // the caller's stream sees every applied step; the epoch's counts come
+    // back once for the statistics and the overflow check
+    if (nsteps > 0)
+        er.cuda(cudaMemcpyAsync(h->hstep_counts, h->step_counts, nsteps * W * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, h->comm_stream), "counts to host");
+    for (int i = 0; i < 2; ++i) {
+        er.cuda(cudaEventRecord(h->ev_cdone[i], h->cstream[i]), "record compute");
+        er.cuda(cudaStreamWaitEvent(caller, h->ev_cdone[i], 0), "join compute");
+    }
+    er.cuda(cudaEventRecord(h->ev_comm, h->comm_stream), "record comm");
+    er.cuda(cudaStreamWaitEvent(caller, h->ev_comm, 0), "join comm");
+    er.cuda(cudaStreamSynchronize(h->comm_stream), "epoch");
+    for (int i = 0; i < 2; ++i) er.cuda(cudaStreamSynchronize(h->cstream[i]), "epoch");
+    if (er.rc != HEAT_OK) return er.rc;
+
+    heat_shard_stats st{};
+    for (int64_t s = 0; s < nsteps; ++s) {
+        int64_t cmax = 0;
+        for (int q = 0; q < W; ++q) {
+            const int64_t c = h->hstep_counts[s * W + q];
+            cmax = std::max(cmax, c);
+            st.entries += std::min(c, cap);
+        }
+        if (cmax > cap) {
+            er.invalid("delta log overflow (" + std::to_string(cmax) + " > " +
+                       std::to_string(cap) + " entries on some rank in step " +
+                       std::to_string(s) + "); raise the capacity");
+        }
         st.max_entries = std::max(st.max_entries, cmax);
-    };
-    for (int64_t s = 0; s <= nsteps && rc == HEAT_OK; ++s) {
-        if (s < nsteps) launch(s);
-        if (s >= 1 && rc == HEAT_OK) exchange(s - 1);
+        st.steps += 1;
     }
-    // later work on the caller's stream sees every applied union
-    for (int i = 0; i < 2 && i < nsteps; ++i) check(cudaStreamWaitEvent(cs, h->slot[i].ex_done, 0), "join");
-    if (rc != HEAT_OK) {  // drain before reporting so buffers are idle
-        cudaStreamSynchronize(cs);
-        cudaStreamSynchronize(h->comm_stream);
-    }
+    // bytes that crossed between GPUs: every rank reads every other rank's log
+    st.exchanged_bytes = (W > 1 ? (W - 1) : 0) * st.entries * (4 * K + 4);
     if (stats) *stats = st;
-    return rc;
+    return er.rc;
 }
 
 }  // extern "C"

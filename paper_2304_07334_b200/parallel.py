@@ -397,10 +397,14 @@ class PipelinedShardTrainer(ShardedTrainer):
 
 
 class NativeShardTrainer(ShardedTrainer):
-    """The production multi-GPU driver: the same pipelined steps as
-    PipelinedShardTrainer, scheduled by the native runtime (csrc/heat_shard.cu)
-    with its own NCCL communicator (unique id broadcast over the default
-    torch.distributed group), so no Python runs between steps."""
+    """The production multi-GPU driver (csrc/heat_shard.cu), with its own NCCL
+    communicator (unique id broadcast over the default torch.distributed
+    group).  Per step: DELTA kernel on one of two alternating compute streams;
+    on a top-priority comm stream, an NCCL all-gather of the 8-byte entry
+    counts (the cross-rank fence) and the fused gather+apply kernels, which
+    read the peers' logs over NVLink through CUDA IPC mappings.  No Python and
+    no host wait between steps; kernel(s) sees every applied step up to
+    s - lag (lag 2, ``HEAT_SHARD_LAG``)."""
 
     def __init__(self, model: DeviceModel, world: int, rank: int, group=None):
         super().__init__(model, world, rank, group)

@@ -815,6 +815,44 @@ def test_native_shard_runtime_world1(torch_cuda):
     tr.close()
 
 
+@pytest.mark.parametrize("lag", ["1", "3"])
+def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag):
+    """The native runtime with other staleness bounds (HEAT_SHARD_LAG: kernel(s)
+    waits for the apply of step s - lag; lag + 1 log slots in rotation, two
+    compute streams): every pair trained once per epoch, every step exchanged,
+    loss within 3 % of the 1-GPU Hogwild run."""
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.parallel import NativeShardTrainer
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    monkeypatch.setenv("HEAT_SHARD_LAG", lag)
+    train, _, _ = make_dataset("c2", scale=0.05)
+    mk = lambda: DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,  # noqa: E731
+                             init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
+    tr = NativeShardTrainer(mk(), 1, 0)
+    m = mk()
+    for e in range(2):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        p = tr.model.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                            mode=N.MODE_DELTA, stream_base=epoch_stream(0, e), window=512)
+        tr.model.counters.reset()
+        st = tr.train_epoch(u, i, p, 512)
+        c = tr.model.counters.read()
+        assert c.pairs == len(u) and st.steps == tr.num_steps and st.entries >= len(u)
+        du, di = m.upload_pairs(u, i)
+        p = m.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                     mode=N.MODE_HOGWILD, stream_base=epoch_stream(0, e), window=2048)
+        m.counters.reset()
+        m.train_range(du, di, 0, len(u), p)
+    assert np.isfinite(tr.model.T.cpu().numpy()).all()
+    ref = m.counters.read().loss
+    assert abs(c.loss - ref) <= 0.03 * abs(ref), (c.loss, ref)
+    tr.close()
+
+
 def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
     """train() (trainer.py:480-533): tables stay on the device across epochs,
     yet the run equals the reference's epoch-by-epoch result bit for bit;
