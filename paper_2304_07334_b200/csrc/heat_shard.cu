@@ -28,8 +28,8 @@
 // rank performs on the same logs with an integer (order-free) sum, so the
 // item replicas stay bit-identical.
 //
-// Fallback exchange (HEAT_SHARD_EXCHANGE=gather, or when peer mappings are
-// unavailable): the host reads the counts of step s and NCCL all-gathers the
+// Fallback exchange (HEAT_SHARD_EXCHANGE=gather, or automatically when some
+// rank cannot map a peer's memory): the host reads the counts of step s and NCCL all-gathers the
 // logs padded to the largest count, then the same apply runs on the gathered
 // copy.  NCCL is resolved at run time from the copy torch already loaded
 // (dlopen RTLD_NOLOAD): no link-time NCCL dependency.
@@ -180,12 +180,12 @@ __global__ void shard_apply_acc(int K, LogView v, const int64_t *__restrict__ co
         const int32_t *idp;
         const float *rp;
         view_entry(v, pre, world, w, &idp, &rp, K);
-        const int64_t id = *idp;
+        const int64_t id = __ldcg(idp);  // peers' logs: read at L2 (theirs), never L1
         if (lane == 0) flags[id] = 1;
         long long *a = acc + id * K;
         if ((K & 3) == 0) {
             for (int k = lane * 4; k < K; k += 128) {
-                const float4 d = *reinterpret_cast<const float4 *>(rp + k);
+                const float4 d = __ldcg(reinterpret_cast<const float4 *>(rp + k));
                 atomicAdd((unsigned long long *)(a + k),
                           (unsigned long long)__double2ll_rn((double)d.x * kShardFixScale));
                 atomicAdd((unsigned long long *)(a + k + 1),
@@ -198,7 +198,7 @@ __global__ void shard_apply_acc(int K, LogView v, const int64_t *__restrict__ co
         } else {
             for (int k = lane; k < K; k += 32)
                 atomicAdd((unsigned long long *)(a + k),
-                          (unsigned long long)__double2ll_rn((double)rp[k] * kShardFixScale));
+                          (unsigned long long)__double2ll_rn((double)__ldcg(rp + k) * kShardFixScale));
         }
     }
 }
@@ -218,7 +218,7 @@ __global__ void shard_apply_cvt(float *__restrict__ T, int K, LogView v,
         const int32_t *idp;
         const float *rp;
         view_entry(v, pre, world, w, &idp, &rp, K);
-        const int64_t id = *idp;
+        const int64_t id = __ldcg(idp);
         int mine = 0;
         if (lane == 0) mine = atomicExch(flags + id, 0);
         mine = __shfl_sync(0xffffffffu, mine, 0);
@@ -348,24 +348,41 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
             memcpy(&mine[(2 * k + 1) * hw], &b, sizeof(b));
         }
         if (!host_all_gather(h, er, mine.data(), (int64_t)mine.size(), all.data())) return false;
-        for (int q = 0; q < W; ++q) {
+        int64_t mapped = 1;
+        for (int q = 0; q < W && mapped; ++q) {
             if (q == h->rank) continue;
-            for (int k = 0; k < kSlots; ++k) {
+            for (int k = 0; k < kSlots && mapped; ++k) {
                 cudaIpcMemHandle_t a, b;
                 memcpy(&a, &all[((int64_t)q * 2 * kSlots + 2 * k) * hw], sizeof(a));
                 memcpy(&b, &all[((int64_t)q * 2 * kSlots + 2 * k + 1) * hw], sizeof(b));
                 void *pa = nullptr, *pb = nullptr;
-                if (!er.cuda(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess),
-                             "map peer log (set HEAT_SHARD_EXCHANGE=gather without peer access)"))
-                    return false;
-                h->opened.push_back(pa);
-                if (!er.cuda(cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess),
-                             "map peer log"))
-                    return false;
+                if (cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+                    (h->opened.push_back(pa),
+                     cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)) {
+                    cudaGetLastError();  // no peer mapping: every rank falls back below
+                    mapped = 0;
+                    break;
+                }
                 h->opened.push_back(pb);
                 pid[q * kSlots + k] = pa;
                 prow[q * kSlots + k] = pb;
             }
+        }
+        // the exchange mode is collective: P2P only if every rank mapped every peer
+        std::vector<int64_t> all_mapped(W);
+        if (!host_all_gather(h, er, &mapped, 1, all_mapped.data())) return false;
+        if (*std::min_element(all_mapped.begin(), all_mapped.end()) == 0) {
+            close_peers(h);
+            h->p2p = false;
+            for (Slot &s : h->slot) {
+                if (!er.cuda(cudaMalloc(&s.g_ids, W * cap * sizeof(int32_t)), "gather ids"))
+                    return false;
+                if (!er.cuda(cudaMalloc(&s.g_rows, W * cap * dim * sizeof(float)), "gather rows"))
+                    return false;
+            }
+            for (int q = 0; q < W; ++q)
+                for (int k = 0; k < kSlots; ++k)
+                    if (q != h->rank) pid[q * kSlots + k] = prow[q * kSlots + k] = nullptr;
         }
     }
     for (int k = 0; k < kSlots; ++k) {
