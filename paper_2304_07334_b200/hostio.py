@@ -43,13 +43,15 @@ class PairPrefetcher:
         self._pool: list = []     # reusable pinned (users, items) buffers
 
     def _buffers(self, P: int):
+        """(users, items, both): two views of one page-locked [2, P] block, so
+        an epoch order goes to the device in a single copy."""
         with self._lock:
-            for i, (u, it) in enumerate(self._pool):
-                if u.numel() == P:
+            for i, b in enumerate(self._pool):
+                if b[0].numel() == P:
                     return self._pool.pop(i)
         pin = torch.cuda.is_available()
-        return (torch.empty(P, dtype=torch.int32, pin_memory=pin),
-                torch.empty(P, dtype=torch.int32, pin_memory=pin))
+        both = torch.empty((2, P), dtype=torch.int32, pin_memory=pin)
+        return (both[0], both[1], both)
 
     def release(self, bufs) -> None:
         with self._lock:

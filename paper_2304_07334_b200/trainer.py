@@ -144,10 +144,12 @@ def sgd_params(model: DeviceModel, cfg, epoch: int, mode: int) -> N.SgdParams:
 
 
 def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int | None = None,
-                        pairs=None, agg=None, before_read=None) -> tuple[EpochReport, dict]:
+                        pairs=None, agg=None, before_read=None,
+                        before_sync=None) -> tuple[EpochReport, dict]:
     """One epoch on device-resident tables; no table transfer.  `before_read`
     (optional) queues more stream work (e.g. the table write-back) ahead of
-    the single synchronisation that reads the counters."""
+    the single synchronisation that reads the counters; `before_sync` runs
+    host work while the device is busy."""
     if mode is None:
         mode = resolve_mode(cfg)
     t0 = time.perf_counter()
@@ -168,6 +170,8 @@ def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int
     model.counters.fetch()
     if before_read is not None:
         before_read()
+    if before_sync is not None:
+        before_sync()
     torch.cuda.current_stream(model.device).synchronize()
     c = model.counters.values()
     wall = time.perf_counter() - t0
@@ -199,9 +203,6 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     t_start = time.perf_counter()
     model = _session_model(S.values, T.values)  # raises without CUDA: no CPU fallback
     bufs = PREFETCH.get(train, shuffle_seed(cfg.seed, epoch))
-    for ahead in range(1, PREFETCH.depth_for(train.num_pairs) + 1):  # host threads keep the
-        # next orders coming
-        PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + ahead))
     dev = model.device
     stream = torch.cuda.current_stream(dev)
     pin_array(S.values)
@@ -209,8 +210,8 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     t_up = time.perf_counter()
     model.S.copy_(torch.from_numpy(S.values), non_blocking=True)
     model.T.copy_(torch.from_numpy(T.values), non_blocking=True)
-    du = bufs[0].to(dev, non_blocking=True)
-    di = bufs[1].to(dev, non_blocking=True)
+    pairs = bufs[2].to(dev, non_blocking=True)  # users and items in one copy
+    du, di = pairs[0], pairs[1]
     if collect_phases:
         stream.synchronize()
     agg = _make_aggregator(model, weights, train, cfg)
@@ -224,8 +225,12 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
         torch.from_numpy(T.values).copy_(model.T, non_blocking=True)
         ev_end.record()
 
+    def prefetch():  # host threads produce the next orders while the GPU runs
+        for ahead in range(1, PREFETCH.depth_for(train.num_pairs) + 1):
+            PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + ahead))
+
     rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=(du, di), agg=agg,
-                                      before_read=write_back)
+                                      before_read=write_back, before_sync=prefetch)
     PREFETCH.release(bufs)
     if agg is not None:  # the reference updates the shared weights in place
         np.copyto(weights, agg.W.cpu().numpy())
