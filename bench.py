@@ -230,6 +230,20 @@ def _ncu_traffic(config: str):
         return None
 
 
+def _l2_ceiling(achieved_gbs: float, table_bytes: int) -> dict:
+    """The second ceiling for configurations whose tables stay in the 126 MB
+    L2 (c1-c4): the streaming L2 read rate measured on this GPU model by
+    scripts/l2_bandwidth.py (profiles/r01_l2_bandwidth.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_l2_bandwidth.json")) as f:
+            l2 = float(json.load(f)["stream_48MB_GBps"])
+    except Exception:
+        return {}
+    return {"tables_fit_l2": table_bytes < 100 * 1024 * 1024, "l2_probe_gbs": l2,
+            "frac_of_l2_probe": achieved_gbs / l2,
+            "l2_probe_source": "scripts/l2_bandwidth.py (profiles/r01_l2_bandwidth.json)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -452,7 +466,8 @@ def main():
                          "traffic_source": prof.get("source") if prof else None,
                          "l2_hit_rate_pct": prof.get("l2_hit_rate_pct") if prof else None,
                          "bytes_per_launch": bytes_per_epoch,
-                         "active_negatives_per_pair": act_total / args.steps / npairs},
+                         "active_negatives_per_pair": act_total / args.steps / npairs,
+                         **_l2_ceiling(achieved, S.values.nbytes + T.values.nbytes)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_epoch * args.steps,
