@@ -70,7 +70,13 @@ __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
 #define MULTI_MINB 5  // measured: 5 CTAs (20 warps) per SM, registers <= 102
 #endif
 
-template <int K, int NW, int D, int LPR>
+// SPLIT (opt-in, HEAT_MULTI_SPLIT=1): the "all reads before any write" point
+// of a pair is an mbarrier that each warp arrives on as soon as its last
+// stage has landed, instead of a CTA barrier after every warp's scoring.
+// Unlike the resident kernel (+7 %), it measured slower here (c3 72.7 M vs
+// 77.7 M samples/s): the warps' stage loops are equally long, so there is
+// little barrier wait to hide, and the waiting warps poll.
+template <int K, int NW, int D, int LPR, bool SPLIT>
 __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     hogwild_multi(HogwildArgs a, FastMod fm, int n_workers, int snap_cap) {
     using G = MwGeom<K, LPR>;
@@ -92,6 +98,12 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     const int gw = blockIdx.x;
     const int64_t npairs = a.stop - a.start;
     if (gw >= n_workers || gw >= npairs) return;  // uniform per CTA
+    __shared__ uint64_t reads_done;
+    uint32_t phase = 0;
+    if (SPLIT) {
+        if (threadIdx.x == 0) mbar_init(&reads_done, NW);
+        __syncthreads();
+    }
     const int N = a.N;
     const int nb = (N + 1 + SR - 1) / SR;          // stages per pair
     const int nbw = nb > w ? (nb - w + NW - 1) / NW : 0;  // this warp's stages
@@ -147,6 +159,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
             ++issued;
         };
         for (int i = 0; i < D; ++i) issue();
+        if (SPLIT && nbw == 0 && lane == 0) mbar_arrive(&reads_done);
 
         float ug[VW], uu[VW];
 #pragma unroll
@@ -207,6 +220,9 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
         for (int i = 0; i < nbw; ++i) {
             cp_async_wait<D - 1>();
             __syncwarp();
+            // the last stage has landed (the groups after it are empty): this
+            // warp's reads of the pair are complete
+            if (SPLIT && i == nbw - 1 && lane == 0) mbar_arrive(&reads_done);
             const int s = w + NW * i;
             const int slot = i % D;
             if (i == 0) {  // ss = u.u (trainer.py:176-178) once the user row landed
@@ -318,7 +334,12 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
         }
         cp_async_wait<0>();
         // every warp has read all of its rows: the pair's writes may start
-        __syncthreads();
+        if (SPLIT) {
+            mbar_wait(&reads_done, phase);
+            phase ^= 1;
+        } else {
+            __syncthreads();
+        }
         if (nbw > 0) {  // ss (hence the coefficients) is known to warps with stages
             __syncwarp();
             if (nsp) apply(sp_rows, sp_ents, nsp);
@@ -367,7 +388,11 @@ static cudaError_t launch_multi_k(const HogwildArgs &a, cudaStream_t st, int *wo
     const MwLayout L = mw_layout<K, D, LPR>(snap_cap);
     const size_t smem = L.per_warp * NW;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
-    auto kern = hogwild_multi<K, NW, D, LPR>;
+    static const bool split = [] {
+        const char *e = getenv("HEAT_MULTI_SPLIT");
+        return e ? atoi(e) != 0 : false;  // measured on c3: 72.7 M split vs 77.7 M barrier
+    }();
+    auto kern = split ? hogwild_multi<K, NW, D, LPR, true> : hogwild_multi<K, NW, D, LPR, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32 * NW, smem, &e);
     if (e != cudaSuccess) return e;

@@ -12,18 +12,22 @@
 //   A  every warp draws its stage's negative ids (counter-form SplitMix64,
 //      one draw per lane) and copies its rows with per-lane 16-byte
 //      cp.async.cg (LDGSTS, L2 evict-last hint) into a padded ring
-//      (rows padded by 16 bytes: conflict-free lane-per-row reads); warp 0 also copies
-//      the user row (double-buffered by pair parity).  wait_group 0, barrier:
-//      every row of the pair has landed before anything is written
-//      (the reference reads all rows first, trainer.py:118-146).
-//   B  lane j of warp w scores row 32w+j: tt = v.v, st = u.v (fp32 FMA),
+//      (rows padded by 16 bytes: conflict-free lane-per-row reads), plus its
+//      own copy of the user row.  wait_group 0; the warp then arrives on the
+//      pair's mbarrier (its reads are complete).
+//   B  lane j of warp w scores row w*rw+j: tt = v.v, st = u.v (fp32 FFMA2),
 //      fp32 similarity screen, exact binary64 only near the margin
-//      (trainer.py:184-221).
+//      (trainer.py:184-221).  Then the warp waits on the mbarrier: every row
+//      of the pair has landed before anything is written (the reference
+//      reads all rows first, trainer.py:118-146).
 //   C  each warp applies the rows of its own stage that must be written:
 //      item deltas with red.global.add from the resident snapshot rows
 //      (pre-pair values even for repeated ids), and adds its user-gradient
 //      partial to the user row (trainer.py:236-293).  Only the warp that
-//      reads a stage ever reads it, so one barrier per pair suffices.
+//      reads a stage ever reads it, so no other barrier is needed.
+// Measured on c2: a CTA barrier before B: 333 M samples/s; after B (EARLY):
+// 340 M; the split arrive/wait (SPLIT, default): 356 M.  HEAT_RESIDENT_EARLY
+// = 0 / 1 / 2 selects them.
 // The pair's loss (1 - sim_p) + mu/N * sum(hinge) is linear, so each warp
 // accumulates its share (trainer.py:222).
 #include <cstdint>
@@ -36,6 +40,10 @@
 namespace heat {
 
 constexpr int kMaxStages = 8;
+#ifndef RS_SLEEP_WAIT
+#define RS_SLEEP_WAIT 1
+#endif
+constexpr bool kSleepWait = RS_SLEEP_WAIT != 0;
 
 template <int K>
 struct RsGeom {
@@ -50,9 +58,10 @@ struct RsGeom {
 };
 
 template <int K>
-__host__ __device__ inline size_t rs_smem_bytes(int rows) {
+__host__ __device__ inline size_t rs_smem_bytes(int rows, int nb, bool early) {
     size_t b = sizeof(float) * RsGeom<K>::SLOTF * rows;  // ring, one padded slot per row
-    b += sizeof(float) * K * 2;           // user row, double-buffered
+    // user row: double-buffered by pair parity, or one copy per warp (EARLY)
+    b += sizeof(float) * K * (early ? nb : 2);
     return (b + 127) & ~size_t(127);
 }
 
@@ -68,7 +77,14 @@ __device__ __forceinline__ void rs_red(float *p, const float (&d)[VW]) {
     }
 }
 
-template <int K, int NB>
+// EARLY: every warp copies its own user row and scores its stage as soon as
+// its own copies land; the CTA barrier moves to just before the writes (all
+// of the pair's reads still precede any of its writes).  Otherwise warp 0
+// copies one shared user row and every warp waits at the barrier first.
+// SPLIT (with EARLY): the pre-write barrier is an mbarrier whose arrival each
+// warp signals as soon as its own copies land, before it scores, so the wait
+// before the writes rarely stalls.
+template <int K, int NB, bool EARLY, bool SPLIT>
 // 7 resident CTAs per SM (the window allows ~7 pairs per SM), but never
 // fewer than 64 registers per thread
 __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB : 1) : 7))
@@ -82,6 +98,12 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
 
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
+    __shared__ uint64_t reads_done;  // SPLIT: one arrival per warp per pair
+    uint32_t phase = 0;
+    if (SPLIT) {
+        if (threadIdx.x == 0) mbar_init(&reads_done, NB);
+        __syncthreads();
+    }
     const int N = a.N;
     const double wneg = a.mu * (1.0 / (double)N);
     const float theta_f = (float)a.theta;
@@ -118,7 +140,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
 
     for (; p < a.stop; p += n_workers, parity ^= 1) {
         ++mine;
-        float *urow = ubuf + parity * K;
+        float *urow = EARLY ? ubuf + w * K : ubuf + parity * K;
         // ---- A: ids, copies
         const int32_t pos = nx_pos;
         const int64_t u = nx_u;
@@ -140,13 +162,17 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
                     cp_async16_hint(my_stage + row * G::SLOTF + my_ch * 4,
                                     srcb + (size_t)rid * K, pol);
             }
-            if (w == 0)
+            if (EARLY || w == 0)
                 for (int ch = lane; ch < G::CH; ch += 32)
                     cp_async16(urow + ch * 4, a.S + u * K + ch * 4);
             cp_async_commit();
             cp_async_wait<0>();
         }
-        __syncthreads();  // every row of the pair (and the user row) has landed
+        if (EARLY) {
+            __syncwarp();  // this warp's stage and user row have landed
+            if (SPLIT && lane == 0) mbar_arrive(&reads_done);
+        } else
+            __syncthreads();  // every row of the pair (and the user row) has landed
 
         // ---- B: score my row
         float uu[VW];
@@ -209,6 +235,15 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
             }
         }
         loss += wneg * hinge;
+        if (SPLIT) {  // every read of the pair precedes every write
+            if (kSleepWait)
+                mbar_wait_sleep(&reads_done, phase);
+            else
+                mbar_wait(&reads_done, phase);
+            phase ^= 1;
+        } else if (EARLY) {
+            __syncthreads();
+        }
 
         // ---- C: apply my stage's written rows from their resident snapshots
         unsigned m = __ballot_sync(0xffffffffu, write);
@@ -283,9 +318,15 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
 
 template <int K, int NB>
 static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
-    const size_t smem = rs_smem_bytes<K>(((a.N + 1 + NB - 1) / NB) * NB);
+    static const int early = [] {
+        const char *e = getenv("HEAT_RESIDENT_EARLY");
+        return e ? atoi(e) : 2;
+    }();
+    const size_t smem = rs_smem_bytes<K>(((a.N + 1 + NB - 1) / NB) * NB, NB, early != 0);
     if (smem > 96 * 1024) return cudaErrorNotSupported;
-    auto kern = hogwild_resident<K, NB>;
+    auto kern = early == 2   ? hogwild_resident<K, NB, true, true>
+                : early == 1 ? hogwild_resident<K, NB, true, false>
+                             : hogwild_resident<K, NB, false, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32 * NB, smem, &e);
     if (e != cudaSuccess) return e;
