@@ -1021,7 +1021,7 @@ def test_c2_recall_parity_throughput_vs_deterministic(torch_cuda):
     """north_star: final recall@20 within 0.5 % absolute.  Full config 2, a
     few epochs: the throughput kernel (B = 1024 in flight) against the
     deterministic kernel, which is bit-identical to the reference's single
-    thread.  (20 epochs: 0.1659 vs 0.1654, profiles/r01_quality_c2.json.)"""
+    thread.  (20 epochs: 0.1650 vs 0.1654, profiles/r01_quality_c2.json.)"""
     from paper_2304_07334_b200 import _native as N
     from paper_2304_07334_b200 import LossParams, TrainingConfig
     from paper_2304_07334_b200.dataset import epoch_pairs
