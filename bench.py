@@ -265,7 +265,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="host seconds for each cpu_baseline sample (16 threads, 1 thread)")
     ap.add_argument("--ref-sample", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     args = ap.parse_args()
     args.e2e_steps = max(0, args.e2e_steps)
     if args.impl == "reference":

@@ -33,12 +33,16 @@ a = np.median(np.array(rows), axis=0) * 1e3
 print(json.dumps({"what": "e2e_breakdown", "config": cfg_name, "wall_ms": a[0], "upload_ms": a[1],
                   "kernel_ms": a[2], "writeback_ms": a[3], "other_ms": a[0] - a[1] - a[2] - a[3],
                   "pairs": int(tr.num_pairs)}))
-# plain copy rates for reference
+# plain copy rates for reference (best of 5 per direction)
 x = torch.empty(64 << 20, dtype=torch.uint8).pin_memory()
 y = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     y.copy_(x, non_blocking=True)
 torch.cuda.synchronize()
-t0 = time.perf_counter(); y.copy_(x, non_blocking=True); torch.cuda.synchronize(); h2d = time.perf_counter() - t0
-t0 = time.perf_counter(); x.copy_(y, non_blocking=True); torch.cuda.synchronize(); d2h = time.perf_counter() - t0
+h2d = d2h = float("inf")
+for _ in range(5):
+    t0 = time.perf_counter(); y.copy_(x, non_blocking=True); torch.cuda.synchronize()
+    h2d = min(h2d, time.perf_counter() - t0)
+    t0 = time.perf_counter(); x.copy_(y, non_blocking=True); torch.cuda.synchronize()
+    d2h = min(d2h, time.perf_counter() - t0)
 print(json.dumps({"what": "pcie", "h2d_GBps": (64 << 20) / h2d / 1e9, "d2h_GBps": (64 << 20) / d2h / 1e9}))
