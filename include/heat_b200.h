@@ -104,8 +104,11 @@ typedef struct heat_counters {
  * `agg` (optional) turns on behaviour aggregation.  HEAT_MODE_EXACT follows
  * the reference's single thread bit for bit (accu/counter carry the flush
  * state).  HEAT_MODE_HOGWILD runs steps of `window` pairs (4096 when <= 0)
- * with W frozen inside a step and every pair's (agg_lr/mini_batch) *
- * pooled (x) ugrad added to W after it (accu/counter unused); `scratch` is then
+ * with W frozen inside a step; every pair's (agg_lr/mini_batch) * pooled (x)
+ * ugrad reaches W on the reference's flush schedule: when the pair's
+ * mini-batch (epoch position / mini_batch) completes, the incomplete one
+ * waiting in `accu` (counter unused; with accu NULL every pair goes straight
+ * to W after its step); `scratch` is then
  * NULL or at least heat_agg_scratch_bytes(dim, window) bytes.  DELTA mode
  * returns HEAT_ERR_UNSUPPORTED.
  * Scratch (HEAT_MODE_EXACT): `scratch` may be NULL (internal allocation) or a

@@ -19,8 +19,11 @@
 //                 + l2*T[hist])  (trainer.py:316-326)
 //
 // Every pair contributes agg_lr/mini_batch * P (x) G to W exactly as in the
-// reference; only the staleness differs (one step instead of threads x
-// mini_batch pairs).  The GEMMs are K x K x C with K <= 128: about 2*C*K^2
+// reference, on the reference's flush schedule: a mini-batch's contributions
+// reach W when its last pair is done (those of an incomplete batch wait in the
+// fp64 accumulator, and the epoch's last incomplete batch is dropped, as the
+// reference's per-epoch thread state drops it).  Only the staleness differs
+// (one step instead of threads x mini_batch pairs).  The GEMMs are K x K x C with K <= 128: about 2*C*K^2
 // flops per step (67 MFLOP for C = 2048, K = 128), a few percent of the
 // step's gather traffic, so they stay on the FMA pipes (fp32 like the tables)
 // instead of a tensor-core pipeline whose setup would dominate.
@@ -190,10 +193,13 @@ __global__ void __launch_bounds__(256)
 // grid.x = output tiles of TA x TA (TA = 16R), grid.y = chunks of RC pairs;
 // a 16 x 16 thread grid, R x R outputs per thread, partial sums added with
 // vector reductions.
-template <int K>
+// TO_ACCU: the partial sums go, unscaled, into the fp64 pending accumulator
+// (pairs of a mini-batch that has not completed yet) instead of into W.
+template <int K, bool TO_ACCU>
 __global__ void __launch_bounds__(256)
     agg_wgrad_kernel(const float *__restrict__ P, const float *__restrict__ G, int64_t n,
-                     int64_t rows_per_cta, float *__restrict__ W, float scale) {
+                     int64_t rows_per_cta, float *__restrict__ W, double *__restrict__ accu,
+                     float scale) {
     constexpr int R = K >= 64 ? 4 : (K == 32 ? 2 : 1);
     constexpr int TA = 16 * R;
     constexpr int TILES = K / TA;
@@ -246,6 +252,15 @@ __global__ void __launch_bounds__(256)
         }
         __syncthreads();
     }
+    if constexpr (TO_ACCU) {
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                atomicAdd(accu + (int64_t)(a0 + ty * R + i) * K + b0 + tx * R + j,
+                          (double)acc[i][j]);
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
         float *dst = W + (int64_t)(a0 + ty * R + i) * K + b0 + tx * R;
@@ -258,6 +273,16 @@ __global__ void __launch_bounds__(256)
             atomicAdd(dst, scale * acc[i][0]);
         }
     }
+}
+
+// ---- 4a. flush of the pending accumulator once its mini-batch completes ----
+// W = f32(f64(W) + scale * accu), accu = 0 (trainer.py:310-316)
+__global__ void agg_flush_kernel(float *__restrict__ W, double *__restrict__ accu, int kk,
+                                 double scale) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= kk) return;
+    W[i] = (float)((double)W[i] + scale * accu[i]);
+    accu[i] = 0.0;
 }
 
 // ---- 5b. history rows: T[h] -= lr * ((1-gamma)/len * WH[m] + l2 * T[h]) ---------
@@ -343,10 +368,38 @@ static cudaError_t run_agg(const HogwildArgs &base, const heat_agg_params &agg, 
         constexpr int TILES = K / (16 * R);
         // ~2 CTAs per SM over the output tiles x pair chunks
         const int64_t want = std::max<int64_t>(1, 2 * sm_count() / (TILES * TILES));
-        int64_t rpc = std::max<int64_t>(32, (n + want - 1) / want);
-        rpc = (rpc + 31) / 32 * 32;
-        const dim3 wg((unsigned)(TILES * TILES), (unsigned)((n + rpc - 1) / rpc));
-        agg_wgrad_kernel<K><<<wg, 256, 0, st>>>(P, G, n, rpc, agg.W, wscale);
+        // the reference's flush schedule (trainer.py:300-316, one accumulator):
+        // pair q of the epoch joins mini-batch q / mini_batch, whose
+        // contributions reach W only once it is complete; an incomplete
+        // batch waits in the fp64 accumulator (dropped at the epoch's end,
+        // like the reference's per-epoch thread state).  c0 pairs of the
+        // current batch precede this step.
+        const int64_t mb = agg.mini_batch;
+        const int64_t c0 = s % mb;
+        const int64_t cut = std::min<int64_t>(n, std::max<int64_t>(0, (c0 + n) / mb * mb - c0));
+        if (c0 > 0 && c0 + n >= mb && agg.accu) {  // the pending batch completes here
+            const int kk = K * K;
+            agg_flush_kernel<<<(kk + 255) / 256, 256, 0, st>>>(agg.W, agg.accu, kk,
+                                                               -agg.lr / (double)mb);
+        }
+        auto wgrad = [&](int64_t r0, int64_t rn, bool to_accu) {
+            if (rn <= 0) return;
+            int64_t rpc = std::max<int64_t>(32, (rn + want - 1) / want);
+            rpc = (rpc + 31) / 32 * 32;
+            const dim3 wg((unsigned)(TILES * TILES), (unsigned)((rn + rpc - 1) / rpc));
+            if (to_accu)
+                agg_wgrad_kernel<K, true><<<wg, 256, 0, st>>>(P + r0 * K, G + r0 * K, rn, rpc,
+                                                              agg.W, agg.accu, 1.f);
+            else
+                agg_wgrad_kernel<K, false><<<wg, 256, 0, st>>>(P + r0 * K, G + r0 * K, rn, rpc,
+                                                               agg.W, nullptr, wscale);
+        };
+        if (agg.accu) {
+            wgrad(0, cut, false);
+            wgrad(cut, n - cut, true);
+        } else {  // no accumulator given: every pair straight into W
+            wgrad(0, n, false);
+        }
         if (agg.history_grad) {
             agg_gemm_kernel<K, true><<<gblocks, 256, GSM, st>>>(G, agg.W, n, Q, nullptr,
                                                                 nullptr, 0.f);

@@ -1,0 +1,205 @@
+"""The reference's own trainer behaviours, restated against the B200 drop-in.
+
+Each test mirrors a behaviour that heatcf's test suite pins for its CPU
+trainer (cited per test: /root/reference/pkg/tests/test_trainer.py), run
+through the public ``train_epoch`` / ``evaluate`` of this package on the GPU.
+``num_threads == 1`` selects the deterministic (EXACT) kernels and
+``num_threads > 1`` the Hogwild throughput kernels, as in the reference.
+Data come from ``synth.make_clustered`` (planted clusters, the same role as
+the reference's clustered fixtures).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2304_07334_b200.trainer import configure
+    configure(mode=None, window=0, fp64=False)  # the reference's thread-count mapping
+    return torch
+
+
+def clustered_small():
+    from paper_2304_07334_b200.synth import make_clustered
+    return make_clustered(60, 240, 6, 24, seed=3)
+
+
+def clustered_medium():
+    from paper_2304_07334_b200.synth import make_clustered
+    return make_clustered(800, 1600, 16, 40, affinity=0.97, seed=11)
+
+
+def fresh(train_set, dim=16, seed_s=1, seed_t=2):
+    from paper_2304_07334_b200 import InitSpec, init_matrix
+    return (init_matrix(train_set.num_users, dim, InitSpec(seed=seed_s)),
+            init_matrix(train_set.num_items, dim, InitSpec(seed=seed_t)))
+
+
+def base_cfg(**kw):
+    from paper_2304_07334_b200 import TrainingConfig
+    d = dict(emb_dim=16, num_negatives=8, learning_rate=0.05, epochs=5, num_threads=1, seed=7)
+    d.update(kw)
+    return TrainingConfig(**d)
+
+
+def xavier(dim, seed):
+    from paper_2304_07334_b200 import InitSpec, init_matrix
+    return init_matrix(dim, dim, InitSpec(kind="xavier", seed=seed)).values
+
+
+def test_reruns_are_bit_identical_single_thread(torch_cuda):
+    """test_trainer.py:27-36 (one thread: bit-identical reruns).  The
+    deterministic kernel also reruns bit-identically with the aggregator on
+    (test_trainer.py:38-52 without the tiling sampler, which is outside the
+    built path)."""
+    from paper_2304_07334_b200 import AggregatorConfig
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, _ = clustered_small()
+    for agg in (False, True):
+        cfg = base_cfg(aggregator=AggregatorConfig(enabled=agg, max_history=20))
+        outs = []
+        for _ in range(2):
+            S, T = fresh(train_set)
+            W = xavier(16, 9) if agg else None
+            for e in range(3):
+                train_epoch(S, T, train_set, cfg, W, epoch=e)
+            outs.append((S.values.tobytes(), T.values.tobytes(),
+                         W.tobytes() if agg else b""))
+        assert outs[0] == outs[1]
+
+
+def test_two_threads_complete_and_learn(torch_cuda):
+    """test_trainer.py:190-197: the multi-thread (Hogwild) mode finishes
+    every epoch with finite tables and a falling loss."""
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, _ = clustered_small()
+    cfg = base_cfg(num_threads=2, epochs=6)
+    S, T = fresh(train_set)
+    losses = [train_epoch(S, T, train_set, cfg, epoch=e).mean_loss for e in range(6)]
+    assert np.isfinite(losses).all() and losses[-1] < losses[0]
+    assert np.isfinite(S.values).all() and np.isfinite(T.values).all()
+
+
+def test_thread_count_parity_on_converged_data(torch_cuda):
+    """test_trainer.py:199-208: recall@20 after 25 epochs with 1 and 2
+    threads (here: the deterministic and the Hogwild kernels) within 0.01."""
+    from paper_2304_07334_b200.evaluator import evaluate
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, test_set = clustered_medium()
+    recalls = {}
+    for threads in (1, 2):
+        cfg = base_cfg(emb_dim=32, num_negatives=16, num_threads=threads)
+        S, T = fresh(train_set, dim=32)
+        for e in range(25):
+            train_epoch(S, T, train_set, cfg, epoch=e)
+        recalls[threads] = evaluate(S, T, train_set, test_set, cfg, k=20).recall_at_k
+    assert abs(recalls[1] - recalls[2]) <= 0.01, recalls
+
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_report_fields(torch_cuda, threads):
+    """test_trainer.py:210-222: EpochReport fields, the six phase keys, phase
+    times within the wall time and a positive read phase (here the measured
+    upload)."""
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, _ = clustered_small()
+    S, T = fresh(train_set)
+    rep = train_epoch(S, T, train_set, base_cfg(num_threads=threads), epoch=0,
+                      collect_phases=True)
+    assert rep.num_pairs == train_set.num_pairs and rep.num_threads == threads
+    assert np.isfinite(rep.mean_loss)
+    assert set(rep.phase_times) == {"read_emb", "similarity", "loss", "gradient", "update",
+                                    "aggregate"}
+    assert sum(rep.phase_times.values()) <= rep.wall_time
+    assert rep.phase_times["read_emb"] > 0
+
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_aggregator_schedule(torch_cuda, threads):
+    """test_trainer.py:225-259: W untouched while the mini-batch exceeds the
+    epoch, updated once it is reached; a disabled aggregator never reads or
+    writes W and leaves training unchanged."""
+    from paper_2304_07334_b200 import AggregatorConfig
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, _ = clustered_small()
+    big = AggregatorConfig(enabled=True, mini_batch_size=train_set.num_pairs + 1,
+                           max_history=20)
+    S, T = fresh(train_set)
+    W = xavier(16, 9)
+    before = W.copy()
+    train_epoch(S, T, train_set, base_cfg(num_threads=threads, aggregator=big), W, epoch=0)
+    assert np.array_equal(W, before)
+
+    small = AggregatorConfig(enabled=True, mini_batch_size=32, max_history=20)
+    S, T = fresh(train_set)
+    train_epoch(S, T, train_set, base_cfg(num_threads=threads, aggregator=small), W, epoch=0)
+    assert not np.array_equal(W, before)
+
+    if threads == 1:  # pass-through is a bitwise statement: deterministic mode
+        cfg_off = base_cfg()
+        S1, T1 = fresh(train_set)
+        train_epoch(S1, T1, train_set, cfg_off, weights=None, epoch=0)
+        W2 = xavier(16, 9)
+        w_before = W2.copy()
+        S2, T2 = fresh(train_set)
+        train_epoch(S2, T2, train_set, cfg_off, weights=W2, epoch=0)
+        assert np.array_equal(W2, w_before)
+        assert S1.values.tobytes() == S2.values.tobytes()
+        assert T1.values.tobytes() == T2.values.tobytes()
+
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_dot_similarity_trains(torch_cuda, threads):
+    """test_trainer.py:262-269."""
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, _ = clustered_small()
+    cfg = base_cfg(similarity="dot", learning_rate=0.01, num_threads=threads)
+    S, T = fresh(train_set)
+    losses = [train_epoch(S, T, train_set, cfg, epoch=e).mean_loss for e in range(5)]
+    assert np.isfinite(losses).all()
+    assert np.isfinite(S.values).all() and np.isfinite(T.values).all()
+
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_decay_reaches_sampled_rows_only(torch_cuda, threads):
+    """test_trainer.py:273-289: with mu = 0 only the positive row moves;
+    with l2 the sampled negatives decay too (at most 1 + 4 rows change)."""
+    from paper_2304_07334_b200 import LossParams, TrainingConfig, from_user_lists
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set = from_user_lists({0: [0]}, num_users=1, num_items=500)
+    base = dict(emb_dim=8, num_negatives=4, learning_rate=0.05, num_threads=threads, seed=7,
+                loss=LossParams(mu=0.0, theta=0.8))
+    S0, T0 = fresh(train_set, dim=8)
+    before = T0.values.copy()
+    train_epoch(S0, T0, train_set, TrainingConfig(**base), epoch=0)
+    assert list(np.flatnonzero(np.any(T0.values != before, axis=1))) == [0]
+    S1, T1 = fresh(train_set, dim=8)
+    train_epoch(S1, T1, train_set, TrainingConfig(**base, l2_reg=0.1), epoch=0)
+    changed = np.flatnonzero(np.any(T1.values != before, axis=1))
+    assert 0 in changed and 1 < len(changed) <= 5
+
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_decay_shrinks_updated_rows(torch_cuda, threads):
+    """test_trainer.py:291-306: at the cosine maximum the similarity gradient
+    is zero, so one pair scales the user row by exactly (1 - lr * l2)."""
+    from paper_2304_07334_b200 import EmbeddingMatrix, LossParams, from_user_lists
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set = from_user_lists({0: [0]}, num_users=1, num_items=2)
+    cfg = base_cfg(emb_dim=4, num_negatives=1, learning_rate=0.1, l2_reg=1.0,
+                   num_threads=threads, loss=LossParams(mu=0.0, theta=0.8))
+    row = np.array([[1.0, 2.0, -1.0, 0.5]], dtype=np.float32)
+    S = EmbeddingMatrix(row.copy())
+    T = EmbeddingMatrix(np.vstack([row, row]).astype(np.float32))
+    norm_before = np.linalg.norm(S.values[0])
+    train_epoch(S, T, train_set, cfg, epoch=0)
+    assert np.allclose(S.values[0], 0.9 * row[0], rtol=1e-6)
+    assert np.linalg.norm(S.values[0]) < norm_before
