@@ -298,3 +298,11 @@ def test_native_epoch_shuffle_is_numpy_bit_identical():
     t0 = time.perf_counter(); epoch_pairs(tr, 5); t1 = time.perf_counter()
     epoch_pairs_numpy(tr, 5); t2 = time.perf_counter()
     print(f"native shuffle {1e3*(t1-t0):.1f} ms vs numpy {1e3*(t2-t1):.1f} ms")
+
+
+def test_metrics_json_schema():
+    """test_evaluator.py:176-181 of the reference: one JSON object per line."""
+    import json
+    from paper_2304_07334_b200.evaluator import MetricsReport, metrics_json
+    obj = json.loads(metrics_json(3, MetricsReport(0.5, 0.25, 20, 11)))
+    assert obj == {"epoch": 3, "recall@20": 0.5, "ndcg@20": 0.25, "users": 11}

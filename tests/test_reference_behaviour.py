@@ -203,3 +203,132 @@ def test_decay_shrinks_updated_rows(torch_cuda, threads):
     train_epoch(S, T, train_set, cfg, epoch=0)
     assert np.allclose(S.values[0], 0.9 * row[0], rtol=1e-6)
     assert np.linalg.norm(S.values[0]) < norm_before
+
+
+# ---- evaluation (test_evaluator.py) -----------------------------------------
+
+def _matrix(rows):
+    from paper_2304_07334_b200 import EmbeddingMatrix
+    return EmbeddingMatrix(np.array(rows, dtype=np.float32))
+
+
+def _plain_cfg(similarity="cosine", dim=2):
+    from paper_2304_07334_b200 import TrainingConfig
+    return TrainingConfig(emb_dim=dim, num_negatives=1, learning_rate=0.1, num_threads=1,
+                          similarity=similarity)
+
+
+def _full_sort_metrics(S, T, train, test, k, similarity="cosine", user_vectors=None):
+    """Recall@k / NDCG@k by full sorts (score desc, id asc), in binary64 —
+    the role of the reference's helpers.brute_force_metrics."""
+    import math
+    rec, nd = [], []
+    Tv = T.values.astype(np.float64)
+    for u in range(test.num_users):
+        want = set(int(i) for i in test.items[test.offsets[u]:test.offsets[u + 1]])
+        if not want:
+            continue
+        q = np.asarray(user_vectors[u] if user_vectors is not None else S.values[u],
+                       dtype=np.float64)
+        sc = Tv @ q
+        if similarity == "cosine":
+            sc = sc / (np.linalg.norm(Tv, axis=1) * np.linalg.norm(q))
+        excl = set(int(i) for i in train.items[train.offsets[u]:train.offsets[u + 1]]) \
+            if u < train.num_users else set()
+        top = sorted((i for i in range(len(sc)) if i not in excl),
+                     key=lambda i: (-float(sc[i]), i))[:k]
+        hits = [r for r, i in enumerate(top, start=1) if i in want]
+        idcg = sum(1.0 / math.log2(r + 1) for r in range(1, min(k, len(want)) + 1))
+        rec.append(len(hits) / len(want))
+        nd.append(sum(1.0 / math.log2(r + 1) for r in hits) / idcg)
+    return sum(rec) / len(rec), sum(nd) / len(nd), len(rec)
+
+
+def test_eval_perfect_rank_and_half_coverage(torch_cuda):
+    """test_evaluator.py:58-75."""
+    from paper_2304_07334_b200 import from_user_lists
+    from paper_2304_07334_b200.evaluator import evaluate
+    S = _matrix([[1, 0]])
+    train = from_user_lists({}, num_users=1, num_items=3)
+    m = evaluate(S, _matrix([[1, 0.01], [0, 1], [-1, 0]]), train,
+                 from_user_lists({0: [0]}, num_users=1, num_items=3), _plain_cfg(), k=1)
+    assert m.recall_at_k == 1.0 and m.ndcg_at_k == 1.0
+    m = evaluate(S, _matrix([[1, 0.01], [0, 1], [0.9, 0.1]]), train,
+                 from_user_lists({0: [0, 1]}, num_users=1, num_items=3), _plain_cfg(), k=2)
+    assert m.recall_at_k == pytest.approx(0.5)
+
+
+def test_eval_users_without_test_items_and_empty_test_set(torch_cuda):
+    """test_evaluator.py:77-93."""
+    from paper_2304_07334_b200 import from_user_lists
+    from paper_2304_07334_b200.evaluator import EmptyTestSetError, evaluate
+    S = _matrix([[1, 0], [0, 1]])
+    T = _matrix([[1, 0], [0, 1]])
+    m = evaluate(S, T, from_user_lists({}, num_users=2, num_items=2),
+                 from_user_lists({0: [0]}, num_users=2, num_items=2), _plain_cfg(), k=1)
+    assert m.users_evaluated == 1
+    with pytest.raises(EmptyTestSetError):
+        evaluate(_matrix([[1, 0]]), _matrix([[1, 0]]),
+                 from_user_lists({0: [0]}, num_users=1, num_items=1),
+                 from_user_lists({}, num_users=1, num_items=1), _plain_cfg(), k=1)
+
+
+def test_eval_five_users_match_full_sort(torch_cuda):
+    """test_evaluator.py:109-123 (cosine and dot, exact to 1e-12), plus the
+    metrics staying in [0, 1] (test_evaluator.py:125-137)."""
+    from paper_2304_07334_b200 import EmbeddingMatrix, from_user_lists
+    from paper_2304_07334_b200.evaluator import evaluate
+    rng = np.random.default_rng(1234)
+    S = EmbeddingMatrix(rng.standard_normal((5, 6)).astype(np.float32))
+    T = EmbeddingMatrix(rng.standard_normal((80, 6)).astype(np.float32))
+    train = from_user_lists({u: rng.integers(0, 80, 15) for u in range(5)}, num_users=5,
+                            num_items=80)
+    test = from_user_lists(
+        {u: np.setdiff1d(np.unique(rng.integers(0, 80, 8)),
+                         train.items[train.offsets[u]:train.offsets[u + 1]]) for u in range(5)},
+        num_users=5, num_items=80)
+    for sim in ("cosine", "dot"):
+        m = evaluate(S, T, train, test, _plain_cfg(sim, dim=6), k=10)
+        rec, nd, users = _full_sort_metrics(S, T, train, test, 10, sim)
+        assert m.recall_at_k == pytest.approx(rec, abs=1e-12)
+        assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12)
+        assert m.users_evaluated == users
+        assert 0.0 <= m.recall_at_k <= 1.0 and 0.0 <= m.ndcg_at_k <= 1.0
+
+
+def test_eval_better_rank_never_lowers_ndcg(torch_cuda):
+    """test_evaluator.py:139-151."""
+    from paper_2304_07334_b200 import from_user_lists
+    from paper_2304_07334_b200.evaluator import evaluate
+    train = from_user_lists({}, num_users=1, num_items=6)
+    test = from_user_lists({0: [5]}, num_users=1, num_items=6)
+    nds = []
+    for angle in (0.9, 0.6, 0.3, 0.1):
+        rows = [[np.cos(a), np.sin(a)] for a in (0.2, 0.35, 0.5, 0.65, 0.8)]
+        rows.append([np.cos(angle), np.sin(angle)])
+        nds.append(evaluate(_matrix([[1, 0]]), _matrix(rows), train, test, _plain_cfg(),
+                            k=4).ndcg_at_k)
+    assert all(b >= a for a, b in zip(nds, nds[1:]))
+
+
+def test_eval_aggregated_query_is_history_mean(torch_cuda):
+    """test_evaluator.py:153-174: gamma = 0 and identity weights make the
+    query the mean of the user's history rows."""
+    from paper_2304_07334_b200 import (AggregatorConfig, EmbeddingMatrix, TrainingConfig,
+                                       from_user_lists)
+    from paper_2304_07334_b200.evaluator import evaluate
+    rng = np.random.default_rng(99)
+    nu, ni, k = 3, 30, 4
+    S = EmbeddingMatrix(rng.standard_normal((nu, k)).astype(np.float32))
+    T = EmbeddingMatrix(rng.standard_normal((ni, k)).astype(np.float32))
+    train = from_user_lists({u: np.arange(u, u + 5) for u in range(nu)}, num_users=nu,
+                            num_items=ni)
+    test = from_user_lists({u: [ni - 1 - u] for u in range(nu)}, num_users=nu, num_items=ni)
+    cfg = TrainingConfig(emb_dim=k, num_negatives=1, learning_rate=0.1, num_threads=1,
+                         aggregator=AggregatorConfig(enabled=True, gamma=0.0, max_history=100))
+    m = evaluate(S, T, train, test, cfg, weights=np.eye(k, dtype=np.float32), k=5)
+    pooled = np.stack([T.values[train.items[train.offsets[u]:train.offsets[u + 1]]]
+                       .astype(np.float64).mean(axis=0) for u in range(nu)])
+    rec, nd, _ = _full_sort_metrics(S, T, train, test, 5, "cosine", user_vectors=pooled)
+    assert m.recall_at_k == pytest.approx(rec, abs=1e-12)
+    assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12)
