@@ -332,3 +332,97 @@ def test_eval_aggregated_query_is_history_mean(torch_cuda):
     rec, nd, _ = _full_sort_metrics(S, T, train, test, 5, "cosine", user_vectors=pooled)
     assert m.recall_at_k == pytest.approx(rec, abs=1e-12)
     assert m.ndcg_at_k == pytest.approx(nd, abs=1e-12)
+
+
+# ---- descent, sparse updates, orchestration (test_trainer.py) ----------------
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_toy_problem_and_clustered_loss_trend(torch_cuda, threads):
+    """test_trainer.py:76-91: one pair, 50 epochs: the loss falls; clustered
+    data, 10 epochs: at most one epoch-to-epoch increase."""
+    from paper_2304_07334_b200 import from_user_lists
+    from paper_2304_07334_b200.trainer import train_epoch
+    toy = from_user_lists({0: [0]}, num_users=1, num_items=2)
+    cfg = base_cfg(emb_dim=8, num_negatives=1, learning_rate=0.02, num_threads=threads)
+    S, T = fresh(toy, dim=8)
+    losses = [train_epoch(S, T, toy, cfg, epoch=e).mean_loss for e in range(50)]
+    assert losses[-1] < losses[0] and np.isfinite(losses).all()
+    train_set, _ = clustered_small()
+    S, T = fresh(train_set)
+    cfg = base_cfg(num_threads=threads)
+    losses = [train_epoch(S, T, train_set, cfg, epoch=e).mean_loss for e in range(10)]
+    assert sum(b > a for a, b in zip(losses, losses[1:])) <= 1, losses
+
+
+@pytest.mark.parametrize("threads", [1, 2])
+def test_untouched_rows_bit_unchanged(torch_cuda, threads):
+    """test_trainer.py:94-107: one pair touches its user row and at most the
+    positive plus two sampled negatives; every other row keeps its bits."""
+    from paper_2304_07334_b200 import from_user_lists
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set = from_user_lists({0: [0]}, num_users=10, num_items=1000)
+    cfg = base_cfg(emb_dim=8, num_negatives=2, epochs=1, num_threads=threads)
+    S, T = fresh(train_set, dim=8)
+    s0, t0 = S.values.copy(), T.values.copy()
+    train_epoch(S, T, train_set, cfg, epoch=0)
+    assert list(np.flatnonzero(np.any(S.values != s0, axis=1))) == [0]
+    changed = np.flatnonzero(np.any(T.values != t0, axis=1))
+    assert 1 <= len(changed) <= 3
+    untouched = np.setdiff1d(np.arange(1000), changed)
+    assert np.array_equal(T.values[untouched], t0[untouched])
+
+
+def test_train_orchestration(torch_cuda, tmp_path):
+    """test_trainer.py:137-166: zero epochs report the initial state with one
+    evaluation; the evaluation schedule [5, 10, 10]; final/best checkpoints
+    hold the returned tables."""
+    from paper_2304_07334_b200.embeddings import load_model
+    from paper_2304_07334_b200.trainer import train
+    train_set, test_set = clustered_small()
+    S, T = fresh(train_set)
+    s0 = S.values.copy()
+    res = train(S, T, train_set, test_set, base_cfg(epochs=0))
+    assert np.array_equal(S.values, s0) and res.reports == [] and len(res.evaluations) == 1
+    S, T = fresh(train_set)
+    res = train(S, T, train_set, test_set, base_cfg(epochs=10), eval_interval=5)
+    assert [e for e, _ in res.evaluations] == [5, 10, 10]
+    S, T = fresh(train_set)
+    train(S, T, train_set, test_set, base_cfg(epochs=2), out_dir=str(tmp_path))
+    s2, t2, w2 = load_model(str(tmp_path / "final.ckpt"))
+    assert s2.values.tobytes() == S.values.tobytes() and t2.values.tobytes() == T.values.tobytes()
+    assert w2 is None and (tmp_path / "best.ckpt").exists()
+
+
+def test_resume_matches_uninterrupted(torch_cuda, tmp_path):
+    """test_trainer.py:168-186: 15 + 15 epochs through a checkpoint reach the
+    recall of 30 uninterrupted epochs within 0.005."""
+    from paper_2304_07334_b200.embeddings import load_model, save_model
+    from paper_2304_07334_b200.trainer import train
+    train_set, test_set = clustered_medium()
+    S, T = fresh(train_set, dim=32)
+    full = train(S, T, train_set, test_set, base_cfg(emb_dim=32, num_negatives=16, epochs=30))
+    S1, T1 = fresh(train_set, dim=32)
+    train(S1, T1, train_set, test_set, base_cfg(emb_dim=32, num_negatives=16, epochs=15))
+    save_model(str(tmp_path / "mid.ckpt"), S1, T1)
+    S2, T2, _ = load_model(str(tmp_path / "mid.ckpt"))
+    resumed = train(S2, T2, train_set, test_set, base_cfg(emb_dim=32, num_negatives=16,
+                                                          epochs=15))
+    assert abs(resumed.final_metrics.recall_at_k - full.final_metrics.recall_at_k) <= 0.005
+
+
+def test_single_thread_checkpoints_bit_reproducible(torch_cuda, tmp_path):
+    """test_acceptance.py:360-382 (c12): two single-thread train() runs write
+    byte-identical final checkpoints."""
+    from paper_2304_07334_b200 import TrainingConfig
+    from paper_2304_07334_b200.trainer import train
+    train_set, test_set = clustered_small()
+    cfg = TrainingConfig(emb_dim=16, num_negatives=8, learning_rate=0.05, epochs=3,
+                         num_threads=1, seed=7)
+    blobs = []
+    for name in ("a", "b"):
+        out = tmp_path / name
+        out.mkdir()
+        S, T = fresh(train_set)
+        train(S, T, train_set, test_set, cfg, out_dir=str(out))
+        blobs.append((out / "final.ckpt").read_bytes())
+    assert blobs[0] == blobs[1]
