@@ -426,3 +426,33 @@ def test_single_thread_checkpoints_bit_reproducible(torch_cuda, tmp_path):
         train(S, T, train_set, test_set, cfg, out_dir=str(out))
         blobs.append((out / "final.ckpt").read_bytes())
     assert blobs[0] == blobs[1]
+
+
+# ---- uniform sampler (test_sampler.py:12-37) ---------------------------------
+
+def _sample(n_items, draws, seed_state):
+    import ctypes
+    import torch
+    from paper_2304_07334_b200 import _native as N
+    out = torch.empty(draws, dtype=torch.int32, device="cuda")
+    # one "pair" of `draws` negatives: draw j of stream s0 is mix64(s0 + (j+1) gamma)
+    N.check(N.lib().heat_sample_negatives(seed_state, 0, 1, draws, n_items,
+                                          ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def test_uniform_sampler_behaviour(torch_cuda):
+    """single-item universe, reproducibility, ids in range, per-id frequency
+    within 5 sigma over 64 draws per item, empty universe rejected."""
+    from paper_2304_07334_b200 import _native as N
+    assert list(_sample(1, 5, 0)) == [0] * 5
+    assert np.array_equal(_sample(1000, 50, 42), _sample(1000, 50, 42))
+    out = _sample(37, 500, 3)
+    assert out.min() >= 0 and out.max() < 37
+    n = 10_000
+    draws = 64 * n
+    counts = np.bincount(_sample(n, draws, 2024), minlength=n)
+    sigma = np.sqrt(draws * (1 / n) * (1 - 1 / n))
+    assert np.all(np.abs(counts - draws / n) <= 5 * sigma)
+    assert N.lib().heat_sample_negatives(0, 0, 1, 1, 0, None, None) == N.HEAT_ERR_INVALID
