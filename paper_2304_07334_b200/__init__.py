@@ -10,7 +10,8 @@ own ``train()``, CLI and bench use this path unchanged.
 from .config import AggregatorConfig, LossParams, SamplerConfig, TrainingConfig
 from .dataset import InteractionSet, epoch_pairs, from_pairs, from_user_lists, history_of, \
     with_universe
-from .embeddings import EmbeddingMatrix, InitSpec, init_matrix, load_model, save_model
+from .embeddings import CorruptCheckpointError, EmbeddingMatrix, InitSpec, init_matrix, \
+    load_checkpoint, load_model, save_checkpoint, save_model
 from .rng import SplitMix64, derive_stream, mix64, stream_state
 
 __version__ = "0.1.0"
@@ -35,9 +36,9 @@ def __getattr__(name):
 
 
 __all__ = [
-    "AggregatorConfig", "EmbeddingMatrix", "EpochReport", "InitSpec", "InteractionSet",
+    "AggregatorConfig", "CorruptCheckpointError", "EmbeddingMatrix", "EpochReport", "InitSpec", "InteractionSet",
     "LossParams", "MetricsReport", "SamplerConfig", "SplitMix64", "TrainResult",
     "TrainingConfig", "configure", "derive_stream", "epoch_pairs", "evaluate", "from_pairs",
-    "from_user_lists", "history_of", "init_matrix", "install", "load_model", "mix64",
-    "save_model", "stream_state", "topk_items", "train", "train_epoch", "with_universe",
+    "from_user_lists", "history_of", "init_matrix", "install", "load_checkpoint", "load_model", "mix64",
+    "save_checkpoint", "save_model", "stream_state", "topk_items", "train", "train_epoch", "with_universe",
 ]
