@@ -5,9 +5,10 @@ scale-out of its Hogwild data parallelism (trainer.py:398-447).
 
 One process per GPU (torchrun), ``torch.distributed`` over NCCL.  An epoch's
 pair order is the same on every rank (same ``epoch_pairs`` seed); the global
-step is B consecutive pairs; rank r trains the pairs of the step whose user
-it owns (``u % world == r``), keyed by their GLOBAL epoch position so the
-negatives equal the 1-GPU run's (heat_train_range ``pair_index``).
+step is ``step_pairs`` consecutive pairs (bench.py: the config's B per rank,
+i.e. world * B); rank r trains the pairs of the step whose user it owns
+(``u % world == r``), keyed by their GLOBAL epoch position so the negatives
+equal the 1-GPU run's (heat_train_range ``pair_index``).
 
 Per step, on every rank:
   1. the throughput kernel runs in DELTA mode over the rank's pairs: user rows
