@@ -266,12 +266,13 @@ int heat_sample_negatives(uint64_t stream_base, int64_t first_pair, int64_t npai
     return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "sample_negatives launch");
 }
 
-int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
-                     const int32_t *ep_users, const int32_t *ep_items, int64_t start,
-                     int64_t stop, const heat_sgd_params *p, heat_counters *counters,
-                     int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
-                     int64_t delta_capacity, const int64_t *pair_index,
-                     const heat_agg_params *agg, void *scratch, void *stream) {
+static int train_range_core(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                            const int32_t *ep_users, const int32_t *ep_items, int64_t start,
+                            int64_t stop, const heat_sgd_params *p, heat_counters *counters,
+                            int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
+                            int64_t delta_capacity, const int64_t *pair_index,
+                            const heat_agg_params *agg, void *scratch, void *stream,
+                            const int64_t *range_dev, const uint64_t *s0_dev) {
     if (!p) return fail(HEAT_ERR_INVALID, "null params");
     if (!S || !T || !counters) return fail(HEAT_ERR_INVALID, "null table or counters pointer");
     if (p->dim < 1) return fail(HEAT_ERR_INVALID, "dim must be >= 1, got %d", p->dim);
@@ -347,7 +348,10 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
         a.delta_rows = delta_rows; a.delta_count = delta_count;
         a.delta_capacity = delta_capacity;
         a.pair_index = pair_index;
+        a.range_dev = range_dev;
+        a.s0_dev = s0_dev;
         if (agg) {
+            if (range_dev) return fail(HEAT_ERR_UNSUPPORTED, "aggregation with a device range");
             void *sc = scratch ? scratch
                                : get_scratch(agg_hogwild_scratch_bytes(p->dim, p->window), st);
             if (!sc) return fail(HEAT_ERR_CUDA, "aggregation: scratch allocation failed");
@@ -357,12 +361,26 @@ int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
             break;
         }
         e = launch_hogwild(a, st, nullptr);
+        if (range_dev && e == cudaErrorNotSupported)
+            return fail(HEAT_ERR_UNSUPPORTED, "no kernel family for a device range at dim %d",
+                        p->dim);
         break;
     }
     default:
         return fail(HEAT_ERR_INVALID, "unknown mode %d", p->mode);
     }
     return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "train_range launch");
+}
+
+int heat_train_range(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                     const int32_t *ep_users, const int32_t *ep_items, int64_t start,
+                     int64_t stop, const heat_sgd_params *p, heat_counters *counters,
+                     int32_t *delta_ids, float *delta_rows, int64_t *delta_count,
+                     int64_t delta_capacity, const int64_t *pair_index,
+                     const heat_agg_params *agg, void *scratch, void *stream) {
+    return train_range_core(S, s_rows, T, t_rows, ep_users, ep_items, start, stop, p, counters,
+                            delta_ids, delta_rows, delta_count, delta_capacity, pair_index, agg,
+                            scratch, stream, nullptr, nullptr);
 }
 
 int heat_eval_users(const void *S, int32_t s_f64, const float *T, int64_t t_rows, int32_t dim,
@@ -429,3 +447,29 @@ int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int
 }
 
 }  // extern "C"
+
+namespace heat {
+
+int train_range_device_step(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                            const int32_t *users, const int32_t *items,
+                            const heat_sgd_params *p, heat_counters *counters, int32_t *delta_ids,
+                            float *delta_rows, int64_t *delta_count, int64_t delta_capacity,
+                            const int64_t *pair_index, const int64_t *range_dev,
+                            const uint64_t *s0_dev, void *stream) {
+    // grid sized for the window (start/stop only bound it); the kernel reads
+    // the step's real range and stream base from range_dev / s0_dev
+    return train_range_core(S, s_rows, T, t_rows, users, items, 0, (int64_t)1 << 40, p, counters,
+                            delta_ids, delta_rows, delta_count, delta_capacity, pair_index,
+                            nullptr, nullptr, stream, range_dev, s0_dev);
+}
+
+bool device_step_supported(const heat_sgd_params *p, const float *S, const float *T) {
+    if (!p || p->mode != HEAT_MODE_DELTA) return false;
+    if (p->dim != 16 && p->dim != 32 && p->dim != 64 && p->dim != 128) return false;
+    if (((uintptr_t)S % 16) || ((uintptr_t)T % 16)) return false;
+    const char *impl = getenv("HEAT_HOGWILD_IMPL");
+    if (getenv("HEAT_FORCE_GENERIC")) return false;
+    return !impl || impl[0] == 'r' || impl[0] == 'm' || impl[0] == 's' || impl[0] == 't';
+}
+
+}  // namespace heat

@@ -496,6 +496,7 @@ cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *worke
         cudaError_t e = launch_hogwild_staged(a, stream, workers_out, impl && impl[0] == 't');
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
+    if (a.range_dev) return cudaErrorNotSupported;  // the families below read start/stop only
     if (!impl || impl[0] != 'g') {  // regs
         cudaError_t e = cudaErrorNotSupported;
         switch (a.K) {

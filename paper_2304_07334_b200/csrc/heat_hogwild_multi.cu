@@ -76,7 +76,8 @@ __host__ __device__ inline MwLayout mw_layout(int snap_cap) {
 // Unlike the resident kernel (+7 %), it measured slower here (c3 72.7 M vs
 // 77.7 M samples/s): the warps' stage loops are equally long, so there is
 // little barrier wait to hide, and the waiting warps poll.
-template <int K, int NW, int D, int LPR, bool SPLIT>
+// DR: the pair range and stream base come from HogwildArgs::range_dev/s0_dev
+template <int K, int NW, int D, int LPR, bool SPLIT, bool DR>
 __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     hogwild_multi(HogwildArgs a, FastMod fm, int n_workers, int snap_cap) {
     using G = MwGeom<K, LPR>;
@@ -96,7 +97,14 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
     WriteEntry *ents = reinterpret_cast<WriteEntry *>(mine + Lo.ents);
 
     const int gw = blockIdx.x;
-    const int64_t npairs = a.stop - a.start;
+    int64_t k_start = a.start, k_stop = a.stop;
+    uint64_t k_s0 = a.s0;
+    if constexpr (DR) {
+        k_start = a.range_dev[0];
+        k_stop = a.range_dev[1];
+        k_s0 = *a.s0_dev;
+    }
+    const int64_t npairs = k_stop - k_start;
     if (gw >= n_workers || gw >= npairs) return;  // uniform per CTA
     __shared__ uint64_t reads_done;
     uint32_t phase = 0;
@@ -122,7 +130,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
 
     double loss = 0.0;
     long long degen = 0, active = 0;
-    for (int64_t p = a.start + gw; p < a.stop; p += n_workers) {
+    for (int64_t p = k_start + gw; p < k_stop; p += n_workers) {
         const int64_t u = a.users[p];
         const int32_t pos = a.items[p];
         const uint64_t key = (uint64_t)(a.pair_index ? a.pair_index[p] : p);
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
             const int r = s * SR + rr;
             uint32_t id = (uint32_t)pos;
             if (r > 0 && r <= N)
-                id = (uint32_t)fm.mod(mix64(a.s0 + (key * (uint64_t)N + (uint64_t)r) * kGamma));
+                id = (uint32_t)fm.mod(mix64(k_s0 + (key * (uint64_t)N + (uint64_t)r) * kGamma));
             if (r > N) id = 0;
             if (lead) ids[slot * SR + rr] = (int32_t)id;
             const int nvalid = min(SR, N + 1 - s * SR);
@@ -392,7 +400,9 @@ static cudaError_t launch_multi_k(const HogwildArgs &a, cudaStream_t st, int *wo
         const char *e = getenv("HEAT_MULTI_SPLIT");
         return e ? atoi(e) != 0 : false;  // measured on c3: 72.7 M split vs 77.7 M barrier
     }();
-    auto kern = split ? hogwild_multi<K, NW, D, LPR, true> : hogwild_multi<K, NW, D, LPR, false>;
+    auto kern = a.range_dev ? hogwild_multi<K, NW, D, LPR, false, true>
+                : split     ? hogwild_multi<K, NW, D, LPR, true, false>
+                            : hogwild_multi<K, NW, D, LPR, false, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32 * NW, smem, &e);
     if (e != cudaSuccess) return e;

@@ -84,7 +84,8 @@ __device__ __forceinline__ void rs_red(float *p, const float (&d)[VW]) {
 // SPLIT (with EARLY): the pre-write barrier is an mbarrier whose arrival each
 // warp signals as soon as its own copies land, before it scores, so the wait
 // before the writes rarely stalls.
-template <int K, int NB, bool EARLY, bool SPLIT, bool IDPF>
+// DR: the pair range and stream base come from HogwildArgs::range_dev/s0_dev
+template <int K, int NB, bool EARLY, bool SPLIT, bool IDPF, bool DR>
 // 7 resident CTAs per SM (the window allows ~7 pairs per SM), but never
 // fewer than 64 registers per thread
 __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB : 1) : 7))
@@ -129,10 +130,17 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     const uint64_t pair_step = (uint64_t)N * kGamma;
     // pair metadata one pair ahead, so no dependent global load sits at the
     // head of a pair
-    int64_t p = a.start + blockIdx.x;
+    int64_t k_start = a.start, k_stop = a.stop;
+    uint64_t k_s0 = a.s0;
+    if constexpr (DR) {
+        k_start = a.range_dev[0];
+        k_stop = a.range_dev[1];
+        k_s0 = *a.s0_dev;
+    }
+    int64_t p = k_start + blockIdx.x;
     int32_t nx_pos = 0, nx_u = 0;
     int64_t nx_pg = 0;
-    if (p < a.stop) {
+    if (p < k_stop) {
         nx_pos = a.items[p];
         nx_u = a.users[p];
         nx_pg = a.pair_index ? a.pair_index[p] : p;
@@ -140,16 +148,16 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     // IDPF: the next pair's row ids are drawn while this pair's copies are in
     // flight (the SplitMix64 + modulo chain then never sits at a pair's head)
     uint32_t nx_id = (uint32_t)nx_pos;
-    if (IDPF && r > 0) nx_id = (uint32_t)fm.mod(mix64(a.s0 + (uint64_t)nx_pg * pair_step + lane_off));
+    if (IDPF && r > 0) nx_id = (uint32_t)fm.mod(mix64(k_s0 + (uint64_t)nx_pg * pair_step + lane_off));
 
-    for (; p < a.stop; p += n_workers, parity ^= 1) {
+    for (; p < k_stop; p += n_workers, parity ^= 1) {
         ++mine;
         float *urow = EARLY ? ubuf + w * K : ubuf + parity * K;
         // ---- A: ids, copies
         const int32_t pos = nx_pos;
         const int64_t u = nx_u;
         const int64_t pg = nx_pg;
-        if (p + n_workers < a.stop) {
+        if (p + n_workers < k_stop) {
             nx_pos = a.items[p + n_workers];
             nx_u = a.users[p + n_workers];
             nx_pg = a.pair_index ? a.pair_index[p + n_workers] : p + n_workers;
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
         if (IDPF)
             id = nx_id;
         else if (r > 0)
-            id = (uint32_t)fm.mod(mix64(a.s0 + (uint64_t)pg * pair_step + lane_off));
+            id = (uint32_t)fm.mod(mix64(k_s0 + (uint64_t)pg * pair_step + lane_off));
         {
             const float *srcb = a.T + my_ch * 4;
 #pragma unroll
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
                 nx_id = (uint32_t)nx_pos;
                 if (r > 0)
                     nx_id = (uint32_t)fm.mod(
-                        mix64(a.s0 + (uint64_t)nx_pg * pair_step + lane_off));
+                        mix64(k_s0 + (uint64_t)nx_pg * pair_step + lane_off));
             }
             cp_async_wait<0>();
         }
@@ -341,10 +349,11 @@ static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int
         const char *e = getenv("HEAT_RESIDENT_IDPF");
         return e ? atoi(e) != 0 : true;  // measured c2: 357.7 M vs 355.9 M
     }();
-    auto kern = early == 2   ? (idpf ? hogwild_resident<K, NB, true, true, true>
-                                     : hogwild_resident<K, NB, true, true, false>)
-                : early == 1 ? hogwild_resident<K, NB, true, false, false>
-                             : hogwild_resident<K, NB, false, false, false>;
+    auto kern = a.range_dev ? hogwild_resident<K, NB, true, true, true, true>
+                : early == 2 ? (idpf ? hogwild_resident<K, NB, true, true, true, false>
+                                     : hogwild_resident<K, NB, true, true, false, false>)
+                : early == 1 ? hogwild_resident<K, NB, true, false, false, false>
+                             : hogwild_resident<K, NB, false, false, false, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32 * NB, smem, &e);
     if (e != cudaSuccess) return e;

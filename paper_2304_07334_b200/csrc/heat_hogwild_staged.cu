@@ -104,7 +104,8 @@ __device__ __forceinline__ void red_add_vec(float *p, const float (&d)[VW]) {
 #define UREG_MAX 128
 #endif
 
-template <int K, int D, bool F64, bool BULK, int LPR>
+// DR: the pair range and stream base come from HogwildArgs::range_dev/s0_dev
+template <int K, int D, bool F64, bool BULK, int LPR, bool DR>
 __global__ void __launch_bounds__(32)
     hogwild_staged(HogwildArgs a, FastMod fm, int n_workers, int snap_cap, int cross) {
     using G = StGeom<K, LPR>;
@@ -129,7 +130,14 @@ __global__ void __launch_bounds__(32)
     const int hs = lane % LPR;       // and its column segment
     const bool lead = hs == 0;       // the lane that accounts for the row
     const int gw = blockIdx.x;
-    const int64_t npairs = a.stop - a.start;
+    int64_t k_start = a.start, k_stop = a.stop;
+    uint64_t k_s0 = a.s0;
+    if constexpr (DR) {
+        k_start = a.range_dev[0];
+        k_stop = a.range_dev[1];
+        k_s0 = *a.s0_dev;
+    }
+    const int64_t npairs = k_stop - k_start;
     if (gw >= n_workers || gw >= npairs) return;
     const int64_t my_pairs = (npairs - gw + n_workers - 1) / n_workers;
     const int N = a.N;
@@ -160,20 +168,20 @@ __global__ void __launch_bounds__(32)
     int64_t g_next = 0;
     int64_t pt = 0;
     int ps = 0, pslot = 0, pus = 0;
-    int32_t pf_u = a.users[a.start + gw];
-    int32_t pf_pos = a.items[a.start + gw];
-    int64_t pf_p = a.start + gw;  // pair whose user row the producer loads next
+    int32_t pf_u = a.users[k_start + gw];
+    int32_t pf_pos = a.items[k_start + gw];
+    int64_t pf_p = k_start + gw;  // pair whose user row the producer loads next
     int32_t nx_u = 0, nx_pos = 0;
     if (my_pairs > 1) {
-        nx_u = a.users[a.start + gw + n_workers];
-        nx_pos = a.items[a.start + gw + n_workers];
+        nx_u = a.users[k_start + gw + n_workers];
+        nx_pos = a.items[k_start + gw + n_workers];
     }
     // counter-form SplitMix64 state of this lane's next draw:
     // s0 + (p*N + j + 1) * GAMMA with j = 32*ps + lane - 1
     auto rng_key = [&](int64_t pp) -> uint64_t {
         return (uint64_t)(a.pair_index ? a.pair_index[pp] : pp);
     };
-    uint64_t rng_state = a.s0 + (rng_key(a.start + gw) * (uint64_t)N + (uint64_t)rr) * kGamma;
+    uint64_t rng_state = k_s0 + (rng_key(k_start + gw) * (uint64_t)N + (uint64_t)rr) * kGamma;
     // this lane's fixed 16-byte chunk and row-within-instruction
     constexpr int RPI = 32 / G::CH > 0 ? 32 / G::CH : 1;  // rows per copy instruction
     constexpr int NI = SR / RPI > 0 ? SR / RPI : 1;       // copy instructions per stage
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(32)
     // the stage being consumed.
     // query row of a pair: S[u], or the aggregated query h (trainer.py:148-173)
     auto qrow = [&](int64_t pp, int32_t uu_) -> const float * {
-        return a.query ? a.query + (pp - a.start) * K : a.S + (int64_t)uu_ * K;
+        return a.query ? a.query + (pp - k_start) * K : a.S + (int64_t)uu_ * K;
     };
     auto issue = [&](int64_t limit) {
         if (g_next >= limit) {
@@ -244,10 +252,10 @@ __global__ void __launch_bounds__(32)
             if (++pus == Lo.ucap) pus = 0;
             pf_u = nx_u;
             pf_pos = nx_pos;
-            const int64_t pn = a.start + gw + pt * n_workers;
+            const int64_t pn = k_start + gw + pt * n_workers;
             pf_p = pn;
             if (pt < my_pairs)
-                rng_state = a.s0 + (rng_key(pn) * (uint64_t)N + (uint64_t)rr) * kGamma;
+                rng_state = k_s0 + (rng_key(pn) * (uint64_t)N + (uint64_t)rr) * kGamma;
             if (pt + 1 < my_pairs) {
                 nx_u = a.users[pn + n_workers];
                 nx_pos = a.items[pn + n_workers];
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(32)
     int cslot = 0, cus = 0;  // consumer ring slot / user slot
     int64_t cgen = 0;        // consumer stage count (bulk mover parity)
     for (int64_t t = 0; t < my_pairs; ++t) {
-        const int64_t p = a.start + gw + t * n_workers;
+        const int64_t p = k_start + gw + t * n_workers;
         const int64_t u = a.users[p];
         const int64_t limit = cross ? g_total : (t + 1) * nb;
         if (!cross)
@@ -513,7 +521,7 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
                     for (int i = 0; i < VW; ++i) sv[i] = a.S[u * K + lane * VW + i];
                 }
-                float *go = a.ugrad_out + (p - a.start) * K + lane * VW;
+                float *go = a.ugrad_out + (p - k_start) * K + lane * VW;
 #pragma unroll
                 for (int i = 0; i < VW; ++i) {
                     d[i] = -a.lr * (a.ugamma * ug[i] + a.l2 * sv[i]);
@@ -551,7 +559,8 @@ static cudaError_t launch_staged_k(const HogwildArgs &a, cudaStream_t st, int *w
     if (const char *e = getenv("HEAT_SNAP")) snap_cap = atoi(e) > 0 ? atoi(e) : snap_cap;
     const StLayout L = st_layout<K, D, LPR>(snap_cap);
     if (L.total > 200 * 1024) return cudaErrorInvalidValue;
-    auto kern = hogwild_staged<K, D, F64, BULK, LPR>;
+    auto kern = a.range_dev ? hogwild_staged<K, D, F64, BULK, LPR, true>
+                            : hogwild_staged<K, D, F64, BULK, LPR, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, L.total, &e);
     if (e != cudaSuccess) return e;

@@ -39,6 +39,11 @@ struct HogwildArgs {
     int64_t delta_capacity;
     // global epoch position of local pair p (RNG key); NULL = p itself
     const int64_t *pair_index;
+    // device-side step descriptor (captured step graphs): when set, the kernel
+    // trains pairs [range_dev[0], range_dev[1]) with stream base *s0_dev, and
+    // start/stop above only size the grid (stop - start = the largest step)
+    const int64_t *range_dev = nullptr;
+    const uint64_t *s0_dev = nullptr;
     // behaviour aggregation (throughput mode): the query of local pair p is
     // query[(p - start) * K] instead of S[u]; the user gradient is written to
     // ugrad_out[(p - start) * K] and S[u] -= lr * (ugamma * ugrad + l2 * S[u])
@@ -93,6 +98,17 @@ cudaError_t launch_exact_spec(float *S, int64_t s_rows, float *T, int64_t t_rows
                               int64_t stop, int K, int N, int cosine, double lr, double l2,
                               double mu, double theta, uint64_t s0, heat_counters *ctr,
                               void *scratch, const int64_t *pair_index, cudaStream_t stream);
+
+// one DELTA step whose pair range / stream base live in device memory (the
+// shard runtime's captured step graphs); device_step_supported says whether a
+// kernel family with that mode serves these parameters
+int train_range_device_step(float *S, int64_t s_rows, float *T, int64_t t_rows,
+                            const int32_t *users, const int32_t *items,
+                            const heat_sgd_params *p, heat_counters *counters, int32_t *delta_ids,
+                            float *delta_rows, int64_t *delta_count, int64_t delta_capacity,
+                            const int64_t *pair_index, const int64_t *range_dev,
+                            const uint64_t *s0_dev, void *stream);
+bool device_step_supported(const heat_sgd_params *p, const float *S, const float *T);
 
 int sm_count();
 // CTAs per SM of a kernel (dynamic smem opt-in applied), cached per device

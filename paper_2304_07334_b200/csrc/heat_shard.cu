@@ -123,6 +123,16 @@ struct heat_shard {
     int64_t *hstep_counts = nullptr;  // pinned copy
     int64_t step_counts_n = 0;
     int64_t *scratch = nullptr;  // device: small collective staging (handles, agreement)
+    // captured step graphs: the epoch's inputs live in runtime-owned buffers
+    // (stable addresses), the per-step pair ranges and the stream base in
+    // device memory, so one instantiated graph replays every epoch of a shape
+    bool graphs = true;
+    int32_t *d_users = nullptr, *d_items = nullptr;
+    int64_t *d_pidx = nullptr, pairs_cap = 0;
+    int64_t *d_bounds = nullptr, *h_bounds = nullptr, bounds_cap = 0;
+    uint64_t *d_s0 = nullptr, *h_s0 = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<int64_t> gkey;
     std::string err;
 };
 
@@ -466,6 +476,7 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
     const char *ex = getenv("HEAT_SHARD_EXCHANGE");
     h->p2p = !(ex && strcmp(ex, "gather") == 0);
     if (const char *l = getenv("HEAT_SHARD_LAG")) h->lag = std::min(std::max(atoi(l), 1), kSlots - 1);
+    if (const char *g = getenv("HEAT_SHARD_GRAPH")) h->graphs = atoi(g) != 0;
     cudaSetDevice(device);
     // the exchange runs at the highest priority: its apply CTAs take the SM
     // slots that the step kernels free before the next kernel's workers do
@@ -487,6 +498,8 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
     // staging for the host-value all-gathers: (1 + world) * 2 * kSlots handles
     ok = ok && cudaMalloc(&h->scratch, (size_t)(1 + world) * 2 * kSlots *
                                            sizeof(cudaIpcMemHandle_t)) == cudaSuccess;
+    ok = ok && cudaMalloc(&h->d_s0, sizeof(uint64_t)) == cudaSuccess &&
+         cudaMallocHost(&h->h_s0, sizeof(uint64_t)) == cudaSuccess;
     if (!ok) {
         heat_shard_destroy(h);
         return HEAT_ERR_CUDA;
@@ -527,6 +540,10 @@ int heat_shard_destroy(heat_shard *h) {
     cudaFree(h->step_counts);
     cudaFreeHost(h->hstep_counts);
     cudaFree(h->scratch);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    cudaFree(h->d_users); cudaFree(h->d_items); cudaFree(h->d_pidx);
+    cudaFree(h->d_bounds); cudaFreeHost(h->h_bounds);
+    cudaFree(h->d_s0); cudaFreeHost(h->h_s0);
     if (h->comm) nccl().comm_destroy(h->comm);
     for (cudaStream_t s : {h->comm_stream, h->cstream[0], h->cstream[1]})
         if (s) cudaStreamDestroy(s);
@@ -574,28 +591,80 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
     if (!ensure_epoch_buffers(h, er, t_rows, K, nsteps)) return er.rc;
     cap = h->cap;
 
-    // log counters start at zero (afterwards each step's apply re-arms its
-    // slot); the internal streams start after the caller's queued work
+    const bool direct = h->p2p || W == 1;
+    // captured step graphs need the device-range kernels and a host-free step
+    // loop (the gather fallback reads counts on the host between steps)
+    const bool dr = direct && h->graphs && device_step_supported(p, S, T);
+    const int64_t total = nsteps > 0 ? step_bounds[nsteps] : 0;
+    if (dr) {  // the epoch's inputs into runtime-owned buffers
+        if (total > h->pairs_cap) {
+            cudaDeviceSynchronize();
+            cudaFree(h->d_users); cudaFree(h->d_items); cudaFree(h->d_pidx);
+            h->d_users = h->d_items = nullptr;
+            h->d_pidx = nullptr;
+            h->pairs_cap = 0;
+            h->gkey.clear();  // the graph holds the old addresses
+            const int64_t c = std::max<int64_t>(total, 1) * 5 / 4;
+            if (!er.cuda(cudaMalloc(&h->d_users, c * sizeof(int32_t)), "pairs") ||
+                !er.cuda(cudaMalloc(&h->d_items, c * sizeof(int32_t)), "pairs") ||
+                !er.cuda(cudaMalloc(&h->d_pidx, c * sizeof(int64_t)), "pairs"))
+                return er.rc;
+            h->pairs_cap = c;
+        }
+        if (nsteps + 1 > h->bounds_cap) {
+            cudaDeviceSynchronize();
+            cudaFree(h->d_bounds);
+            cudaFreeHost(h->h_bounds);
+            h->d_bounds = nullptr;
+            h->h_bounds = nullptr;
+            h->bounds_cap = 0;
+            h->gkey.clear();
+            if (!er.cuda(cudaMalloc(&h->d_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds") ||
+                !er.cuda(cudaMallocHost(&h->h_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds"))
+                return er.rc;
+            h->bounds_cap = nsteps + 1;
+        }
+        memcpy(h->h_bounds, step_bounds, (nsteps + 1) * sizeof(int64_t));
+        *h->h_s0 = p->stream_base;
+        if (total > 0) {
+            er.cuda(cudaMemcpyAsync(h->d_users, local_users, total * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, caller), "pairs in");
+            er.cuda(cudaMemcpyAsync(h->d_items, local_items, total * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, caller), "pairs in");
+            if (pair_index)
+                er.cuda(cudaMemcpyAsync(h->d_pidx, pair_index, total * sizeof(int64_t),
+                                        cudaMemcpyDeviceToDevice, caller), "pairs in");
+        }
+        er.cuda(cudaMemcpyAsync(h->d_bounds, h->h_bounds, (nsteps + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, caller), "bounds in");
+        er.cuda(cudaMemcpyAsync(h->d_s0, h->h_s0, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                caller), "s0 in");
+    }
+    // log counters start at zero (afterwards each step's apply re-arms its slot)
     for (Slot &sl : h->slot) er.cuda(cudaMemsetAsync(sl.cnt, 0, sizeof(int64_t), caller), "zero");
-    er.cuda(cudaEventRecord(h->ev_start, caller), "record start");
-    for (cudaStream_t s : {h->cstream[0], h->cstream[1], h->comm_stream})
-        er.cuda(cudaStreamWaitEvent(s, h->ev_start, 0), "wait start");
 
     const int lag = h->lag, nslots = h->lag + 1;
+    const int32_t *tr_users = dr ? h->d_users : local_users;
+    const int32_t *tr_items = dr ? h->d_items : local_items;
+    const int64_t *tr_pidx = dr ? (pair_index ? h->d_pidx : nullptr) : pair_index;
     auto compute = [&](int64_t s) {
         Slot &sl = h->slot[s % nslots];
         cudaStream_t cs = h->cstream[s & 1];
         if (s >= lag) er.cuda(cudaStreamWaitEvent(cs, h->slot[(s - lag) % nslots].ex_done, 0),
                               "wait apply");
-        const int64_t a = step_bounds[s], b = step_bounds[s + 1];
-        if (b > a) {
-            const int r = heat_train_range(S, s_rows, T, t_rows, local_users, local_items, a, b, p,
-                                           counters, sl.ids, sl.rows, sl.cnt, cap, pair_index,
-                                           nullptr, nullptr, cs);
-            if (r != HEAT_OK && er.rc == HEAT_OK) {
-                h->err = std::string("train_range: ") + heat_last_error();
-                er.rc = r;
-            }
+        int r = HEAT_OK;
+        if (dr) {  // every step launches (empty ones exit at once): a fixed topology
+            r = train_range_device_step(S, s_rows, T, t_rows, tr_users, tr_items, p, counters,
+                                        sl.ids, sl.rows, sl.cnt, cap, tr_pidx, h->d_bounds + s,
+                                        h->d_s0, cs);
+        } else if (step_bounds[s + 1] > step_bounds[s]) {
+            r = heat_train_range(S, s_rows, T, t_rows, tr_users, tr_items, step_bounds[s],
+                                 step_bounds[s + 1], p, counters, sl.ids, sl.rows, sl.cnt, cap,
+                                 tr_pidx, nullptr, nullptr, cs);
+        }
+        if (r != HEAT_OK && er.rc == HEAT_OK) {
+            h->err = std::string("train_range: ") + heat_last_error();
+            er.rc = r;
         }
         er.cuda(cudaEventRecord(sl.log_ready, cs), "record log");
     };
@@ -642,32 +711,79 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
                                        h->acc, h->flags, h->comm_stream), "apply");
         er.cuda(cudaEventRecord(sl.ex_done, h->comm_stream), "record apply");
     };
-    const bool direct = h->p2p || W == 1;
-    for (int64_t s = 0; s < nsteps && er.rc == HEAT_OK; ++s) {
-        compute(s);
-        if (direct) {  // nothing waits on the host: queue the step's exchange right behind it
-            count(s);
-            apply(s);
-        } else {  // gather fallback: the host wait on the counts of s-1 overlaps kernel(s)
-            if (s >= 1) apply(s - 1);
-            count(s);
+    // the whole step sequence on the internal streams, forked from and joined
+    // back to `origin` (the caller's stream, or the capturing stream)
+    auto enqueue_epoch = [&](cudaStream_t origin) {
+        er.cuda(cudaEventRecord(h->ev_start, origin), "record start");
+        for (cudaStream_t st : {h->cstream[0], h->cstream[1], h->comm_stream})
+            if (st != origin) er.cuda(cudaStreamWaitEvent(st, h->ev_start, 0), "wait start");
+        for (int64_t s = 0; s < nsteps && er.rc == HEAT_OK; ++s) {
+            compute(s);
+            if (direct) {  // nothing waits on the host: the step's exchange right behind it
+                count(s);
+                apply(s);
+            } else {  // gather fallback: the host wait on the counts of s-1 overlaps kernel(s)
+                if (s >= 1) apply(s - 1);
+                count(s);
+            }
+        }
+        if (!direct && nsteps >= 1 && er.rc == HEAT_OK) apply(nsteps - 1);
+        for (int i = 0; i < 2; ++i) {
+            if (h->cstream[i] == origin) continue;
+            er.cuda(cudaEventRecord(h->ev_cdone[i], h->cstream[i]), "record compute");
+            er.cuda(cudaStreamWaitEvent(origin, h->ev_cdone[i], 0), "join compute");
+        }
+        er.cuda(cudaEventRecord(h->ev_comm, h->comm_stream), "record comm");
+        er.cuda(cudaStreamWaitEvent(origin, h->ev_comm, 0), "join comm");
+    };
+
+    // graph key: everything a captured epoch bakes in (not the stream base,
+    // the pair order or the step ranges, which live in device memory)
+    std::vector<int64_t> key;
+    if (dr) {
+        heat_sgd_params q = *p;
+        q.stream_base = 0;
+        key.resize(sizeof(q) / sizeof(int64_t) + 1);
+        memcpy(key.data(), &q, sizeof(q));
+        for (int64_t v : {(int64_t)(uintptr_t)S, s_rows, (int64_t)(uintptr_t)T, t_rows,
+                          (int64_t)(uintptr_t)counters, nsteps, cap, (int64_t)lag,
+                          (int64_t)(pair_index != nullptr), (int64_t)W})
+            key.push_back(v);
+    }
+    if (dr && h->gexec && key == h->gkey) {
+        er.cuda(cudaGraphLaunch(h->gexec, caller), "replay epoch");
+    } else {
+        enqueue_epoch(caller);
+        if (dr && er.rc == HEAT_OK) {
+            // record the same sequence once more, unexecuted, for later epochs
+            // (this epoch also warmed every launch-configuration cache)
+            if (h->gexec) cudaGraphExecDestroy(h->gexec);
+            h->gexec = nullptr;
+            h->gkey.clear();
+            cudaGraph_t g = nullptr;
+            if (cudaStreamBeginCapture(h->cstream[0], cudaStreamCaptureModeRelaxed) ==
+                cudaSuccess) {
+                enqueue_epoch(h->cstream[0]);
+                const cudaError_t ce = cudaStreamEndCapture(h->cstream[0], &g);
+                if (ce == cudaSuccess && er.rc == HEAT_OK &&
+                    cudaGraphInstantiate(&h->gexec, g, 0) == cudaSuccess) {
+                    h->gkey = key;
+                } else {
+                    h->gexec = nullptr;
+                    h->graphs = false;  // stay on direct launches
+                }
+                if (g) cudaGraphDestroy(g);
+            }
+            cudaGetLastError();
+            if (er.rc != HEAT_OK) return er.rc;
         }
     }
-    if (!direct && nsteps >= 1 && er.rc == HEAT_OK) apply(nsteps - 1);
 
-    // the caller's stream sees every applied step; the epoch's counts come
-    // back once for the statistics and the overflow check
+    // the epoch's counts come back once for the statistics and the overflow check
     if (nsteps > 0)
         er.cuda(cudaMemcpyAsync(h->hstep_counts, h->step_counts, nsteps * W * sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, h->comm_stream), "counts to host");
-    for (int i = 0; i < 2; ++i) {
-        er.cuda(cudaEventRecord(h->ev_cdone[i], h->cstream[i]), "record compute");
-        er.cuda(cudaStreamWaitEvent(caller, h->ev_cdone[i], 0), "join compute");
-    }
-    er.cuda(cudaEventRecord(h->ev_comm, h->comm_stream), "record comm");
-    er.cuda(cudaStreamWaitEvent(caller, h->ev_comm, 0), "join comm");
-    er.cuda(cudaStreamSynchronize(h->comm_stream), "epoch");
-    for (int i = 0; i < 2; ++i) er.cuda(cudaStreamSynchronize(h->cstream[i]), "epoch");
+                                cudaMemcpyDeviceToHost, caller), "counts to host");
+    er.cuda(cudaStreamSynchronize(caller), "epoch");
     if (er.rc != HEAT_OK) return er.rc;
 
     heat_shard_stats st{};

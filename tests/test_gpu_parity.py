@@ -815,8 +815,8 @@ def test_native_shard_runtime_world1(torch_cuda):
     tr.close()
 
 
-@pytest.mark.parametrize("lag", ["1", "3"])
-def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag):
+@pytest.mark.parametrize("lag,graph", [("1", "1"), ("3", "1"), ("2", "0")])
+def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag, graph):
     """The native runtime with other staleness bounds (HEAT_SHARD_LAG: kernel(s)
     waits for the apply of step s - lag; lag + 1 log slots in rotation, two
     compute streams): every pair trained once per epoch, every step exchanged,
@@ -829,12 +829,13 @@ def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag):
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
     from paper_2304_07334_b200.synth import make_dataset
     monkeypatch.setenv("HEAT_SHARD_LAG", lag)
+    monkeypatch.setenv("HEAT_SHARD_GRAPH", graph)  # captured step graphs / direct launches
     train, _, _ = make_dataset("c2", scale=0.05)
     mk = lambda: DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,  # noqa: E731
                              init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
     tr = NativeShardTrainer(mk(), 1, 0)
     m = mk()
-    for e in range(2):
+    for e in range(3):  # epoch 0 launches step by step and captures; 1, 2 replay the graph
         u, i = epoch_pairs(train, shuffle_seed(0, e))
         p = tr.model.params(n_neg=100, lr=1e-3, l2=0.0, mu=150.0, theta=0.9, cosine=True,
                             mode=N.MODE_DELTA, stream_base=epoch_stream(0, e), window=512)
