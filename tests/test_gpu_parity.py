@@ -854,6 +854,45 @@ def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag, graph):
     tr.close()
 
 
+def test_shard_graph_replay_equals_direct_launches(torch_cuda, monkeypatch):
+    """The captured step graph (device-side step ranges and stream base,
+    replayed from the second epoch of a shape on) trains the same pairs with
+    the same negatives as step-by-step launches.  With one worker and lag 1
+    the steps run strictly in order, so both runs agree up to the order of
+    the per-warp user-gradient additions (fp32 rounding, ~1e-5 relative after
+    five epochs); a wrong stream base changes the tables far more (the
+    negative control below).  A changed shape (learning rate) recaptures."""
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.parallel import NativeShardTrainer
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    train, _, _ = make_dataset("c2", scale=0.02)
+    monkeypatch.setenv("HEAT_SHARD_LAG", "1")
+    out = {}
+    for graph in ("1", "0", "stale"):
+        monkeypatch.setenv("HEAT_SHARD_GRAPH", "0" if graph == "stale" else graph)
+        m = DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,
+                        init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
+        tr = NativeShardTrainer(m, 1, 0)
+        for e, lr in ((0, 1e-2), (1, 1e-2), (2, 1e-2), (3, 5e-3), (4, 5e-3)):
+            u, i = epoch_pairs(train, shuffle_seed(0, e))
+            s0 = epoch_stream(0, 0 if graph == "stale" else e)  # stale: epoch 0's negatives
+            p = m.params(n_neg=100, lr=lr, l2=0.0, mu=150.0, theta=0.9, cosine=True,
+                         mode=N.MODE_DELTA, stream_base=s0, window=1)
+            m.counters.reset()
+            st = tr.train_epoch(u, i, p, 256)
+            assert m.counters.read().pairs == len(u) and st.steps == tr.num_steps
+        out[graph] = (m.S.cpu().numpy().astype(np.float64), m.T.cpu().numpy().astype(np.float64))
+        tr.close()
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)  # noqa: E731
+    for a, b, c in zip(out["1"], out["0"], out["stale"]):
+        assert rel(a, b) <= 1e-4, rel(a, b)
+        assert rel(c, b) > 20 * max(rel(a, b), 1e-6), (rel(c, b), rel(a, b))
+
+
 def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
     """train() (trainer.py:480-533): tables stay on the device across epochs,
     yet the run equals the reference's epoch-by-epoch result bit for bit;
