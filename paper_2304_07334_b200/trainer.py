@@ -290,9 +290,22 @@ def train(S, T, train_set, test_set, cfg, weights=None, *, eval_interval: int = 
                 save_model(f"{out_dir}/best.ckpt", S, T, weights if agg is not None else None)
         return metrics
 
+    from .hostio import PREFETCH
+    depth = PREFETCH.depth_for(train_set.num_pairs)
     for epoch in range(cfg.epochs):
         t0 = time.perf_counter()
-        rep, _ = run_epoch_on_device(model, train_set, cfg, epoch, agg=agg)
+        # the epoch order from the host prefetcher (shuffles of the next
+        # epochs run on host threads while this one trains), one copy up
+        bufs = PREFETCH.get(train_set, shuffle_seed(cfg.seed, epoch))
+        pairs = bufs[2].to(model.device, non_blocking=True)
+
+        def ahead(e=epoch):
+            for k in range(1, min(depth, cfg.epochs - 1 - e) + 1):
+                PREFETCH.prefetch(train_set, shuffle_seed(cfg.seed, e + k))
+
+        rep, _ = run_epoch_on_device(model, train_set, cfg, epoch, pairs=(pairs[0], pairs[1]),
+                                     agg=agg, before_sync=ahead)
+        PREFETCH.release(bufs)
         rep.wall_time = time.perf_counter() - t0
         reports.append(rep)
         if on_epoch is not None:
