@@ -456,3 +456,29 @@ def test_uniform_sampler_behaviour(torch_cuda):
     sigma = np.sqrt(draws * (1 / n) * (1 - 1 / n))
     assert np.all(np.abs(counts - draws / n) <= 5 * sigma)
     assert N.lib().heat_sample_negatives(0, 0, 1, 1, 0, None, None) == N.HEAT_ERR_INVALID
+
+
+@pytest.mark.parametrize("threads", [1, 8])
+def test_local_gradient_accumulation_costs_no_accuracy(torch_cuda, threads):
+    """test_acceptance.py:274-301 (c10, accuracy part): 40 epochs with the
+    weight gradient flushed every 32 pairs reach the recall of flushing every
+    pair within 0.005 (deterministic kernels; 0.01 for the throughput
+    aggregator, the reference's thread-parity bound)."""
+    from paper_2304_07334_b200 import AggregatorConfig, TrainingConfig
+    from paper_2304_07334_b200.evaluator import evaluate
+    from paper_2304_07334_b200.trainer import train_epoch
+    train_set, test_set = clustered_medium()
+
+    def run(m):
+        cfg = TrainingConfig(emb_dim=32, num_negatives=16, learning_rate=0.05, epochs=40,
+                             num_threads=threads, seed=7,
+                             aggregator=AggregatorConfig(enabled=True, gamma=0.5, max_history=50,
+                                                         mini_batch_size=m))
+        S, T = fresh(train_set, dim=32)
+        W = xavier(32, 5)
+        for e in range(cfg.epochs):
+            train_epoch(S, T, train_set, cfg, W, epoch=e)
+        return evaluate(S, T, train_set, test_set, cfg, weights=W, k=20).recall_at_k
+
+    r32, r1 = run(32), run(1)
+    assert abs(r32 - r1) <= (0.005 if threads == 1 else 0.01), (r32, r1)
