@@ -29,7 +29,8 @@
 // item replicas stay bit-identical.
 //
 // Fallback exchange (HEAT_SHARD_EXCHANGE=gather, or automatically when some
-// rank cannot map a peer's memory): the host reads the counts of step s and NCCL all-gathers the
+// rank cannot map a peer's memory; at world 1 it runs with local copies in
+// place of the NCCL calls, which is how its scheduling is tested on one GPU): the host reads the counts of step s and NCCL all-gathers the
 // logs padded to the largest count, then the same apply runs on the gathered
 // copy.  NCCL is resolved at run time from the copy torch already loaded
 // (dlopen RTLD_NOLOAD): no link-time NCCL dependency.
@@ -591,7 +592,9 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
     if (!ensure_epoch_buffers(h, er, t_rows, K, nsteps)) return er.rc;
     cap = h->cap;
 
-    const bool direct = h->p2p || W == 1;
+    // the gather fallback also runs at world 1 (local copies instead of the
+    // NCCL calls), so its host-side scheduling is exercised on one GPU
+    const bool direct = h->p2p;
     // captured step graphs need the device-range kernels and a host-free step
     // loop (the gather fallback reads counts on the host between steps)
     const bool dr = direct && h->graphs && device_step_supported(p, S, T);
@@ -673,10 +676,13 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         Slot &sl = h->slot[s % nslots];
         er.cuda(cudaStreamWaitEvent(h->comm_stream, sl.log_ready, 0), "wait log");
         int64_t *cnts = h->step_counts + s * W;
-        if (W > 1)  // (world 1: the apply records the log's own counter)
+        if (W > 1)  // (world 1, direct: the apply records the log's own counter)
             er.nccl(n.all_gather(sl.cnt, cnts, 1, ncclInt64, h->comm, h->comm_stream),
                     "all_gather counts");
-        if (!h->p2p && W > 1) {
+        else if (!direct)
+            er.cuda(cudaMemcpyAsync(cnts, sl.cnt, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                                    h->comm_stream), "count copy");
+        if (!direct) {
             er.cuda(cudaMemcpyAsync(h->hstep_counts + s * W, cnts, W * sizeof(int64_t),
                                     cudaMemcpyDeviceToHost, h->comm_stream), "count to host");
             er.cuda(cudaEventRecord(sl.cnt_ready, h->comm_stream), "record counts");
@@ -686,7 +692,7 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         Slot &sl = h->slot[t % nslots];
         int64_t *cnts = h->step_counts + t * W;
         LogView v{};
-        if (h->p2p || W == 1) {
+        if (direct) {
             v.pids = sl.pids;
             v.prows = sl.prows;
         } else {  // gather fallback: counts read on the host, logs padded to the max
@@ -694,7 +700,7 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
             int64_t cmax = 0;
             for (int q = 0; q < W; ++q) cmax = std::max(cmax, h->hstep_counts[t * W + q]);
             cmax = std::min(cmax, cap);
-            if (cmax > 0 && er.rc == HEAT_OK) {
+            if (cmax > 0 && er.rc == HEAT_OK && W > 1) {
                 er.nccl(n.group_start(), "group start");
                 er.nccl(n.all_gather(sl.ids, sl.g_ids, (size_t)cmax, ncclInt32, h->comm,
                                      h->comm_stream), "all_gather ids");
@@ -702,12 +708,13 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
                                      h->comm_stream), "all_gather rows");
                 er.nccl(n.group_end(), "group end");
             }
-            v.ids = sl.g_ids;
-            v.rows = sl.g_rows;
+            v.ids = W > 1 ? sl.g_ids : sl.ids;  // world 1: the log is the gathered copy
+            v.rows = W > 1 ? sl.g_rows : sl.rows;
             v.stride = cmax;
         }
         if (er.rc == HEAT_OK)
-            er.cuda(launch_shard_apply(T, (int)K, v, W > 1 ? cnts : sl.cnt, cnts, sl.cnt, W, cap,
+            er.cuda(launch_shard_apply(T, (int)K, v, (direct && W == 1) ? sl.cnt : cnts, cnts,
+                                       sl.cnt, W, cap,
                                        h->acc, h->flags, h->comm_stream), "apply");
         er.cuda(cudaEventRecord(sl.ex_done, h->comm_stream), "record apply");
     };

@@ -815,11 +815,13 @@ def test_native_shard_runtime_world1(torch_cuda):
     tr.close()
 
 
-@pytest.mark.parametrize("lag,graph", [("1", "1"), ("3", "1"), ("2", "0")])
-def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag, graph):
+@pytest.mark.parametrize("lag,graph,exchange", [("1", "1", "p2p"), ("3", "1", "p2p"),
+                                                ("2", "0", "p2p"), ("2", "0", "gather")])
+def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag, graph, exchange):
     """The native runtime with other staleness bounds (HEAT_SHARD_LAG: kernel(s)
     waits for the apply of step s - lag; lag + 1 log slots in rotation, two
-    compute streams): every pair trained once per epoch, every step exchanged,
+    compute streams), with and without captured step graphs, and through the
+    gather fallback: every pair trained once per epoch, every step exchanged,
     loss within 3 % of the 1-GPU Hogwild run."""
     from paper_2304_07334_b200 import _native as N
     from paper_2304_07334_b200.dataset import epoch_pairs
@@ -830,6 +832,9 @@ def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag, graph):
     from paper_2304_07334_b200.synth import make_dataset
     monkeypatch.setenv("HEAT_SHARD_LAG", lag)
     monkeypatch.setenv("HEAT_SHARD_GRAPH", graph)  # captured step graphs / direct launches
+    # gather: the fallback exchange (counts read on the host each step, the
+    # log as its own gathered copy at world 1)
+    monkeypatch.setenv("HEAT_SHARD_EXCHANGE", exchange)
     train, _, _ = make_dataset("c2", scale=0.05)
     mk = lambda: DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,  # noqa: E731
                              init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
