@@ -236,10 +236,25 @@ __global__ void shard_apply_cvt(float *__restrict__ T, int K, LogView v,
         if (!mine) continue;  // another warp converts this row
         long long *a = acc + id * K;
         float *t = T + id * K;
-        for (int k = lane; k < K; k += 32) {
-            const long long q = a[k];
-            a[k] = 0;
-            t[k] += (float)((double)q * (1.0 / kShardFixScale));
+        if ((K & 3) == 0) {  // 4 columns per lane: 2 x 16 B of accumulator, 16 B of T
+            for (int k = lane * 4; k < K; k += 128) {
+                const longlong2 q01 = *reinterpret_cast<const longlong2 *>(a + k);
+                const longlong2 q23 = *reinterpret_cast<const longlong2 *>(a + k + 2);
+                *reinterpret_cast<longlong2 *>(a + k) = make_longlong2(0, 0);
+                *reinterpret_cast<longlong2 *>(a + k + 2) = make_longlong2(0, 0);
+                float4 tv = *reinterpret_cast<const float4 *>(t + k);
+                tv.x += (float)((double)q01.x * (1.0 / kShardFixScale));
+                tv.y += (float)((double)q01.y * (1.0 / kShardFixScale));
+                tv.z += (float)((double)q23.x * (1.0 / kShardFixScale));
+                tv.w += (float)((double)q23.y * (1.0 / kShardFixScale));
+                *reinterpret_cast<float4 *>(t + k) = tv;
+            }
+        } else {
+            for (int k = lane; k < K; k += 32) {
+                const long long q = a[k];
+                a[k] = 0;
+                t[k] += (float)((double)q * (1.0 / kShardFixScale));
+            }
         }
     }
 }
