@@ -492,6 +492,10 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
     const char *ex = getenv("HEAT_SHARD_EXCHANGE");
     h->p2p = !(ex && strcmp(ex, "gather") == 0);
     if (const char *l = getenv("HEAT_SHARD_LAG")) h->lag = std::min(std::max(atoi(l), 1), kSlots - 1);
+    // captured step graphs: on by default at world 1; with NCCL calls inside
+    // the capture (world > 1) only on request, as that path has not run on a
+    // multi-GPU box here
+    h->graphs = world == 1;
     if (const char *g = getenv("HEAT_SHARD_GRAPH")) h->graphs = atoi(g) != 0;
     cudaSetDevice(device);
     // the exchange runs at the highest priority: its apply CTAs take the SM
@@ -790,14 +794,15 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
                 if (ce == cudaSuccess && er.rc == HEAT_OK &&
                     cudaGraphInstantiate(&h->gexec, g, 0) == cudaSuccess) {
                     h->gkey = key;
-                } else {
+                } else {  // the epoch itself ran: stay on direct launches, no error
                     h->gexec = nullptr;
-                    h->graphs = false;  // stay on direct launches
+                    h->graphs = false;
+                    er.rc = HEAT_OK;
+                    h->err.clear();
                 }
                 if (g) cudaGraphDestroy(g);
             }
             cudaGetLastError();
-            if (er.rc != HEAT_OK) return er.rc;
         }
     }
 
