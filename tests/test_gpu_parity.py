@@ -898,6 +898,41 @@ def test_shard_graph_replay_equals_direct_launches(torch_cuda, monkeypatch):
         assert rel(c, b) > 20 * max(rel(a, b), 1e-6), (rel(c, b), rel(a, b))
 
 
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_sharded_properties(torch_cuda, cfg):
+    """The multi-GPU step code (native runtime, world 1) at BASELINE.json's
+    full c4 / c5 table sizes with the config's B per step: every pair
+    trained once per epoch, one exchange per step, the loss finite and
+    falling, the tables finite."""
+    import torch
+    from paper_2304_07334_b200 import _native as N
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from paper_2304_07334_b200.parallel import NativeShardTrainer
+    from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
+    from paper_2304_07334_b200.synth import make_dataset
+    kw = {"sample_users": 0.02} if cfg == "c5" else {}
+    tr, _, sp = make_dataset(cfg, **kw)
+    m = DeviceModel(init_matrix(tr.num_users, sp.dim, InitSpec(seed=0)).values,
+                    init_matrix(tr.num_items, sp.dim, InitSpec(seed=0)).values)
+    sh = NativeShardTrainer(m, 1, 0)
+    losses = []
+    for e in range(2):
+        u, i = epoch_pairs(tr, shuffle_seed(0, e))
+        p = m.params(n_neg=sp.negatives, lr=sp.learning_rate, l2=0.0, mu=sp.mu, theta=sp.theta,
+                     cosine=True, mode=N.MODE_DELTA, stream_base=epoch_stream(0, e),
+                     window=sp.batch)
+        m.counters.reset()
+        st = sh.train_epoch(u, i, p, sp.batch)
+        c = m.counters.read()
+        assert c.pairs == tr.num_pairs and st.steps == sh.num_steps and np.isfinite(c.loss)
+        losses.append(c.loss / c.pairs)
+    sh.close()
+    assert losses[1] < losses[0]
+    assert bool(torch.isfinite(m.S).all()) and bool(torch.isfinite(m.T).all())
+
+
 def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
     """train() (trainer.py:480-533): tables stay on the device across epochs,
     yet the run equals the reference's epoch-by-epoch result bit for bit;
@@ -1168,9 +1203,9 @@ def test_delta_mode_every_kernel_family(torch_cuda, K, N):
     assert np.isfinite(T0).all() and not np.array_equal(T0, T)
 
 
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
 def test_full_size_properties(torch_cuda, cfg):
-    """BASELINE.json's full sizes (c4 53 k x 92 k x 128, N 1000; c5 10 M x 2 M
+    """BASELINE.json's full sizes (c1-c3; c4 53 k x 92 k x 128, N 1000; c5 10 M x 2 M
     x 128 tables with a 2 % user sample), through size-independent
     properties: every pair trained exactly once per epoch, the loss finite and
     falling, the tables finite, and user rows that own no pair bit-identical
