@@ -3,18 +3,29 @@
 Metric (BASELINE.json): training samples/s, one sample = one (user, positive,
 N negatives) pair — the reference's ``pairs_per_s`` (bench.py:83 of heatcf).
 A bench "step" is one epoch over the synthetic workload's training pairs
-(the unit the reference's bench times).  Default workload: BASELINE config 2
-(30k users x 41k items, 1.03M interactions with a 20 % hold-out, K=64, N=100,
-theta 0.9, mu 150, B=1024), Hogwild kernel with B pairs in flight.
+(the unit the reference's bench times).  Default workload: BASELINE config 4
+(53k users x 92k items, 2.98M interactions, K=128, N=1000, theta 0.8, mu 300,
+B=2048) — the largest configuration stated for one GPU and the one the
+1->8 GPU target names — with the Hogwild kernel and B pairs in flight.
+``--config c1..c5`` selects another (c2/c3 are parity-test shapes; c5 keeps
+its full 10 M x 2 M tables with a 2 % user sample of its interactions).
 
 JSON line keys beyond the base contract:
-  roofline      algorithmic bytes of the fused kernel / its CUDA-event time,
-                against MEASURED_PEAKS.json hbm_gbs
+  roofline      algorithmic bytes of the fused kernel / its CUDA-event time.
+                bound "l2" when S+T fit the 126 MB L2 (c1-c4; ncu: >=98.6 %
+                L2 hit rate), against the L2 streaming-read ceiling measured
+                live in this run (heat_probe_l2_read); bound "hbm" otherwise
+                (c5), against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the C oracle port (restatement of trainer.py:103-466, pthreads
                 Hogwild, all host cores) on a bounded sample of the same pairs
   e2e           the same metric through the public drop-in API
                 ``train_epoch(S, T, train, cfg)`` with host numpy tables:
                 shuffle + H2D of tables and pairs + kernel + D2H of tables
+
+The ``--impl reference`` arm imports nothing from the product package: its
+data come from ``workloads`` (pure numpy) and its epoch order and timed
+training from ``oracle`` (numpy + the C port), so it never maps
+libheat_b200.so.
 """
 
 from __future__ import annotations
@@ -104,18 +115,28 @@ class ClockSampler:
 
 
 def build_workload(name: str):
-    """Synthetic stand-in of a BASELINE config.  c5 keeps its full 10 M x 2 M
-    tables (5.1 GB + 1.0 GB: the HBM-bound case) with interactions generated
-    for a seeded 2 % of the users (10 M of its 500 M interactions)."""
-    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
-    from paper_2304_07334_b200.synth import make_dataset
+    """Synthetic stand-in of a BASELINE config (workloads.py; pure numpy, no
+    product import).  c5 keeps its full 10 M x 2 M tables (5.1 GB + 1.0 GB:
+    the HBM-bound case) with interactions generated for a seeded 2 % of the
+    users (10 M of its 500 M interactions).  S and T are float32 numpy
+    arrays drawn as the reference's init_matrix(InitSpec(seed=0)) draws."""
+    from workloads import init_table, make_dataset
     if name == "c5":
         train, test, spec = make_dataset(name, sample_users=0.02)
     else:
         train, test, spec = make_dataset(name)
-    S = init_matrix(train.num_users, spec.dim, InitSpec(seed=0))
-    T = init_matrix(train.num_items, spec.dim, InitSpec(seed=0))
+    S = init_table(train.num_users, spec.dim, seed=0)
+    T = init_table(train.num_items, spec.dim, seed=0)
     return train, test, spec, S, T
+
+
+def workload_config(spec, train) -> dict:
+    """The `config` object both arms print (identical for the same workload)."""
+    return {"workload": spec.name, "users": train.num_users, "items": train.num_items,
+            "train_pairs": train.num_pairs, "dim": spec.dim, "negatives": spec.negatives,
+            "theta": spec.theta, "mu": spec.mu, "batch": spec.batch, "lr": spec.learning_rate,
+            "similarity": "cosine", "sampler": "uniform", "l2_reg": 0.0,
+            "init": "N(0, 0.01) seed 0 (S and T)", "gen_seed": 12345}
 
 
 def train_config(spec, threads: int):
@@ -134,9 +155,7 @@ def cpu_baseline(spec, train, S0, T0, sample_pairs: int, threads: int, epoch: in
     """Oracle port (C, pthreads Hogwild, the reference's chunk-claiming
     driver) on the first `sample_pairs` pairs of the epoch."""
     from oracle import oracle as O
-    from paper_2304_07334_b200.dataset import epoch_pairs
-    from paper_2304_07334_b200.rng import shuffle_seed
-    u, i = epoch_pairs(train, shuffle_seed(0, epoch))
+    u, i = O.epoch_pairs(train.offsets, train.items, train.num_users, O.shuffle_seed(0, epoch))
     n = min(sample_pairs, len(u))
     S, T = S0.copy(), T0.copy()
     O.lib()
@@ -156,8 +175,6 @@ def cpu_baseline_timed(spec, train, S0, T0, threads: int, seconds: float = 10.0)
     a probe of up to 200 k pairs sizes the sample, which then runs over consecutive
     epochs (tables carried, as a training run would) until it is used up."""
     from oracle import oracle as O
-    from paper_2304_07334_b200.dataset import epoch_pairs
-    from paper_2304_07334_b200.rng import shuffle_seed
     probe = cpu_baseline(spec, train, S0, T0, 20000, threads)  # thread start-up, JIT-free
     if probe["seconds"] * 10 < seconds:  # refine on a longer probe
         probe = cpu_baseline(spec, train, S0, T0, min(200_000, train.num_pairs), threads)
@@ -165,7 +182,7 @@ def cpu_baseline_timed(spec, train, S0, T0, threads: int, seconds: float = 10.0)
     S, T = S0.copy(), T0.copy()
     done, dt, e = 0, 0.0, 0
     while done < target:
-        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        u, i = O.epoch_pairs(train.offsets, train.items, train.num_users, O.shuffle_seed(0, e))
         n = min(target - done, len(u))
         t0 = time.perf_counter()
         O.train_epoch_threads(S, T, u[:n], i[:n], seed=0, epoch=e, num_threads=threads,
@@ -188,14 +205,14 @@ def run_reference(args):
         return 0
     train, _, spec, S, T = build_workload(args.config)
     threads = os.cpu_count() or 1
-    sample = args.ref_sample or {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 20_000,
-                                 "c5": 20_000}[spec.name]
+    sample = args.ref_sample or {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 60_000,
+                                 "c5": 40_000}[spec.name]
     for w in range(args.warmup):
-        cpu_baseline(spec, train, S.values, T.values, min(sample, 20000), threads, epoch=w)
+        cpu_baseline(spec, train, S, T, min(sample, 20000), threads, epoch=w)
     vals = []
     secs = []
     for s in range(args.steps):
-        r = cpu_baseline(spec, train, S.values, T.values, sample, threads, epoch=args.warmup + s)
+        r = cpu_baseline(spec, train, S, T, sample, threads, epoch=args.warmup + s)
         vals.append(r["value"])
         secs.append(r["seconds"])
     v = float(np.mean(vals))
@@ -203,12 +220,9 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": float(np.mean(secs)) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": spec.name, "users": train.num_users,
-                       "items": train.num_items, "train_pairs": train.num_pairs,
-                       "dim": spec.dim, "negatives": spec.negatives, "theta": spec.theta,
-                       "mu": spec.mu, "batch": spec.batch, "mode": "hogwild (host threads)",
-                       "lr": spec.learning_rate,
-                       "step": "a bounded sample of one epoch (cpu_baseline.sample)"},
+            "config": workload_config(spec, train),
+            "run": {"mode": "hogwild (host threads)", "threads": threads,
+                    "step": "a bounded sample of one epoch (cpu_baseline.sample)"},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "port",
                              "sample": r["sample"]},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -230,18 +244,42 @@ def _ncu_traffic(config: str):
         return None
 
 
-def _l2_ceiling(achieved_gbs: float, table_bytes: int) -> dict:
-    """The second ceiling for configurations whose tables stay in the 126 MB
-    L2 (c1-c4): the streaming L2 read rate measured on this GPU model by
-    scripts/l2_bandwidth.py (profiles/r01_l2_bandwidth.json)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_l2_bandwidth.json")) as f:
-            l2 = float(json.load(f)["stream_48MB_GBps"])
-    except Exception:
-        return {}
-    return {"tables_fit_l2": table_bytes < 100 * 1024 * 1024, "l2_probe_gbs": l2,
-            "frac_of_l2_probe": achieved_gbs / l2,
-            "l2_probe_source": "scripts/l2_bandwidth.py (profiles/r01_l2_bandwidth.json)"}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def l2_probe(dev, table_bytes: int) -> dict:
+    """The L2 read ceiling measured live on this GPU: heat_probe_l2_read
+    streams a 48 MB buffer (and one the size of S+T when that fits L2) 50
+    times after a warming pass, timed with CUDA events on the launching
+    stream; the best of 3 runs per size."""
+    import ctypes
+
+    import torch
+
+    from paper_2304_07334_b200 import _native as N
+    L = N.lib()
+    stream = torch.cuda.current_stream(dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+    out = {}
+    sizes = {"48MB": 48 * 1024 * 1024}
+    if table_bytes < L2_BYTES * 0.9:
+        sizes["tables"] = max(4 * 1024 * 1024, int(table_bytes))
+    for name, nbytes in sizes.items():
+        buf = torch.ones(nbytes // 4, dtype=torch.float32, device=dev)
+        best = 0.0
+        for _ in range(3):
+            N.check(L.heat_probe_l2_read(buf.data_ptr(), buf.numel(), 1, sink.data_ptr(),
+                                         ctypes.c_void_p(stream.cuda_stream)))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            N.check(L.heat_probe_l2_read(buf.data_ptr(), buf.numel(), 50, sink.data_ptr(),
+                                         ctypes.c_void_p(stream.cuda_stream)))
+            e1.record(stream)
+            e1.synchronize()
+            best = max(best, buf.numel() * 4.0 * 50 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out[name] = best
+        del buf
+    return out
 
 
 def main():
@@ -250,7 +288,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20, help="timed epochs")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--mode", default="hogwild", choices=["hogwild", "exact"])
     ap.add_argument("--window", type=int, default=0, help="pairs in flight (0: config batch)")
     ap.add_argument("--fp64", action="store_true")
@@ -295,7 +333,7 @@ def main():
     K, NN = spec.dim, spec.negatives
     total_epochs = args.warmup + args.steps
     npairs = train.num_pairs
-    model = DeviceModel(S.values, T.values, dev)
+    model = DeviceModel(S, T, dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -388,7 +426,8 @@ def main():
     if not sharded and args.e2e_steps:
         configure(mode=args.mode, window=window, fp64=args.fp64)
         cfg = train_config(spec, threads=8 if args.mode == "hogwild" else 1)
-        Se, Te = S.copy(), T.copy()
+        from paper_2304_07334_b200.embeddings import EmbeddingMatrix
+        Se, Te = EmbeddingMatrix(S.copy()), EmbeddingMatrix(T.copy())
         train_epoch(Se, Te, train, cfg, epoch=0)
         train_epoch(Se, Te, train, cfg, epoch=1)
         torch.cuda.synchronize()
@@ -398,8 +437,8 @@ def main():
             assert np.isfinite(rep.mean_loss)  # the step's result, read back on the host
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         e2e = {"value": npairs / e2e_s, "unit": "samples/s",
-               "h2d_bytes_per_step": S.values.nbytes + T.values.nbytes + 8 * npairs,
-               "d2h_bytes_per_step": S.values.nbytes + T.values.nbytes + 32,
+               "h2d_bytes_per_step": S.nbytes + T.nbytes + 8 * npairs,
+               "d2h_bytes_per_step": S.nbytes + T.nbytes + 32,
                "path": "paper_2304_07334_b200.train_epoch (host numpy S/T, shuffle, H2D, "
                        "kernel, D2H), steady state over consecutive epochs"}
     elif sharded and args.e2e_steps:
@@ -436,38 +475,51 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         # about 10 s of host work each (bounded samples of the same workload)
-        cpu = cpu_baseline_timed(spec, train, S.values, T.values, threads, args.cpu_seconds)
+        cpu = cpu_baseline_timed(spec, train, S, T, threads, args.cpu_seconds)
         cpu.pop("seconds", None)
         # the single-thread figure beside it
-        one = cpu_baseline_timed(spec, train, S.values, T.values, 1, args.cpu_seconds)
+        one = cpu_baseline_timed(spec, train, S, T, 1, args.cpu_seconds)
         cpu["value_1_thread"] = one["value"]
         cpu["sample_1_thread"] = one["sample"]
 
     if rank == 0:
         prof = _ncu_traffic(spec.name)
+        table_bytes = S.nbytes + T.nbytes
+        hbm = {"hbm_peak": peak, "hbm_peak_kind": peak_kind, "frac_of_hbm": achieved / peak}
+        if table_bytes < L2_BYTES * 0.9:
+            # S+T stay in L2 (ncu: >= 98.6 % sector hit rate on c2-c4): the L2
+            # read ceiling, measured live, bounds the kernel; HBM frac kept beside
+            probe = l2_probe(dev, table_bytes)
+            l2_peak = max(probe.values())
+            roofline = {"bound": "l2", "achieved": achieved, "peak": l2_peak,
+                        "peak_kind": "measured live: heat_probe_l2_read streaming read, best of "
+                                     "48 MB and S+T-sized buffers " +
+                                     json.dumps({k: round(v, 1) for k, v in probe.items()}),
+                        "unit": "GB/s", "frac": achieved / l2_peak, **hbm}
+        else:
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": peak,
+                        "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak}
+        roofline.update({
+            "traffic": prof.get("dram_bytes_per_launch") if prof else None,
+            "traffic_source": prof.get("source") if prof else None,
+            "l2_hit_rate_pct": prof.get("l2_hit_rate_pct") if prof else None,
+            "bytes_per_launch": bytes_per_epoch,
+            "bytes_per_pair": "4K(N+2)+8 read + 4K(2+A_p) written (SURVEY.md §8(d))",
+            "table_bytes": table_bytes,
+            "active_negatives_per_pair": act_total / args.steps / npairs})
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32", "data": "synthetic",
-            "config": {"workload": spec.name, "users": train.num_users,
-                       "items": train.num_items, "train_pairs": npairs, "dim": K,
-                       "negatives": NN, "theta": spec.theta, "mu": spec.mu,
-                       "batch": spec.batch, "window": window, "mode": args.mode,
-                       "lr": spec.learning_rate, "step": "one epoch",
-                       "l2_flush": "512 MiB write before every timed epoch; S+T "
-                                   f"{(S.values.nbytes + T.values.nbytes) / 1e6:.1f} MB",
-                       "parallelism": (f"users sharded x{world}, item-delta exchange every "
-                                       f"{exchange_pairs} global pairs (P2P gather+apply)"
-                                       if sharded else "single GPU")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": prof.get("dram_bytes_per_launch") if prof else None,
-                         "traffic_source": prof.get("source") if prof else None,
-                         "l2_hit_rate_pct": prof.get("l2_hit_rate_pct") if prof else None,
-                         "bytes_per_launch": bytes_per_epoch,
-                         "active_negatives_per_pair": act_total / args.steps / npairs,
-                         **_l2_ceiling(achieved, S.values.nbytes + T.values.nbytes)},
+            "config": workload_config(spec, train),
+            "run": {"window": window, "mode": args.mode, "step": "one epoch",
+                    "l2_flush": "512 MiB write before every timed epoch; S+T "
+                                f"{(S.nbytes + T.nbytes) / 1e6:.1f} MB",
+                    "parallelism": (f"users sharded x{world}, item-delta exchange every "
+                                    f"{exchange_pairs} global pairs (P2P gather+apply)"
+                                    if sharded else "single GPU")},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_epoch * args.steps,

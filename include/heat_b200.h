@@ -224,6 +224,11 @@ int heat_epoch_pairs(const int64_t *offsets, int64_t num_users, const int32_t *i
  * recomputes, full recomputes, pairs.  reset != 0 zeroes them. */
 int heat_exact_stats(unsigned long long *out, int reset);
 
+/* Diagnostic: streaming read of n floats (device buffer) `passes` times at
+ * L2 on `stream`; bench.py times it to measure the L2 read ceiling that
+ * bounds the L2-resident configurations (not a reference interface). */
+int heat_probe_l2_read(const float *buf, int64_t n, int32_t passes, float *sink, void *stream);
+
 const char *heat_last_error(void);
 int heat_version(void);
 

@@ -229,6 +229,18 @@ cudaError_t launch_apply_deltas(float *T, int64_t t_rows, int K, const int32_t *
 
 using namespace heat;
 
+__global__ void l2_probe_kernel(const float4 *__restrict__ a, long long n4, int passes,
+                                float *sink) {
+    float acc = 0.f;
+    for (int p = 0; p < passes; ++p)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+             i += (long long)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(a + i);
+            acc += (v.x + v.y) + (v.z + v.w);
+        }
+    if (acc == 1234.5f) sink[0] = acc;  // keeps the loads live
+}
+
 extern "C" {
 
 const char *heat_last_error(void) { return g_err.c_str(); }
@@ -444,6 +456,21 @@ int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int
                                               reinterpret_cast<long long *>(acc), flags,
                                               (cudaStream_t)stream);
     return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "apply_row_deltas_fixed launch");
+}
+
+/* Diagnostic (not part of the reference interface): streaming read of
+ * `n` floats `passes` times, 16-byte vectors at L2 (ld.global.cg), 8 CTAs of
+ * 512 threads per SM.  bench.py times it with events to measure the L2
+ * ceiling of the L2-resident configurations on the box it runs on. */
+int heat_probe_l2_read(const float *buf, int64_t n, int32_t passes, float *sink, void *stream) {
+    if (!buf || !sink || n < 4 || passes < 1) return fail(HEAT_ERR_INVALID, "bad probe args");
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    l2_probe_kernel<<<sms * 8, 512, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4 *>(buf), n / 4, passes, sink);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "l2 probe launch");
 }
 
 }  // extern "C"

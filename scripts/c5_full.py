@@ -28,7 +28,7 @@ from paper_2304_07334_b200.dataset import epoch_pairs  # noqa: E402
 from paper_2304_07334_b200.device import DeviceModel  # noqa: E402
 from paper_2304_07334_b200.embeddings import InitSpec, init_matrix  # noqa: E402
 from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed  # noqa: E402
-from paper_2304_07334_b200.synth import make_dataset  # noqa: E402
+from workloads import make_dataset  # noqa: E402
 
 EPOCHS = int(os.environ.get("C5_EPOCHS", "2"))
 out = {"what": "c5_full", "epochs": EPOCHS}

@@ -11,7 +11,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2304_07334_b200 import TrainingConfig, LossParams  # noqa: E402
 from paper_2304_07334_b200.embeddings import EmbeddingMatrix, InitSpec, init_matrix  # noqa: E402
-from paper_2304_07334_b200.synth import make_dataset  # noqa: E402
+from workloads import make_dataset  # noqa: E402
 from paper_2304_07334_b200.trainer import configure, train_epoch  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"

@@ -20,7 +20,7 @@ from paper_2304_07334_b200.device import DeviceModel  # noqa: E402
 from paper_2304_07334_b200.embeddings import InitSpec, init_matrix  # noqa: E402
 from paper_2304_07334_b200.evaluator import evaluate_device  # noqa: E402
 from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed  # noqa: E402
-from paper_2304_07334_b200.synth import make_dataset  # noqa: E402
+from workloads import make_dataset  # noqa: E402
 
 flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
 

@@ -12,7 +12,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2304_07334_b200 import LossParams, TrainingConfig  # noqa: E402
 from paper_2304_07334_b200.embeddings import InitSpec, init_matrix  # noqa: E402
-from paper_2304_07334_b200.synth import make_dataset  # noqa: E402
+from workloads import make_dataset  # noqa: E402
 from paper_2304_07334_b200.trainer import configure, train  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"

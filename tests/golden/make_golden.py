@@ -49,7 +49,7 @@ from heatcf.evaluator import evaluate as r_evaluate, _topk_from_scores  # noqa: 
 from heatcf.kernels import LossParams as RLoss  # noqa: E402
 from heatcf.rng import SplitMix64, derive_stream, stream_state  # noqa: E402
 
-from paper_2304_07334_b200.synth import make_dataset  # noqa: E402  (data only)
+from workloads import make_dataset  # noqa: E402  (data only)
 
 
 def rset(s) -> RSet:

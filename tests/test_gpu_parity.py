@@ -89,7 +89,7 @@ def test_exact_c1_two_epochs_bit_exact(torch_cuda):
     from paper_2304_07334_b200.device import DeviceModel
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
     train, _, _ = make_dataset("c1")
     S = init_matrix(1000, 32, InitSpec(seed=0)).values
@@ -137,7 +137,7 @@ def test_exact_c2_prefix_bit_exact(torch_cuda):
     from paper_2304_07334_b200.device import DeviceModel
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     with open(os.path.join(GOLDEN, "c2_prefix.json")) as f:
         g = json.load(f)
     train, _, _ = make_dataset("c2")
@@ -195,7 +195,7 @@ def test_exact_matches_oracle_random(torch_cuda, K, N, cos, l2, theta):
 
 def test_train_epoch_api_exact_equals_reference(torch_cuda):
     from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     from paper_2304_07334_b200.trainer import train_epoch
     z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
     train, _, _ = make_dataset("c1")
@@ -217,7 +217,7 @@ def test_hogwild_descends_and_matches_oracle_quality(torch_cuda):
     from oracle import oracle as O
     from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
     from paper_2304_07334_b200.evaluator import evaluate
-    from paper_2304_07334_b200.synth import make_clustered
+    from workloads import make_clustered
     from paper_2304_07334_b200.trainer import configure, train_epoch
     from paper_2304_07334_b200.dataset import epoch_pairs
     from paper_2304_07334_b200.rng import shuffle_seed
@@ -274,7 +274,7 @@ def test_eval_matches_reference_golden(torch_cuda):
 def test_eval_c2_init_matches_reference(torch_cuda):
     from paper_2304_07334_b200 import InitSpec, init_matrix, TrainingConfig
     from paper_2304_07334_b200.evaluator import evaluate
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     z = np.load(os.path.join(GOLDEN, "eval.npz"))
     tr, te, _ = make_dataset("c2")
     S = init_matrix(tr.num_users, 64, InitSpec(seed=0))
@@ -355,7 +355,7 @@ def test_hogwild_window1_tracks_reference(torch_cuda, fp64, force_generic, monke
     from paper_2304_07334_b200.device import DeviceModel
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     if force_generic:
         monkeypatch.setenv("HEAT_FORCE_GENERIC", "1")
     z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
@@ -425,7 +425,7 @@ def test_logical_shards_keep_item_replicas_identical(torch_cuda, G):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import ShardedTrainer
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     train, _, _ = make_dataset("c2", scale=0.05)
     S = init_matrix(train.num_users, 64, InitSpec(seed=0)).values
     T = init_matrix(train.num_items, 64, InitSpec(seed=0)).values
@@ -641,7 +641,7 @@ def test_agg_hogwild_quality_matches_oracle(torch_cuda):
     from paper_2304_07334_b200.dataset import epoch_pairs
     from paper_2304_07334_b200.evaluator import evaluate
     from paper_2304_07334_b200.rng import shuffle_seed
-    from paper_2304_07334_b200.synth import make_clustered
+    from workloads import make_clustered
     from paper_2304_07334_b200.trainer import configure, train_epoch
     train, test = make_clustered(800, 1600, 16, 40, affinity=0.97, seed=11)
     K, E = 32, 20
@@ -732,7 +732,7 @@ def test_pipelined_shards_keep_replicas_identical(torch_cuda, G):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import PipelinedShardTrainer, run_loopback
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     train, _, _ = make_dataset("c2", scale=0.05)
     S = init_matrix(train.num_users, 64, InitSpec(seed=0)).values
     T = init_matrix(train.num_items, 64, InitSpec(seed=0)).values
@@ -783,7 +783,7 @@ def test_native_shard_runtime_world1(torch_cuda):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import NativeShardTrainer
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     train, _, _ = make_dataset("c2", scale=0.05)
     mk = lambda: DeviceModel(init_matrix(train.num_users, 64, InitSpec(seed=0)).values,  # noqa: E731
                              init_matrix(train.num_items, 64, InitSpec(seed=0)).values)
@@ -829,7 +829,7 @@ def test_native_shard_runtime_lag(torch_cuda, monkeypatch, lag, graph, exchange)
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import NativeShardTrainer
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     monkeypatch.setenv("HEAT_SHARD_LAG", lag)
     monkeypatch.setenv("HEAT_SHARD_GRAPH", graph)  # captured step graphs / direct launches
     # gather: the fallback exchange (counts read on the host each step, the
@@ -873,7 +873,7 @@ def test_shard_graph_replay_equals_direct_launches(torch_cuda, monkeypatch):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import NativeShardTrainer
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     train, _, _ = make_dataset("c2", scale=0.02)
     monkeypatch.setenv("HEAT_SHARD_LAG", "1")
     out = {}
@@ -911,7 +911,7 @@ def test_full_size_sharded_properties(torch_cuda, cfg):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import NativeShardTrainer
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     kw = {"sample_users": 0.02} if cfg == "c5" else {}
     tr, _, sp = make_dataset(cfg, **kw)
     m = DeviceModel(init_matrix(tr.num_users, sp.dim, InitSpec(seed=0)).values,
@@ -943,7 +943,7 @@ def test_train_device_resident_run_with_checkpoints(torch_cuda, tmp_path):
     from paper_2304_07334_b200 import LossParams, TrainingConfig, init_matrix, InitSpec
     from paper_2304_07334_b200.dataset import from_user_lists
     from paper_2304_07334_b200.embeddings import load_model
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     from paper_2304_07334_b200.trainer import train
     z = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
     tr, _, _ = make_dataset("c1")
@@ -1109,7 +1109,7 @@ def test_c2_recall_parity_throughput_vs_deterministic(torch_cuda):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.evaluator import evaluate_device
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     tr, te, sp = make_dataset("c2")
     rec = {}
     for mode in (N.MODE_HOGWILD, N.MODE_EXACT):
@@ -1181,7 +1181,7 @@ def test_delta_mode_every_kernel_family(torch_cuda, K, N):
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.parallel import PipelinedShardTrainer, run_loopback
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_clustered
+    from workloads import make_clustered
     train, _ = make_clustered(600, 3000, 8, 30, seed=5)
     S = init_matrix(600, K, InitSpec(seed=1)).values
     T = init_matrix(3000, K, InitSpec(seed=2)).values
@@ -1216,7 +1216,7 @@ def test_full_size_properties(torch_cuda, cfg):
     from paper_2304_07334_b200.device import DeviceModel
     from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
     from paper_2304_07334_b200.rng import epoch_stream, shuffle_seed
-    from paper_2304_07334_b200.synth import make_dataset
+    from workloads import make_dataset
     kw = {"sample_users": 0.02} if cfg == "c5" else {}
     tr, _, sp = make_dataset(cfg, **kw)
     S = init_matrix(tr.num_users, sp.dim, InitSpec(seed=0)).values

@@ -20,7 +20,7 @@ from paper_2304_07334_b200 import (AggregatorConfig, InitSpec, LossParams, Sampl
 from paper_2304_07334_b200 import rng as R
 from paper_2304_07334_b200.dataset import epoch_pairs, from_pairs, with_universe
 from paper_2304_07334_b200.parallel import delta_capacity, merge_order, shard_epoch
-from paper_2304_07334_b200.synth import CONFIGS, make_clustered, make_dataset
+from workloads import CONFIGS, make_clustered, make_dataset
 
 
 def test_abi_exports_every_declared_symbol():
@@ -306,3 +306,32 @@ def test_metrics_json_schema():
     from paper_2304_07334_b200.evaluator import MetricsReport, metrics_json
     obj = json.loads(metrics_json(3, MetricsReport(0.5, 0.25, 20, 11)))
     assert obj == {"epoch": 3, "recall@20": 0.5, "ndcg@20": 0.25, "users": 11}
+
+
+def test_reference_arm_never_loads_the_product():
+    """bench.py --impl reference: data from workloads.py, epoch order and the
+    timed training from oracle/ — no module of the product package imported
+    and libheat_b200.so never mapped (Next 1)."""
+    import json
+    import subprocess
+    import sys
+    code = (
+        "import runpy, sys, json\n"
+        "sys.argv = ['bench.py', '--impl', 'reference', '--config', 'c1', '--steps', '1',"
+        " '--warmup', '0', '--ref-sample', '2000']\n"
+        "try:\n"
+        "    runpy.run_path('bench.py', run_name='__main__')\n"
+        "except SystemExit:\n"
+        "    pass\n"
+        "mods = sorted(m for m in sys.modules if m.startswith('paper_2304_07334_b200'))\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "print('CHECK ' + json.dumps({'mods': mods, 'so': 'libheat_b200' in maps}))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         timeout=600, check=True).stdout
+    lines = out.strip().splitlines()
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    chk = json.loads(lines[-1][len("CHECK "):])
+    assert chk == {"mods": [], "so": False}, chk

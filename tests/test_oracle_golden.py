@@ -15,7 +15,7 @@ import pytest
 from oracle import oracle as O
 from paper_2304_07334_b200 import rng as hrng
 from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
-from paper_2304_07334_b200.synth import make_dataset
+from workloads import make_dataset
 
 from conftest import GOLDEN
 

@@ -28,12 +28,12 @@ def torch_cuda():
 
 
 def clustered_small():
-    from paper_2304_07334_b200.synth import make_clustered
+    from workloads import make_clustered
     return make_clustered(60, 240, 6, 24, seed=3)
 
 
 def clustered_medium():
-    from paper_2304_07334_b200.synth import make_clustered
+    from workloads import make_clustered
     return make_clustered(800, 1600, 16, 40, affinity=0.97, seed=11)
 
 

@@ -1,5 +1,11 @@
 """Seeded synthetic stand-ins for the paper's datasets.
 
+BENCH AND TEST INPUT DATA, not product code: both bench.py arms (ours and
+``--impl reference``), the tests and the golden-vector script build their
+workloads here.  It is pure numpy and imports nothing from the product
+package or the oracle, so the reference arm's data path never loads the
+product's native library.
+
 The public datasets (Gowalla, Yelp2018, Amazon-Books) are not
 available offline.  BASELINE.json configs 2-4 carry their shapes; this module
 generates interaction sets with those user/item/interaction counts:
@@ -25,7 +31,47 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .dataset import InteractionSet, from_pairs
+
+
+class InteractionSet:
+    """Minimal CSR interaction set with the attributes the reference's
+    ``InteractionSet`` exposes (dataset.py:29-52): ``items[offsets[u]:
+    offsets[u+1]]`` is user u's sorted, distinct positives.  Both the product
+    (duck-typed) and the reference accept it."""
+
+    __slots__ = ("num_users", "num_items", "offsets", "items")
+
+    def __init__(self, num_users: int, num_items: int, offsets, items):
+        self.num_users, self.num_items = int(num_users), int(num_items)
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        self.items = np.ascontiguousarray(items, dtype=np.int32)
+        assert len(self.offsets) == self.num_users + 1
+        assert self.offsets[-1] == len(self.items)
+
+    def slice(self, user: int) -> np.ndarray:
+        return self.items[self.offsets[user]:self.offsets[user + 1]]
+
+    @property
+    def num_pairs(self) -> int:
+        return int(len(self.items))
+
+
+def from_pairs(users, items, num_users: int, num_items: int) -> InteractionSet:
+    """CSR from parallel (user, item) arrays: sorted per user, duplicates dropped."""
+    key = np.unique(np.asarray(users, np.int64) * num_items + np.asarray(items, np.int64))
+    u = key // num_items
+    offsets = np.zeros(num_users + 1, dtype=np.int64)
+    np.cumsum(np.bincount(u, minlength=num_users), out=offsets[1:])
+    return InteractionSet(num_users, num_items, offsets, (key % num_items).astype(np.int32))
+
+
+def init_table(rows: int, dim: int, seed: int = 0, std: float = 0.01) -> np.ndarray:
+    """rows x dim float32 table drawn N(0, std) by numpy's PCG64 — the draw the
+    reference's ``init_matrix(rows, dim, InitSpec(seed=seed))`` makes
+    (embeddings.py:85-95), so S == T[:U] at init as with the CLI
+    (cli.py:129-132)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.normal(0.0, std, size=(rows, dim)).astype(np.float32)
 
 GEN_SEED = 12345
 
