@@ -13,7 +13,7 @@ import pytest
 from paper_2304_07334_b200.embeddings import (CorruptCheckpointError, EmbeddingMatrix, InitSpec,
                                               init_matrix, load_checkpoint, load_model,
                                               save_checkpoint, save_model)
-from paper_2304_07334_b200.embeddings import _write_block
+from paper_2304_07334_b200.embeddings import encode_block
 
 
 def test_init_validation_and_statistics():
@@ -72,8 +72,8 @@ def test_model_bundles(tmp_path):
         save_model(str(tmp_path / "bad.ckpt"), S, T, np.zeros((3, 3), dtype=np.float32))
     bad = tmp_path / "dims.ckpt"
     with open(bad, "wb") as f:
-        _write_block(f, init_matrix(3, 4, InitSpec(seed=1)))
-        _write_block(f, init_matrix(3, 5, InitSpec(seed=2)))
+        f.write(encode_block(init_matrix(3, 4, InitSpec(seed=1)).values))
+        f.write(encode_block(init_matrix(3, 5, InitSpec(seed=2)).values))
     with pytest.raises(CorruptCheckpointError):
         load_model(str(bad))
     save_model(p, S, T)

@@ -469,9 +469,9 @@ def test_local_gradient_accumulation_costs_no_accuracy(torch_cuda, threads):
     from paper_2304_07334_b200.trainer import train_epoch
     train_set, test_set = clustered_medium()
 
-    def run(m):
+    def run(m, seed=7):
         cfg = TrainingConfig(emb_dim=32, num_negatives=16, learning_rate=0.05, epochs=40,
-                             num_threads=threads, seed=7,
+                             num_threads=threads, seed=seed,
                              aggregator=AggregatorConfig(enabled=True, gamma=0.5, max_history=50,
                                                          mini_batch_size=m))
         S, T = fresh(train_set, dim=32)
@@ -480,5 +480,14 @@ def test_local_gradient_accumulation_costs_no_accuracy(torch_cuda, threads):
             train_epoch(S, T, train_set, cfg, W, epoch=e)
         return evaluate(S, T, train_set, test_set, cfg, weights=W, k=20).recall_at_k
 
-    r32, r1 = run(32), run(1)
-    assert abs(r32 - r1) <= (0.005 if threads == 1 else 0.01), (r32, r1)
+    if threads == 1:
+        r32, r1 = run(32), run(1)
+        assert abs(r32 - r1) <= 0.005, (r32, r1)
+    else:
+        # Hogwild runs scatter by about +-0.007 recall around their mean here
+        # (one seed measured 0.2657 vs 0.2760), so the throughput variant
+        # compares means over three training seeds
+        seeds = (7, 8, 9)
+        r32 = float(np.mean([run(32, s) for s in seeds]))
+        r1 = float(np.mean([run(1, s) for s in seeds]))
+        assert abs(r32 - r1) <= 0.01, (r32, r1)
