@@ -24,7 +24,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 # per-file extra flags: the exact kernel must never contract a*b+c into FMA
 EXTRA = {"heat_exact.cu": ["--fmad=false"], "heat_exact_spec.cu": ["--fmad=false"]}
 SOURCES = ["heat_capi.cu", "heat_sample.cu", "heat_exact.cu", "heat_exact_spec.cu",
-           "heat_hogwild.cu", "heat_hogwild_staged.cu",
+           "heat_hogwild.cu", "heat_hogwild_staged.cu", "heat_hogwild_stream.cu",
            "heat_hogwild_resident.cu", "heat_hogwild_multi.cu", "heat_agg_hogwild.cu", "heat_shard.cu",
            "heat_eval.cu", "heat_host.cpp"]
 

@@ -496,7 +496,8 @@ bool device_step_supported(const heat_sgd_params *p, const float *S, const float
     if (((uintptr_t)S % 16) || ((uintptr_t)T % 16)) return false;
     const char *impl = getenv("HEAT_HOGWILD_IMPL");
     if (getenv("HEAT_FORCE_GENERIC")) return false;
-    return !impl || impl[0] == 'r' || impl[0] == 'm' || impl[0] == 's' || impl[0] == 't';
+    return !impl || impl[0] == 'r' || impl[0] == 'm' || impl[0] == 's' || impl[0] == 't' ||
+           impl[0] == 'w';
 }
 
 }  // namespace heat

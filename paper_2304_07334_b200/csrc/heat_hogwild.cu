@@ -482,6 +482,13 @@ cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *worke
         cudaError_t e = launch_hogwild_resident(a, stream, workers_out);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
+    // register-streamed rows (heat_hogwild_stream.cu)
+    if (aligned && impl && impl[0] == 'w') {
+        cudaError_t e = launch_hogwild_stream(a, stream, workers_out);
+        if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue &&
+            e != cudaErrorMemoryAllocation)
+            return e;
+    }
     // several warps per pair (large N, K <= 64: the pair does not fit the
     // resident kernel, and one warp per pair leaves the SMs underoccupied)
     const bool multi_forced = impl && impl[0] == 'm';

@@ -62,6 +62,8 @@ cudaError_t launch_hogwild_resident(const HogwildArgs &a, cudaStream_t stream, i
 cudaError_t launch_hogwild_multi(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t stream, int *workers_out,
                                   bool bulk);
+cudaError_t launch_hogwild_stream(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
+bool hogwild_stream_supported(const HogwildArgs &a);
 
 size_t agg_hogwild_scratch_bytes(int K, int window);
 cudaError_t launch_agg_hogwild(const HogwildArgs &base, const heat_agg_params &agg,
