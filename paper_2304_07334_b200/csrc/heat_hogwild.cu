@@ -482,8 +482,12 @@ cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *worke
         cudaError_t e = launch_hogwild_resident(a, stream, workers_out);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
-    // register-streamed rows (heat_hogwild_stream.cu)
-    if (aligned && impl && impl[0] == 'w') {
+    // register-streamed rows (heat_hogwild_stream.cu): the default for
+    // K = 128 (configs 4/5: c4 29.4 M vs 22.4 M samples/s staged, c5 14.5 M vs
+    // 12.7 M); for K <= 64 the pair-per-CTA kernels keep more warps busy
+    // under the config windows (c3: multi 77.6 M vs 40.4 M)
+    const bool wide_default = (!impl || (impl[0] == 'r' && impl[1] == 'e')) && a.K == 128;
+    if (aligned && ((impl && impl[0] == 'w') || wide_default)) {
         cudaError_t e = launch_hogwild_stream(a, stream, workers_out);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue &&
             e != cudaErrorMemoryAllocation)

@@ -153,12 +153,26 @@ __global__ void __launch_bounds__(32, MINB)
         return (int64_t)__shfl_sync(kFull, t, 0);
     };
 
-    int64_t t = claim_next();
-    while (t < npairs) {
-        const int64_t p = k_start + t;
-        const int32_t u = a.users[p];
-        const int32_t pos = a.items[p];
-        const uint64_t pg = a.pair_index ? (uint64_t)a.pair_index[p] : (uint64_t)p;
+    // the next pair is claimed and its (user, item, RNG key) fetched one pair
+    // ahead, so a pair starts without a chain of dependent global reads
+    // (atomic -> ids -> rows).  Only read-only inputs are prefetched: table
+    // rows are read when the pair starts.
+    struct Next { int64_t t; int32_t u, pos; uint64_t pg; };
+    auto fetch = [&](int64_t tt) -> Next {
+        Next n{tt, 0, 0, 0};
+        if (tt < npairs) {
+            const int64_t pp = k_start + tt;
+            n.u = a.users[pp];
+            n.pos = a.items[pp];
+            n.pg = a.pair_index ? (uint64_t)a.pair_index[pp] : (uint64_t)pp;
+        }
+        return n;
+    };
+    Next nx = fetch(claim_next());
+    while (nx.t < npairs) {
+        const int32_t u = nx.u;
+        const int32_t pos = nx.pos;
+        const uint64_t pg = nx.pg;
 
         float4 uv[V];
 #pragma unroll
@@ -192,6 +206,7 @@ __global__ void __launch_bounds__(32, MINB)
         };
         issue(0, 0, 0);
         issue(1, 1, 0);
+        nx = fetch(claim_next());
 
         // fp32 u.u for the screen; the exact binary64 ss (trainer.py:176-178)
         // is summed at the end of the pair, where the written rows are resolved
@@ -217,6 +232,8 @@ __global__ void __launch_bounds__(32, MINB)
             for (int j = 0; j < V; ++j) *reinterpret_cast<float4 *>(urow + 32 * j + 4 * c) = uv[j];
         }
         __syncwarp();
+        // exact ss = u.u as trainer.py:176-178 sums it, while the first rows load
+        const double ss = seq_dot<K>(urow, urow);
         const bool decay_all = a.l2 != 0.f;
         int cnt = 0;  // rows recorded for writing (same value in every lane)
 
@@ -298,9 +315,6 @@ __global__ void __launch_bounds__(32, MINB)
             round(0, rd + 2, more);
             round(1, rd + 3, more);
         }
-        // every row of the pair is read: claim the next pair (the atomic's
-        // latency overlaps the resolve and the writes)
-        const int64_t tn = claim_next();
 
         // resolve, four recorded rows at a time (one per row slot g): re-read
         // the row into its snapshot slot (shared memory, then the worker's
@@ -310,7 +324,6 @@ __global__ void __launch_bounds__(32, MINB)
         // (trainer.py:184-227).  A band row that is not written becomes a
         // hole (id -1).  Every read of the pair precedes every write.
         __syncwarp();
-        const double ss = seq_dot<K>(urow, urow);
         const float irs = ss > 0.0 ? rsqrtf((float)ss) : 0.f;
         const double wneg = a.mu * (1.0 / (double)N);
         double hinge = 0.0, sim_p = 0.0;
@@ -434,7 +447,6 @@ __global__ void __launch_bounds__(32, MINB)
         if (lane == 0) loss += (1.0 - sim_p) + wneg * hinge;
         ++npairs_mine;
         __syncwarp();
-        t = tn;
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
