@@ -23,6 +23,10 @@ time reads /root/reference):
                       tables plus per-epoch mean losses.
 - c2_prefix.json      first 8 steps (B=1024) of config 2 epoch 0: running
                       loss and sha256 of S/T after each step.
+- c2_epoch0.json      config 2's whole epoch 0 (805 steps of B=1024): running
+                      loss / degenerate count and S/T sha256 after every step.
+- c3_prefix.json,     first 8 steps of configs 3 (B=1024, K 64, N 500) and 4
+  c4_prefix.json      (B=2048, K 128, N 1000): the same records.
 - eval.npz            evaluate() on c1-shaped data with a 20 % split (trained
                       tables from c1_epoch, k=20 and k=5, cosine and dot),
                       top-k lists of the first 64 users; evaluate() on the
@@ -257,6 +261,59 @@ def c2_prefix_golden(steps=8, B=1024):
         json.dump(out, f, indent=1)
 
 
+def shape_golden(name: str, steps: int | None, fname: str, hash_every: int = 1):
+    """Config `name` (workloads.CONFIGS) trained by the reference exactly as
+    train_epoch(num_threads=1) does, one _train_chunk call per step of the
+    config's B pairs: running loss / degenerate count after every step and
+    sha256 of S and T after every `hash_every`-th step (and the last).
+    `steps` None = the whole of epoch 0."""
+    train, _, spec = make_dataset(name)
+    rtrain = rset(train)
+    K, N, B = spec.dim, spec.negatives, spec.batch
+    S = r_init(train.num_users, K, RInit(seed=0))
+    T = r_init(train.num_items, K, RInit(seed=0))
+    ep_users, ep_items = r_epoch_pairs(rtrain, stream_state(0, 0x53485546, 0)[0] >> 1)
+    total = len(ep_users) if steps is None else min(len(ep_users), steps * B)
+    nsteps = (total + B - 1) // B
+    cfg = rtrainer.TrainingConfig(emb_dim=K, num_negatives=N, learning_rate=spec.learning_rate,
+                                  num_threads=1, loss=RLoss(mu=spec.mu, theta=spec.theta), seed=0)
+    st = rtrainer._ThreadState(cfg, T, (0x45504F43, 0, 0))
+    w = np.zeros((1, 1), dtype=np.float32)
+    out = {"config": name, "steps": nsteps, "B": B, "pairs": total, "K": K, "N": N,
+           "theta": spec.theta, "mu": spec.mu, "lr": spec.learning_rate,
+           "loss": [], "degen": [], "hash_steps": [], "S_sha256": [], "T_sha256": []}
+    for s in range(nsteps):
+        a, b = s * B, min(total, (s + 1) * B)
+        rtrainer._train_chunk(
+            S.values, T.values, ep_users, ep_items, a, b, False, T.rows, st.rng_state,
+            st.tile_ids, st.tile_emb, st.tile_ctr, 1, True, N, spec.learning_rate, 0.0,
+            spec.mu, spec.theta, False, w, 0.5, spec.learning_rate, 32, False, rtrain.offsets,
+            rtrain.items, 100, st.agg_accu, st.agg_ctr, st.ubuf, st.pooled, st.ugrad, st.wh,
+            st.pos_buf, st.neg_buf, st.neg_ids, st.tts, st.sts, st.sims, st.dnegs, st.loss_out,
+            st.degen_out, st.phase_cycles, False)
+        out["loss"].append(float(st.loss_out[0]))
+        out["degen"].append(int(st.degen_out[0]))
+        if (s + 1) % hash_every == 0 or s == nsteps - 1:
+            out["hash_steps"].append(s)
+            out["S_sha256"].append(hashlib.sha256(S.values.tobytes()).hexdigest())
+            out["T_sha256"].append(hashlib.sha256(T.values.tobytes()).hexdigest())
+    out["pairs_sha256"] = hashlib.sha256(ep_users[:total].tobytes() +
+                                         ep_items[:total].tobytes()).hexdigest()
+    with open(os.path.join(HERE, fname), "w") as f:
+        json.dump(out, f, indent=0)
+
+
+def shapes_golden():
+    """The graded shapes: config 2's whole epoch 0, and prefixes of configs 3
+    and 4 (K 64 / N 500, K 128 / N 1000)."""
+    shape_golden("c2", None, "c2_epoch0.json", hash_every=1)
+    print("c2 epoch 0 done")
+    shape_golden("c3", 8, "c3_prefix.json")
+    print("c3 prefix done")
+    shape_golden("c4", 8, "c4_prefix.json")
+    print("c4 prefix done")
+
+
 def eval_golden(S_c1, T_c1):
     tr, te, _ = make_dataset("c1", test_fraction=0.2)
     rtr, rte = rset(tr), rset(te)
@@ -332,6 +389,9 @@ def agg_golden():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "shapes":
+        shapes_golden()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "agg":
         agg_golden()
         print("agg done")
@@ -346,5 +406,6 @@ if __name__ == "__main__":
     print("c2 prefix done")
     eval_golden(S, T)
     print("eval done")
+    shapes_golden()
     agg_golden()
     print("agg done")

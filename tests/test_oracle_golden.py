@@ -139,6 +139,38 @@ def test_oracle_c2_prefix_bit_exact():
         assert hashlib.sha256(T.tobytes()).hexdigest() == g["T_sha256"][s]
 
 
+@pytest.mark.parametrize("fname,hash_stride", [("c3_prefix.json", 1), ("c4_prefix.json", 1),
+                                             ("c2_epoch0.json", 100)])
+def test_oracle_graded_shapes_bit_exact(fname, hash_stride):
+    """The graded shapes from the reference: config 2's whole epoch 0 (817
+    steps), and the first 8 steps of configs 3 (K 64, N 500) and 4 (K 128,
+    N 1000).  The oracle's running loss equals the reference's after every
+    step; S/T hashes are checked every `hash_stride`-th recorded step and at
+    the end."""
+    from workloads import CONFIGS
+    with open(os.path.join(GOLDEN, fname)) as f:
+        g = json.load(f)
+    spec = CONFIGS[g["config"]]
+    train, _, _ = make_dataset(g["config"])
+    S = init_matrix(train.num_users, spec.dim, InitSpec(seed=0)).values
+    T = init_matrix(train.num_items, spec.dim, InitSpec(seed=0)).values
+    ep_u, ep_i = O.epoch_pairs(train.offsets, train.items, train.num_users, O.shuffle_seed(0, 0))
+    n, B = g["pairs"], g["B"]
+    assert hashlib.sha256(ep_u[:n].tobytes() + ep_i[:n].tobytes()).hexdigest() == g["pairs_sha256"]
+    hashed = dict(zip(g["hash_steps"], zip(g["S_sha256"], g["T_sha256"])))
+    check = set(g["hash_steps"][::hash_stride]) | {g["hash_steps"][-1]}
+    state = O.derive_stream(0, 0x45504F43, 0, 0)
+    loss = 0.0
+    for s in range(g["steps"]):
+        r = O.train_range(S, T, ep_u, ep_i, s * B, min(n, (s + 1) * B), state, n_neg=spec.negatives,
+                          lr=spec.learning_rate, mu=spec.mu, theta=spec.theta, loss0=loss)
+        state, loss = r.state, r.loss
+        assert loss == g["loss"][s], s
+        if s in check:
+            assert (hashlib.sha256(S.tobytes()).hexdigest(),
+                    hashlib.sha256(T.tobytes()).hexdigest()) == hashed[s], s
+
+
 def test_oracle_evaluator_matches_reference():
     z = np.load(os.path.join(GOLDEN, "eval.npz"))
     c1 = np.load(os.path.join(GOLDEN, "c1_epoch.npz"))
