@@ -293,23 +293,37 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                 ttf += __shfl_xor_sync(0xffffffffu, ttf, 1);
                 stf += __shfl_xor_sync(0xffffffffu, stf, 1);
             }
-            // similarity and loss weight (trainer.py:184-221)
+            // similarity and loss weight (trainer.py:184-221): fp32 screen;
+            // rows that can reach the margin are decided from the reference's
+            // binary64 sums over the staged row (heat_row_update.cuh)
+            float sf = 0.f;
+            const bool band =
+                valid && margin_band(r, a.cosine, (float)ss, ttf, stf, rss, theta_f, &sf);
+            double ssx = ss, ttx = (double)ttf, stx = (double)stf;
+            for (unsigned mb = __ballot_sync(0xffffffffu, band && lead), first = 1; mb; first = 0) {
+                const int src = __ffs(mb) - 1;
+                mb &= mb - 1;
+                double s_, t_, c_;
+                warp_dots64<K>(urow, ring + ((size_t)slot * SR + src / LPR) * G::SLOTF,
+                               [](int k) { return G::pcol(k); }, first != 0, s_, t_, c_);
+                if (first) ssx = s_;
+                if (lane / LPR == src / LPR) {
+                    ttx = t_;
+                    stx = c_;
+                }
+            }
+            if (!band) ssx = ss;
             bool write = false;
             double wt = 0.0;
             if (valid) {
                 bool degenerate = false;
-                double sim = (double)stf;
+                double sim = band ? stx : (double)sf;
                 if (a.cosine) {
-                    if (ss <= 0.0 || ttf <= 0.f) {
-                        degenerate = true;
-                        sim = 0.0;
-                        if (lead) ++degen;
-                    } else {
-                        const float sf = stf * rss * rsqrtf(ttf);
-                        sim = (double)sf;
-                        if (r > 0 && sf > theta_f - 1e-5f)
-                            sim = (double)stf / (sqrt(ss) * sqrt((double)ttf));
+                    if (band) {
+                        degenerate = ssx <= 0.0 || ttx <= 0.0;
+                        sim = degenerate ? 0.0 : stx / (sqrt(ssx) * sqrt(ttx));
                     }
+                    if (degenerate && lead) ++degen;
                 }
                 if (r == 0) {
                     sim_p = sim;
@@ -334,7 +348,7 @@ __global__ void __launch_bounds__(32 * NW, MULTI_MINB)
                 for (int v = 0; v < VW; ++v)
                     snap[cnt * K + lane * VW + v] = srow[G::pcol(lane * VW + v)];
                 if (lane == src)
-                    ents[cnt] = WriteEntry{(double)ttf, (double)stf, wt, ids[slot * SR + src / LPR], 0};
+                    ents[cnt] = WriteEntry{ttx, stx, wt, ids[slot * SR + src / LPR], 0};
                 ++cnt;
             }
             __syncwarp();

@@ -89,7 +89,7 @@ template <int K, int NB, bool EARLY, bool SPLIT, bool IDPF, bool DR>
 // 7 resident CTAs per SM (the window allows ~7 pairs per SM), but never
 // fewer than 64 registers per thread
 __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB : 1) : 7))
-    hogwild_resident(HogwildArgs a, FastMod fm, int n_workers) {
+    hogwild_resident(HogwildArgs a, FastMod fm, int n_workers, int strict) {
     using G = RsGeom<K>;
     constexpr int VW = G::VW;
     extern __shared__ __align__(128) unsigned char sm[];
@@ -225,22 +225,35 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
         }
         const float ttf = (ta.x + ta.y) + (tb.x + tb.y);
         const float stf = (sa.x + sa.y) + (sb.x + sb.y);
+        // fp32 screen; rows that can reach the margin are decided from the
+        // reference's binary64 sums over the resident row (heat_row_update.cuh)
+        float sf = 0.f;
+        const bool band = valid && margin_band(r, a.cosine, sp, ttf, stf, rss, theta_f, &sf);
+        double ssx = ss, ttx = (double)ttf, stx = (double)stf;
+        for (unsigned mb = __ballot_sync(0xffffffffu, band), first = 1; mb; first = 0) {
+            const int src = __ffs(mb) - 1;
+            mb &= mb - 1;
+            double s_, t_, c_;
+            warp_dots64<K>(urow, my_stage + src * G::SLOTF, ContiguousCols{}, first != 0, s_, t_,
+                           c_);
+            if (first) ssx = s_;  // every lane: the binary64 u.u of the pair
+            if (lane == src) {
+                ttx = t_;
+                stx = c_;
+            }
+        }
+        if (!band) ssx = ss;
         bool write = false;
         double wt = 0.0, hinge = 0.0, sim = 0.0;
         if (valid) {
             bool degenerate = false;
-            sim = (double)stf;
+            sim = band ? stx : (double)sf;
             if (a.cosine) {
-                if (sp <= 0.f || ttf <= 0.f) {
-                    degenerate = true;
-                    sim = 0.0;
-                    ++degen;
-                } else {
-                    const float sf = stf * rss * rsqrtf(ttf);
-                    sim = (double)sf;
-                    if (r > 0 && sf > theta_f - 1e-5f)
-                        sim = (double)stf / (sqrt(ss) * sqrt((double)ttf));
+                if (band) {
+                    degenerate = ssx <= 0.0 || ttx <= 0.0;
+                    sim = degenerate ? 0.0 : stx / (sqrt(ssx) * sqrt(ttx));
                 }
+                if (degenerate) ++degen;
             }
             if (r == 0) {
                 wt = -1.0;
@@ -275,12 +288,13 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
             while (m) {
                 const int src = __ffs(m) - 1;
                 m &= m - 1;
-                const float tt_s = __shfl_sync(0xffffffffu, ttf, src);
-                const float st_s = __shfl_sync(0xffffffffu, stf, src);
+                const double tt_s = __shfl_sync(0xffffffffu, ttx, src);
+                const double st_s = __shfl_sync(0xffffffffu, stx, src);
+                const double ss_s = __shfl_sync(0xffffffffu, ssx, src);
                 const float w_s = (float)__shfl_sync(0xffffffffu, wt, src);
                 const int32_t id_s = (int32_t)__shfl_sync(0xffffffffu, id, src);
-                const WriteEntry we{(double)tt_s, (double)st_s, (double)w_s, id_s, 0};
-                const RowCoef co = row_coef_f(we, ss, rss, a.lr, a.l2, a.cosine);
+                const WriteEntry we{tt_s, st_s, (double)w_s, id_s, 0};
+                const RowCoef co = row_coef_f(we, ss_s, rss, a.lr, a.l2, a.cosine);
                 const float *srow = my_stage + src * G::SLOTF;
                 float d[VW];
 #pragma unroll
@@ -321,6 +335,13 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
             rs_red<VW>(a.S + u * K + lane * VW, d);
         }
         __syncwarp();
+        // strict (window 1): the next pair reads only after every warp's
+        // writes of this one, so the worker runs the reference's sequence;
+        // otherwise a warp may read pair t+1 while another still writes t
+        if (strict) {
+            __threadfence_block();
+            __syncthreads();
+        }
     }
     // telemetry
 #pragma unroll
@@ -361,7 +382,8 @@ static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int
     if (a.window > 0 && a.window < nw) nw = a.window;
     if (a.stop - a.start < nw) nw = a.stop - a.start;
     if (workers_out) *workers_out = (int)nw;
-    kern<<<(unsigned)nw, 32 * NB, smem, st>>>(a, FastMod::make((uint64_t)a.num_items), (int)nw);
+    kern<<<(unsigned)nw, 32 * NB, smem, st>>>(a, FastMod::make((uint64_t)a.num_items), (int)nw,
+                                              a.window == 1 ? 1 : 0);
     return cudaGetLastError();
 }
 

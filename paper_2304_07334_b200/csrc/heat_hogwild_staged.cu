@@ -461,21 +461,48 @@ __global__ void __launch_bounds__(32)
             }
             // similarity and loss weight (trainer.py:184-221).  fp32 screen; the
             // binary64 value only for rows that can cross the margin.
+            // fp32 dots: screen, then the reference's binary64 sums for the
+            // rows that can reach the margin (heat_row_update.cuh)
+            bool band = false;
+            float sf = 0.f;
+            double ssx = ss;
+            if constexpr (!F64) {
+                band = valid && margin_band(r, a.cosine, (float)ss, (float)tt, (float)st, rss,
+                                            theta_f, &sf);
+                for (unsigned mb = __ballot_sync(0xffffffffu, band && lead), first = 1; mb;
+                     first = 0) {
+                    const int src = __ffs(mb) - 1;
+                    mb &= mb - 1;
+                    double s_, t_, c_;
+                    warp_dots64<K>(up, ring + ((size_t)slot * SR + src / LPR) * G::SLOTF,
+                                   [](int k) { return G::pcol(k); }, first != 0, s_, t_, c_);
+                    if (first) ssx = s_;
+                    if (lane / LPR == src / LPR) {
+                        tt = t_;
+                        st = c_;
+                    }
+                }
+                if (!band) ssx = ss;
+            }
             bool write = false;
             double w = 0.0;
             if (valid) {
                 bool degenerate = false;
                 double sim = st;
                 if (a.cosine) {
-                    if (ss <= 0.0 || tt <= 0.0) {
-                        degenerate = true;
-                        sim = 0.0;
-                        if (lead) ++degen;
+                    if (F64 || band) {
+                        if (ssx <= 0.0 || tt <= 0.0) {
+                            degenerate = true;
+                            sim = 0.0;
+                        } else {
+                            sim = st / (sqrt(ssx) * sqrt(tt));
+                        }
                     } else {
-                        const float sf = (float)st * rss * rsqrtf((float)tt);
                         sim = (double)sf;
-                        if (F64 || (r > 0 && sf > theta_f - 1e-5f)) sim = st / (sqrt(ss) * sqrt(tt));
                     }
+                    if (degenerate && lead) ++degen;
+                } else if (!F64 && !band) {
+                    sim = (double)sf;
                 }
                 if (r == 0) {
                     sim_p = sim;

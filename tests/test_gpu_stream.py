@@ -199,3 +199,21 @@ def test_device_range_mode_in_shard_runtime(torch_cuda, wide):
     ref = m.counters.read().loss
     assert abs(c.loss - ref) <= 0.03 * abs(ref), (c.loss, ref)
     tr.close()
+
+
+@pytest.mark.parametrize("impl,K,N", [("resident", 64, 100), ("resident", 32, 200),
+                                      ("multi", 64, 500), ("multi", 32, 300),
+                                      ("staged", 64, 300), ("staged", 16, 50)])
+def test_every_fp32_family_decides_the_margin_in_binary64(torch_cuda, monkeypatch, impl, K, N):
+    """The other fp32 throughput kernels (pair per CTA, several warps per pair,
+    staged ring) screen in fp32 and decide rows near theta from the
+    reference's binary64 sums (heat_row_update.cuh ref_dots): at window 1,
+    with theta inside the similarity distribution, the active count matches
+    the oracle's and loss / tables stay within 1e-4."""
+    monkeypatch.setenv("HEAT_HOGWILD_IMPL", impl)
+    c, r, S, S2, T, T2 = _run(K, N, 0.1)
+    assert c.pairs == 400 and c.degenerate == r.degenerate
+    assert r.active > 100
+    assert abs(c.active - r.active) <= max(2, r.active // 1000), (c.active, r.active)
+    assert abs(c.loss - r.loss) <= 1e-4 * abs(r.loss)
+    assert _rel_fro(S, S2) <= 1e-4 and _rel_fro(T, T2) <= 1e-4
