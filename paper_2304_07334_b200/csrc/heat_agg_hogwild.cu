@@ -330,14 +330,13 @@ size_t agg_hogwild_scratch_bytes(int K, int window) {
 template <int K>
 static cudaError_t run_agg(const HogwildArgs &base, const heat_agg_params &agg, void *scratch,
                            cudaStream_t st) {
-    static bool attr_set = false;  // per process: the attribute is per function, any device
-    if (!attr_set) {
-        cudaFuncSetAttribute(agg_gemm_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)agg_gemm_smem<K>());
-        cudaFuncSetAttribute(agg_gemm_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)agg_gemm_smem<K>());
-        attr_set = true;
-    }
+    // the dynamic shared-memory opt-in is per device context: kernel_occupancy
+    // applies it once per (device, kernel, size), under its lock
+    cudaError_t oe;
+    kernel_occupancy((const void *)agg_gemm_kernel<K, false>, 256, agg_gemm_smem<K>(), &oe);
+    if (oe != cudaSuccess) return oe;
+    kernel_occupancy((const void *)agg_gemm_kernel<K, true>, 256, agg_gemm_smem<K>(), &oe);
+    if (oe != cudaSuccess) return oe;
     const int64_t C = agg_step(base.window);
     float *P = reinterpret_cast<float *>(scratch);
     float *Q = P + C * K;

@@ -70,8 +70,16 @@ class PairPrefetcher:
         if hit is not None:
             th, holder = hit
             th.join()
-            if "err" not in holder:
+            # the key holds ids only: reuse the prefetched order only if it was
+            # computed from this very object (its arrays), never from an
+            # earlier set whose ids CPython has since recycled
+            src = holder.get("train")
+            same = (src is not None and src[0] is train and src[1] is train.items
+                    and src[2] is train.offsets)
+            if "err" not in holder and same:
                 return holder["bufs"]
+            if "bufs" in holder:
+                self.release(holder["bufs"])
         return self._compute(train, seed, self._buffers(train.num_pairs))
 
     # epochs computed ahead, one host thread each: the shuffle is sequential
@@ -100,7 +108,9 @@ class PairPrefetcher:
             th.join()
             if "bufs" in holder:
                 self.release(holder["bufs"])
-        holder: dict = {}
+        # strong references to the set the order is computed from (checked by
+        # identity in get())
+        holder: dict = {"train": (train, train.items, train.offsets)}
         bufs = self._buffers(train.num_pairs)
 
         def run():

@@ -63,7 +63,7 @@ class TrainResult:
 @dataclass
 class GpuOptions:
     mode: str | None = None  # None: exact when num_threads == 1, else hogwild
-    window: int = 0          # hogwild: pairs in flight (0 = the GPU's capacity)
+    window: int = 0          # hogwild: pairs in flight (0 = default_window())
     fp64: bool = False       # hogwild: binary64 dot products
     device: object = None
 
@@ -136,11 +136,28 @@ def resolve_mode(cfg) -> int:
     return N.MODE_EXACT if mode == "exact" else N.MODE_HOGWILD
 
 
-def sgd_params(model: DeviceModel, cfg, epoch: int, mode: int) -> N.SgdParams:
+# Hogwild window when none is configured: one pair in flight per 512 pairs of
+# the epoch (never fewer than the reference's thread count), capped by the
+# kernels at the GPU's resident workers.  The BASELINE configs run with
+# 1/815 (c2, B = 1024) and 1/1455 (c4, B = 2048) of an epoch in flight; a
+# small interaction set then keeps the same staleness instead of putting a
+# quarter of its epoch in flight at once (e.g. 7.7 k pairs -> 15 in flight,
+# the reference's 8-thread pool runs 8).
+WINDOW_PAIRS_PER_SLOT = 512
+
+
+def default_window(cfg, num_pairs: int) -> int:
+    if _OPTIONS.window > 0:
+        return _OPTIONS.window
+    return max(int(cfg.num_threads), int(num_pairs) // WINDOW_PAIRS_PER_SLOT, 1)
+
+
+def sgd_params(model: DeviceModel, cfg, epoch: int, mode: int, num_pairs: int = 0) -> N.SgdParams:
     return model.params(n_neg=cfg.num_negatives, lr=cfg.learning_rate, l2=cfg.l2_reg,
                         mu=cfg.loss.mu, theta=cfg.loss.theta, cosine=cfg.similarity == "cosine",
                         mode=mode, stream_base=epoch_stream(cfg.seed, epoch),
-                        window=_OPTIONS.window, fp64=_OPTIONS.fp64)
+                        window=default_window(cfg, num_pairs) if num_pairs else _OPTIONS.window,
+                        fp64=_OPTIONS.fp64)
 
 
 def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int | None = None,
@@ -161,7 +178,8 @@ def run_epoch_on_device(model: DeviceModel, train, cfg, epoch: int, *, mode: int
     model.counters.reset()
     if agg is not None:
         agg.reset_epoch()  # per-epoch accumulator state (trainer.py:398-400)
-    params = sgd_params(model, cfg, epoch, mode)
+    # (the throughput aggregator keeps its own step: window 0 = 4096 pairs)
+    params = sgd_params(model, cfg, epoch, mode, num_pairs=npairs if agg is None else 0)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()

@@ -1,0 +1,97 @@
+"""heatcf's own callers running on the GPU through install().
+
+The reference package (heatcf, /root/reference/pkg) is installed unmodified
+into baseline/_ref (git-ignored; it travels to the GPU box with the repo):
+
+    python -m pip install --no-index --no-build-isolation --no-deps \
+        --find-links /opt/wheelhouse --target baseline/_ref <copy of /root/reference/pkg>
+
+Here heatcf.trainer.train (trainer.py:480-533) runs twice on the same data:
+once as shipped (numba, CPU) and once after install() rebound its
+train_epoch / evaluate to this package (trainer.py:516 and :493 resolve them
+at call time).  With num_threads = 1 (the reference's deterministic mode ->
+the EXACT kernel) the tables and every epoch's loss are bit-identical and the
+evaluations agree to 1e-12; with num_threads = 8 (Hogwild -> the throughput
+kernel) the final recall agrees within the reference's thread-parity bound.
+heatcf.bench.run_bench needs matplotlib, which this image lacks, so only its
+sampler filtering is tested (on CPU, tests/test_install_heatcf.py).
+Skipped when baseline/_ref/heatcf is absent.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+@pytest.fixture(scope="module")
+def heatcf():
+    if not os.path.isdir(os.path.join(REF, "heatcf")):
+        pytest.skip("heatcf not installed into baseline/_ref")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.dont_write_bytecode = True
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    try:
+        import heatcf as h
+        import heatcf.trainer  # noqa: F401
+        import heatcf.evaluator  # noqa: F401
+        import heatcf.synth  # noqa: F401
+        import heatcf.embeddings  # noqa: F401
+    except Exception as exc:  # pragma: no cover
+        pytest.skip(f"heatcf not importable: {exc}")
+    import torch
+    assert torch.cuda.is_available()
+    return h
+
+
+def _run(h, threads, installed, tmp_path=None):
+    from paper_2304_07334_b200.install import install, uninstall
+    train_set, test_set = h.synth.make_clustered(400, 1200, 8, 24, seed=3)
+    cfg = h.TrainingConfig(emb_dim=32, num_negatives=16, learning_rate=0.05, epochs=4,
+                           num_threads=threads, seed=7)
+    S = h.init_matrix(train_set.num_users, 32, h.InitSpec(seed=1))
+    T = h.init_matrix(train_set.num_items, 32, h.InitSpec(seed=2))
+    if installed:
+        install(h)
+    try:
+        res = h.trainer.train(S, T, train_set, test_set, cfg, eval_interval=2, k=20,
+                              out_dir=str(tmp_path) if tmp_path else None)
+    finally:
+        if installed:
+            uninstall()
+    return S, T, res
+
+
+def test_heatcf_train_deterministic_is_bit_identical(heatcf, tmp_path):
+    Sr, Tr, rr = _run(heatcf, 1, installed=False)
+    Sg, Tg, rg = _run(heatcf, 1, installed=True, tmp_path=tmp_path)
+    assert heatcf.trainer.train_epoch.__module__.startswith("heatcf")  # uninstalled again
+    assert Sg.values.tobytes() == Sr.values.tobytes()
+    assert Tg.values.tobytes() == Tr.values.tobytes()
+    assert [r.mean_loss for r in rg.reports] == [r.mean_loss for r in rr.reports]
+    assert [r.num_pairs for r in rg.reports] == [r.num_pairs for r in rr.reports]
+    assert len(rg.evaluations) == len(rr.evaluations) == 3
+    for (eg, mg), (er, mr) in zip(rg.evaluations, rr.evaluations):
+        assert eg == er
+        assert abs(mg.recall_at_k - mr.recall_at_k) <= 1e-12
+        assert abs(mg.ndcg_at_k - mr.ndcg_at_k) <= 1e-12
+    assert rg.best_epoch == rr.best_epoch
+    # the checkpoints heatcf wrote through the installed path load in heatcf
+    s2, t2, _ = heatcf.embeddings.load_model(str(tmp_path / "final.ckpt"))
+    assert s2.values.tobytes() == Sg.values.tobytes() and t2.values.tobytes() == Tg.values.tobytes()
+
+
+def test_heatcf_train_hogwild_matches_reference_quality(heatcf):
+    _, _, rr = _run(heatcf, 8, installed=False)
+    _, _, rg = _run(heatcf, 8, installed=True)
+    assert np.isfinite([r.mean_loss for r in rg.reports]).all()
+    # the reference's own thread-parity bound (test_trainer.py:199-208)
+    assert abs(rg.final_metrics.recall_at_k - rr.final_metrics.recall_at_k) <= 0.01, (
+        rg.final_metrics.recall_at_k, rr.final_metrics.recall_at_k)

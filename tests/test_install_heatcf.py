@@ -56,3 +56,27 @@ def test_reference_objects_flow_through_validation(heatcf_mod):
         train_epoch(S, T, train, heatcf_mod.TrainingConfig(
             emb_dim=8, num_negatives=1,
             sampler=heatcf_mod.SamplerConfig(kind="tiling", tile_size=2, refresh_interval=2)))
+
+
+def test_installed_bench_skips_the_tiling_sampler():
+    """Both shipped configs bench `uniform,tiling`; the tiling sampler is not
+    on the B200 path, so the installed run_bench drops those variants up front
+    and says so in its warnings (rather than stopping at the first tiling row)."""
+    import dataclasses
+    from paper_2304_07334_b200.install import _bench_without_tiling
+    seen = []
+
+    @dataclasses.dataclass(frozen=True)
+    class Cfg:
+        bench_samplers: tuple = ("uniform", "tiling")
+
+    def fake_run_bench(train, cfg, log=None):
+        seen.append(cfg.bench_samplers)
+        return [{"variant": "uniform"}], ["w"]
+
+    logs = []
+    rows, warnings = _bench_without_tiling(fake_run_bench)(None, Cfg(), log=logs.append)
+    assert seen == [("uniform",)] and rows == [{"variant": "uniform"}]
+    assert "tiling" in warnings[0] and warnings[1:] == ["w"] and "tiling" in logs[0]
+    rows, warnings = _bench_without_tiling(fake_run_bench)(None, Cfg(("uniform",)))
+    assert seen[-1] == ("uniform",) and warnings == ["w"]
