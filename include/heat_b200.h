@@ -209,6 +209,38 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
 const char *heat_shard_last_error(heat_shard *h);
 int heat_shard_destroy(heat_shard *h);
 
+/* Loopback group: `world` ranks in ONE process on one device, for testing
+ * the runtime's multi-rank step logic where only one GPU exists (no NCCL,
+ * no CUDA IPC).  The collectives become stream-ordered copies into a shared
+ * count row plus event waits: a rank's count "collective" of step s completes
+ * once every rank's comm stream has finished its apply of step s-1 and seen
+ * its own step-s log — the ordering the NCCL all-gather gives between
+ * processes.  Peers' logs are read through plain device pointers by the same
+ * fused gather+apply kernels (or, with HEAT_SHARD_EXCHANGE=gather, copied
+ * into the gathered buffer).  Nothing spins: every cross-rank dependency is
+ * an event wait, so the ranks' kernels never wait on one another.
+ * heat_shard_epoch_loopback runs one epoch of every rank (same nsteps; each
+ * rank its own S/T replica, pairs, bounds and counters), interleaving their
+ * steps; stats is an array of `world`.  Handles from heat_shard_create_loopback
+ * are destroyed one by one with heat_shard_destroy. */
+typedef struct heat_shard_rank {
+    float *S;
+    int64_t s_rows;
+    float *T;
+    int64_t t_rows;
+    const int32_t *local_users;
+    const int32_t *local_items;
+    const int64_t *pair_index;
+    const int64_t *step_bounds; /* host, nsteps + 1 */
+    int64_t capacity;
+    heat_counters *counters;
+} heat_shard_rank;
+
+int heat_shard_create_loopback(int32_t world, int32_t device, heat_shard **out);
+int heat_shard_epoch_loopback(heat_shard **ranks_h, int32_t world, const heat_shard_rank *ranks,
+                              int64_t nsteps, const heat_sgd_params *params,
+                              heat_shard_stats *stats, void *stream);
+
 /* HOST function: one epoch's (user, positive) order, bit-identical to
  * numpy Generator(PCG64(seed)).permutation applied to the CSR pairs
  * (dataset.py:146-158).  offsets/items/out_* are host arrays; the PCG64 state

@@ -25,8 +25,8 @@ EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
            "heat_eval_users", "heat_apply_row_deltas", "heat_apply_row_deltas_fixed",
            "heat_epoch_pairs", "heat_aggregate_users", "heat_agg_scratch_bytes",
            "heat_exact_stats", "heat_nccl_unique_id", "heat_shard_create", "heat_shard_epoch",
-           "heat_shard_last_error", "heat_shard_destroy", "heat_probe_l2_read", "heat_last_error",
-           "heat_version")
+           "heat_shard_last_error", "heat_shard_destroy", "heat_shard_create_loopback",
+           "heat_shard_epoch_loopback", "heat_probe_l2_read", "heat_last_error", "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -82,6 +82,23 @@ class ShardStats(ctypes.Structure):
         ("max_entries", ctypes.c_int64),
     ]
 
+
+class ShardRank(ctypes.Structure):
+    """heat_shard_rank (include/heat_b200.h): one loopback rank's epoch inputs."""
+    _fields_ = [
+        ("S", ctypes.c_void_p),
+        ("s_rows", ctypes.c_int64),
+        ("T", ctypes.c_void_p),
+        ("t_rows", ctypes.c_int64),
+        ("local_users", ctypes.c_void_p),
+        ("local_items", ctypes.c_void_p),
+        ("pair_index", ctypes.c_void_p),
+        ("step_bounds", ctypes.c_void_p),
+        ("capacity", ctypes.c_int64),
+        ("counters", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -125,6 +142,10 @@ def lib():
     L.heat_shard_last_error.argtypes = [P]
     L.heat_shard_destroy.restype = ctypes.c_int
     L.heat_shard_destroy.argtypes = [P]
+    L.heat_shard_create_loopback.restype = ctypes.c_int
+    L.heat_shard_create_loopback.argtypes = [i32, i32, P]
+    L.heat_shard_epoch_loopback.restype = ctypes.c_int
+    L.heat_shard_epoch_loopback.argtypes = [P, i32, P, i64, ctypes.POINTER(SgdParams), P, P]
     L.heat_epoch_pairs.restype = ctypes.c_int
     L.heat_epoch_pairs.argtypes = [P, i64, P, i64, u64, u64, u64, u64, i32, ctypes.c_uint32, P, P]
     L.heat_aggregate_users.restype = ctypes.c_int

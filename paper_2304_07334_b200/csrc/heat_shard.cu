@@ -124,6 +124,12 @@ struct heat_shard {
     int64_t *hstep_counts = nullptr;  // pinned copy
     int64_t step_counts_n = 0;
     int64_t *scratch = nullptr;  // device: small collective staging (handles, agreement)
+    // loopback group (heat_shard_create_loopback): `world` ranks of one
+    // process on one device; the NCCL calls become stream-ordered copies and
+    // event waits, peers' logs are read through plain device pointers
+    bool loopback = false;
+    int64_t *shared_counts = nullptr;  // group-owned [nsteps * world] (rank 0 allocates)
+    cudaEvent_t arrive[heat::kSlots] = {};
     // captured step graphs: the epoch's inputs live in runtime-owned buffers
     // (stable addresses), the per-step pair ranges and the stream base in
     // device memory, so one instantiated graph replays every epoch of a shape
@@ -361,7 +367,7 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
         pid[h->rank * kSlots + k] = h->slot[k].ids;
         prow[h->rank * kSlots + k] = h->slot[k].rows;
     }
-    if (W > 1 && h->p2p) {
+    if (W > 1 && h->p2p && !h->loopback) {
         // 2 * kSlots IPC handles per rank, exchanged as int64 words
         static_assert(sizeof(cudaIpcMemHandle_t) % sizeof(int64_t) == 0, "handle size");
         constexpr int64_t hw = sizeof(cudaIpcMemHandle_t) / sizeof(int64_t);
@@ -555,6 +561,8 @@ int heat_shard_destroy(heat_shard *h) {
     }
     for (cudaEvent_t e : {h->ev_start, h->ev_comm, h->ev_cdone[0], h->ev_cdone[1]})
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->arrive)
+        if (e) cudaEventDestroy(e);
     cudaFree(h->acc);
     cudaFree(h->flags);
     cudaFree(h->step_counts);
@@ -573,143 +581,172 @@ int heat_shard_destroy(heat_shard *h) {
 
 const char *heat_shard_last_error(heat_shard *h) { return h ? h->err.c_str() : ""; }
 
-int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t t_rows,
-                     const int32_t *local_users, const int32_t *local_items,
-                     const int64_t *pair_index, const int64_t *step_bounds, int64_t nsteps,
-                     int64_t capacity, const heat_sgd_params *p, heat_counters *counters,
-                     heat_shard_stats *stats, void *stream) {
-    if (!h || !p || !step_bounds || nsteps < 0 || capacity < 1) return HEAT_ERR_INVALID;
-    if (p->mode != HEAT_MODE_DELTA) {
-        h->err = "heat_shard_epoch runs HEAT_MODE_DELTA steps";
-        return HEAT_ERR_INVALID;
-    }
-    cudaSetDevice(h->device);
-    cudaStream_t caller = (cudaStream_t)stream;
-    const int W = h->world;
-    const int64_t K = p->dim;
-    ShardErr er{h};
-    const NcclApi &n = nccl();
+}  // extern "C"
 
-    // every rank must run the same number of steps with the same log layout:
-    // agree (max capacity) and check, before any per-step collective
-    int64_t cap = capacity;
-    if (W > 1) {
-        const int64_t mine[3] = {capacity, nsteps, K};
-        std::vector<int64_t> all(3 * W);
-        if (!host_all_gather(h, er, mine, 3, all.data())) return er.rc;
-        for (int q = 0; q < W; ++q) {
-            if (all[3 * q + 1] != nsteps || all[3 * q + 2] != K) {
-                er.invalid("ranks disagree on the epoch's step count or dim (steps " +
-                           std::to_string(nsteps) + " vs " + std::to_string(all[3 * q + 1]) +
-                           " on rank " + std::to_string(q) + ")");
-                return er.rc;
+namespace heat {
+
+// One rank's epoch: inputs, the step sequence (compute / count / apply) and
+// the closing statistics.  heat_shard_epoch drives one of these per process
+// (NCCL between processes); heat_shard_epoch_loopback drives `world` of them
+// in one process, interleaving their steps so every stream dependency the
+// NCCL collectives provide is expressed as an event wait instead.
+struct EpochRun {
+    heat_shard *h = nullptr;
+    ShardErr er{nullptr};
+    float *S = nullptr, *T = nullptr;
+    int64_t s_rows = 0, t_rows = 0, nsteps = 0, cap = 0, K = 0, total = 0;
+    const int32_t *users = nullptr, *items = nullptr;
+    const int64_t *pidx = nullptr, *bounds = nullptr;
+    const heat_sgd_params *p = nullptr;
+    heat_counters *counters = nullptr;
+    cudaStream_t caller = nullptr;
+    bool direct = true, dr = false;
+    int W = 1, lag = 2, nslots = 3;
+    std::vector<int64_t> key;
+    EpochRun **group = nullptr;  // loopback: every rank's run
+
+    const int32_t *tr_users() const { return dr ? h->d_users : users; }
+    const int32_t *tr_items() const { return dr ? h->d_items : items; }
+    const int64_t *tr_pidx() const { return dr ? (pidx ? h->d_pidx : nullptr) : pidx; }
+
+    // agreement on the log layout, buffers, the epoch inputs for captured
+    // graphs; `agreed` is the cap every rank uses (host all-gather or loopback)
+    int setup(int64_t agreed) {
+        if (!ensure_slots(h, er, agreed, K)) return er.rc;
+        if (!ensure_epoch_buffers(h, er, t_rows, K, nsteps)) return er.rc;
+        cap = h->cap;
+        direct = h->p2p;
+        // the gather fallback reads a slot on the host after its step's count:
+        // compute(s) must not refill the slot apply(s - nslots) still reads,
+        // which needs lag >= 2 (lag 1 would let compute(s) run before apply(s-1)
+        // is even enqueued)
+        lag = direct ? h->lag : std::max(h->lag, 2);
+        nslots = lag + 1;
+        // captured step graphs need the device-range kernels and a host-free
+        // step loop (the gather fallback reads counts on the host between steps)
+        dr = direct && h->graphs && !h->loopback && device_step_supported(p, S, T);
+        total = nsteps > 0 ? bounds[nsteps] : 0;
+        if (dr) {  // the epoch's inputs into runtime-owned buffers
+            if (total > h->pairs_cap) {
+                cudaDeviceSynchronize();
+                cudaFree(h->d_users); cudaFree(h->d_items); cudaFree(h->d_pidx);
+                h->d_users = h->d_items = nullptr;
+                h->d_pidx = nullptr;
+                h->pairs_cap = 0;
+                h->gkey.clear();  // the graph holds the old addresses
+                const int64_t c = std::max<int64_t>(total, 1) * 5 / 4;
+                if (!er.cuda(cudaMalloc(&h->d_users, c * sizeof(int32_t)), "pairs") ||
+                    !er.cuda(cudaMalloc(&h->d_items, c * sizeof(int32_t)), "pairs") ||
+                    !er.cuda(cudaMalloc(&h->d_pidx, c * sizeof(int64_t)), "pairs"))
+                    return er.rc;
+                h->pairs_cap = c;
             }
-            cap = std::max(cap, all[3 * q]);
-        }
-    }
-    if (!ensure_slots(h, er, cap, K)) return er.rc;
-    if (!ensure_epoch_buffers(h, er, t_rows, K, nsteps)) return er.rc;
-    cap = h->cap;
-
-    // the gather fallback also runs at world 1 (local copies instead of the
-    // NCCL calls), so its host-side scheduling is exercised on one GPU
-    const bool direct = h->p2p;
-    // captured step graphs need the device-range kernels and a host-free step
-    // loop (the gather fallback reads counts on the host between steps)
-    const bool dr = direct && h->graphs && device_step_supported(p, S, T);
-    const int64_t total = nsteps > 0 ? step_bounds[nsteps] : 0;
-    if (dr) {  // the epoch's inputs into runtime-owned buffers
-        if (total > h->pairs_cap) {
-            cudaDeviceSynchronize();
-            cudaFree(h->d_users); cudaFree(h->d_items); cudaFree(h->d_pidx);
-            h->d_users = h->d_items = nullptr;
-            h->d_pidx = nullptr;
-            h->pairs_cap = 0;
-            h->gkey.clear();  // the graph holds the old addresses
-            const int64_t c = std::max<int64_t>(total, 1) * 5 / 4;
-            if (!er.cuda(cudaMalloc(&h->d_users, c * sizeof(int32_t)), "pairs") ||
-                !er.cuda(cudaMalloc(&h->d_items, c * sizeof(int32_t)), "pairs") ||
-                !er.cuda(cudaMalloc(&h->d_pidx, c * sizeof(int64_t)), "pairs"))
-                return er.rc;
-            h->pairs_cap = c;
-        }
-        if (nsteps + 1 > h->bounds_cap) {
-            cudaDeviceSynchronize();
-            cudaFree(h->d_bounds);
-            cudaFreeHost(h->h_bounds);
-            h->d_bounds = nullptr;
-            h->h_bounds = nullptr;
-            h->bounds_cap = 0;
-            h->gkey.clear();
-            if (!er.cuda(cudaMalloc(&h->d_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds") ||
-                !er.cuda(cudaMallocHost(&h->h_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds"))
-                return er.rc;
-            h->bounds_cap = nsteps + 1;
-        }
-        memcpy(h->h_bounds, step_bounds, (nsteps + 1) * sizeof(int64_t));
-        *h->h_s0 = p->stream_base;
-        if (total > 0) {
-            er.cuda(cudaMemcpyAsync(h->d_users, local_users, total * sizeof(int32_t),
-                                    cudaMemcpyDeviceToDevice, caller), "pairs in");
-            er.cuda(cudaMemcpyAsync(h->d_items, local_items, total * sizeof(int32_t),
-                                    cudaMemcpyDeviceToDevice, caller), "pairs in");
-            if (pair_index)
-                er.cuda(cudaMemcpyAsync(h->d_pidx, pair_index, total * sizeof(int64_t),
+            if (nsteps + 1 > h->bounds_cap) {
+                cudaDeviceSynchronize();
+                cudaFree(h->d_bounds);
+                cudaFreeHost(h->h_bounds);
+                h->d_bounds = nullptr;
+                h->h_bounds = nullptr;
+                h->bounds_cap = 0;
+                h->gkey.clear();
+                if (!er.cuda(cudaMalloc(&h->d_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds") ||
+                    !er.cuda(cudaMallocHost(&h->h_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds"))
+                    return er.rc;
+                h->bounds_cap = nsteps + 1;
+            }
+            memcpy(h->h_bounds, bounds, (nsteps + 1) * sizeof(int64_t));
+            *h->h_s0 = p->stream_base;
+            if (total > 0) {
+                er.cuda(cudaMemcpyAsync(h->d_users, users, total * sizeof(int32_t),
                                         cudaMemcpyDeviceToDevice, caller), "pairs in");
+                er.cuda(cudaMemcpyAsync(h->d_items, items, total * sizeof(int32_t),
+                                        cudaMemcpyDeviceToDevice, caller), "pairs in");
+                if (pidx)
+                    er.cuda(cudaMemcpyAsync(h->d_pidx, pidx, total * sizeof(int64_t),
+                                            cudaMemcpyDeviceToDevice, caller), "pairs in");
+            }
+            er.cuda(cudaMemcpyAsync(h->d_bounds, h->h_bounds, (nsteps + 1) * sizeof(int64_t),
+                                    cudaMemcpyHostToDevice, caller), "bounds in");
+            er.cuda(cudaMemcpyAsync(h->d_s0, h->h_s0, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                    caller), "s0 in");
         }
-        er.cuda(cudaMemcpyAsync(h->d_bounds, h->h_bounds, (nsteps + 1) * sizeof(int64_t),
-                                cudaMemcpyHostToDevice, caller), "bounds in");
-        er.cuda(cudaMemcpyAsync(h->d_s0, h->h_s0, sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                caller), "s0 in");
+        // log counters start at zero (afterwards each step's apply re-arms its slot)
+        for (Slot &sl : h->slot)
+            if (sl.cnt) er.cuda(cudaMemsetAsync(sl.cnt, 0, sizeof(int64_t), caller), "zero");
+        return er.rc;
     }
-    // log counters start at zero (afterwards each step's apply re-arms its slot)
-    for (Slot &sl : h->slot) er.cuda(cudaMemsetAsync(sl.cnt, 0, sizeof(int64_t), caller), "zero");
 
-    const int lag = h->lag, nslots = h->lag + 1;
-    const int32_t *tr_users = dr ? h->d_users : local_users;
-    const int32_t *tr_items = dr ? h->d_items : local_items;
-    const int64_t *tr_pidx = dr ? (pair_index ? h->d_pidx : nullptr) : pair_index;
-    auto compute = [&](int64_t s) {
+    int64_t *counts_row(int64_t s) const {
+        return (h->loopback ? h->shared_counts : h->step_counts) + s * W;
+    }
+
+    void compute(int64_t s) {
         Slot &sl = h->slot[s % nslots];
         cudaStream_t cs = h->cstream[s & 1];
-        if (s >= lag) er.cuda(cudaStreamWaitEvent(cs, h->slot[(s - lag) % nslots].ex_done, 0),
-                              "wait apply");
+        if (s >= lag)
+            er.cuda(cudaStreamWaitEvent(cs, h->slot[(s - lag) % nslots].ex_done, 0), "wait apply");
         int r = HEAT_OK;
         if (dr) {  // every step launches (empty ones exit at once): a fixed topology
-            r = train_range_device_step(S, s_rows, T, t_rows, tr_users, tr_items, p, counters,
-                                        sl.ids, sl.rows, sl.cnt, cap, tr_pidx, h->d_bounds + s,
+            r = train_range_device_step(S, s_rows, T, t_rows, tr_users(), tr_items(), p, counters,
+                                        sl.ids, sl.rows, sl.cnt, cap, tr_pidx(), h->d_bounds + s,
                                         h->d_s0, cs);
-        } else if (step_bounds[s + 1] > step_bounds[s]) {
-            r = heat_train_range(S, s_rows, T, t_rows, tr_users, tr_items, step_bounds[s],
-                                 step_bounds[s + 1], p, counters, sl.ids, sl.rows, sl.cnt, cap,
-                                 tr_pidx, nullptr, nullptr, cs);
+        } else if (bounds[s + 1] > bounds[s]) {
+            r = heat_train_range(S, s_rows, T, t_rows, tr_users(), tr_items(), bounds[s],
+                                 bounds[s + 1], p, counters, sl.ids, sl.rows, sl.cnt, cap,
+                                 tr_pidx(), nullptr, nullptr, cs);
         }
         if (r != HEAT_OK && er.rc == HEAT_OK) {
             h->err = std::string("train_range: ") + heat_last_error();
             er.rc = r;
         }
         er.cuda(cudaEventRecord(sl.log_ready, cs), "record log");
-    };
+    }
+
+    // the gather fallback's host copy of the step's counts
+    void counts_to_host(int64_t s) {
+        er.cuda(cudaMemcpyAsync(h->hstep_counts + s * W, counts_row(s), W * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, h->comm_stream), "count to host");
+        er.cuda(cudaEventRecord(h->slot[s % nslots].cnt_ready, h->comm_stream), "record counts");
+    }
+
     // counts of step s: the fence every rank passes before reading slot s
-    auto count = [&](int64_t s) {
+    // (NCCL all-gather between processes; at world 1 a local copy)
+    void count(int64_t s) {
         Slot &sl = h->slot[s % nslots];
         er.cuda(cudaStreamWaitEvent(h->comm_stream, sl.log_ready, 0), "wait log");
         int64_t *cnts = h->step_counts + s * W;
         if (W > 1)  // (world 1, direct: the apply records the log's own counter)
-            er.nccl(n.all_gather(sl.cnt, cnts, 1, ncclInt64, h->comm, h->comm_stream),
+            er.nccl(nccl().all_gather(sl.cnt, cnts, 1, ncclInt64, h->comm, h->comm_stream),
                     "all_gather counts");
         else if (!direct)
             er.cuda(cudaMemcpyAsync(cnts, sl.cnt, sizeof(int64_t), cudaMemcpyDeviceToDevice,
                                     h->comm_stream), "count copy");
-        if (!direct) {
-            er.cuda(cudaMemcpyAsync(h->hstep_counts + s * W, cnts, W * sizeof(int64_t),
-                                    cudaMemcpyDeviceToHost, h->comm_stream), "count to host");
-            er.cuda(cudaEventRecord(sl.cnt_ready, h->comm_stream), "record counts");
-        }
-    };
-    auto apply = [&](int64_t t) {
+        if (!direct) counts_to_host(s);
+    }
+
+    // loopback count, phase 1 (every rank before any phase 2): this rank's
+    // count into the group's row, after its step-s log and its apply(s-1)
+    // (stream order on the comm stream) — what this rank brings to the
+    // collective — then an arrival event
+    void count_arrive(int64_t s) {
+        Slot &sl = h->slot[s % nslots];
+        er.cuda(cudaStreamWaitEvent(h->comm_stream, sl.log_ready, 0), "wait log");
+        er.cuda(cudaMemcpyAsync(counts_row(s) + h->rank, sl.cnt, sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, h->comm_stream), "count copy");
+        er.cuda(cudaEventRecord(h->arrive[s % nslots], h->comm_stream), "record arrival");
+    }
+
+    // phase 2: the collective completes on this rank once every rank arrived
+    void count_complete(int64_t s) {
+        for (int q = 0; q < W; ++q)
+            er.cuda(cudaStreamWaitEvent(h->comm_stream, group[q]->h->arrive[s % nslots], 0),
+                    "wait arrivals");
+        if (!direct) counts_to_host(s);
+    }
+
+    void apply(int64_t t) {
         Slot &sl = h->slot[t % nslots];
-        int64_t *cnts = h->step_counts + t * W;
+        int64_t *cnts = counts_row(t);
         LogView v{};
         if (direct) {
             v.pids = sl.pids;
@@ -720,12 +757,24 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
             for (int q = 0; q < W; ++q) cmax = std::max(cmax, h->hstep_counts[t * W + q]);
             cmax = std::min(cmax, cap);
             if (cmax > 0 && er.rc == HEAT_OK && W > 1) {
-                er.nccl(n.group_start(), "group start");
-                er.nccl(n.all_gather(sl.ids, sl.g_ids, (size_t)cmax, ncclInt32, h->comm,
-                                     h->comm_stream), "all_gather ids");
-                er.nccl(n.all_gather(sl.rows, sl.g_rows, (size_t)(cmax * K), ncclFloat32, h->comm,
-                                     h->comm_stream), "all_gather rows");
-                er.nccl(n.group_end(), "group end");
+                if (h->loopback) {  // the all-gather as copies of every rank's log
+                    for (int q = 0; q < W; ++q) {
+                        const Slot &qs = group[q]->h->slot[t % nslots];
+                        er.cuda(cudaMemcpyAsync(sl.g_ids + q * cmax, qs.ids, cmax * sizeof(int32_t),
+                                                cudaMemcpyDeviceToDevice, h->comm_stream), "gather");
+                        er.cuda(cudaMemcpyAsync(sl.g_rows + q * cmax * K, qs.rows,
+                                                cmax * K * sizeof(float), cudaMemcpyDeviceToDevice,
+                                                h->comm_stream), "gather");
+                    }
+                } else {
+                    const NcclApi &n = nccl();
+                    er.nccl(n.group_start(), "group start");
+                    er.nccl(n.all_gather(sl.ids, sl.g_ids, (size_t)cmax, ncclInt32, h->comm,
+                                         h->comm_stream), "all_gather ids");
+                    er.nccl(n.all_gather(sl.rows, sl.g_rows, (size_t)(cmax * K), ncclFloat32, h->comm,
+                                         h->comm_stream), "all_gather rows");
+                    er.nccl(n.group_end(), "group end");
+                }
             }
             v.ids = W > 1 ? sl.g_ids : sl.ids;  // world 1: the log is the gathered copy
             v.rows = W > 1 ? sl.g_rows : sl.rows;
@@ -733,16 +782,29 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         }
         if (er.rc == HEAT_OK)
             er.cuda(launch_shard_apply(T, (int)K, v, (direct && W == 1) ? sl.cnt : cnts, cnts,
-                                       sl.cnt, W, cap,
-                                       h->acc, h->flags, h->comm_stream), "apply");
+                                       sl.cnt, W, cap, h->acc, h->flags, h->comm_stream), "apply");
         er.cuda(cudaEventRecord(sl.ex_done, h->comm_stream), "record apply");
-    };
-    // the whole step sequence on the internal streams, forked from and joined
-    // back to `origin` (the caller's stream, or the capturing stream)
-    auto enqueue_epoch = [&](cudaStream_t origin) {
+    }
+
+    // fork the internal streams from `origin` / join them back
+    void fork(cudaStream_t origin) {
         er.cuda(cudaEventRecord(h->ev_start, origin), "record start");
         for (cudaStream_t st : {h->cstream[0], h->cstream[1], h->comm_stream})
             if (st != origin) er.cuda(cudaStreamWaitEvent(st, h->ev_start, 0), "wait start");
+    }
+    void join(cudaStream_t origin) {
+        for (int i = 0; i < 2; ++i) {
+            if (h->cstream[i] == origin) continue;
+            er.cuda(cudaEventRecord(h->ev_cdone[i], h->cstream[i]), "record compute");
+            er.cuda(cudaStreamWaitEvent(origin, h->ev_cdone[i], 0), "join compute");
+        }
+        er.cuda(cudaEventRecord(h->ev_comm, h->comm_stream), "record comm");
+        er.cuda(cudaStreamWaitEvent(origin, h->ev_comm, 0), "join comm");
+    }
+
+    // the whole step sequence of one process's rank
+    void enqueue_epoch(cudaStream_t origin) {
+        fork(origin);
         for (int64_t s = 0; s < nsteps && er.rc == HEAT_OK; ++s) {
             compute(s);
             if (direct) {  // nothing waits on the host: the step's exchange right behind it
@@ -754,85 +816,252 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
             }
         }
         if (!direct && nsteps >= 1 && er.rc == HEAT_OK) apply(nsteps - 1);
-        for (int i = 0; i < 2; ++i) {
-            if (h->cstream[i] == origin) continue;
-            er.cuda(cudaEventRecord(h->ev_cdone[i], h->cstream[i]), "record compute");
-            er.cuda(cudaStreamWaitEvent(origin, h->ev_cdone[i], 0), "join compute");
-        }
-        er.cuda(cudaEventRecord(h->ev_comm, h->comm_stream), "record comm");
-        er.cuda(cudaStreamWaitEvent(origin, h->ev_comm, 0), "join comm");
-    };
+        join(origin);
+    }
 
     // graph key: everything a captured epoch bakes in (not the stream base,
     // the pair order or the step ranges, which live in device memory)
-    std::vector<int64_t> key;
-    if (dr) {
+    void make_key() {
+        key.clear();
+        if (!dr) return;
         heat_sgd_params q = *p;
         q.stream_base = 0;
         key.resize(sizeof(q) / sizeof(int64_t) + 1);
         memcpy(key.data(), &q, sizeof(q));
         for (int64_t v : {(int64_t)(uintptr_t)S, s_rows, (int64_t)(uintptr_t)T, t_rows,
                           (int64_t)(uintptr_t)counters, nsteps, cap, (int64_t)lag,
-                          (int64_t)(pair_index != nullptr), (int64_t)W})
+                          (int64_t)(pidx != nullptr), (int64_t)W})
             key.push_back(v);
     }
-    if (dr && h->gexec && key == h->gkey) {
-        er.cuda(cudaGraphLaunch(h->gexec, caller), "replay epoch");
-    } else {
+
+    void run_single() {
+        make_key();
+        if (dr && h->gexec && key == h->gkey) {
+            er.cuda(cudaGraphLaunch(h->gexec, caller), "replay epoch");
+            return;
+        }
         enqueue_epoch(caller);
-        if (dr && er.rc == HEAT_OK) {
-            // record the same sequence once more, unexecuted, for later epochs
-            // (this epoch also warmed every launch-configuration cache)
-            if (h->gexec) cudaGraphExecDestroy(h->gexec);
-            h->gexec = nullptr;
-            h->gkey.clear();
-            cudaGraph_t g = nullptr;
-            if (cudaStreamBeginCapture(h->cstream[0], cudaStreamCaptureModeRelaxed) ==
-                cudaSuccess) {
-                enqueue_epoch(h->cstream[0]);
-                const cudaError_t ce = cudaStreamEndCapture(h->cstream[0], &g);
-                if (ce == cudaSuccess && er.rc == HEAT_OK &&
-                    cudaGraphInstantiate(&h->gexec, g, 0) == cudaSuccess) {
-                    h->gkey = key;
-                } else {  // the epoch itself ran: stay on direct launches, no error
-                    h->gexec = nullptr;
-                    h->graphs = false;
-                    er.rc = HEAT_OK;
-                    h->err.clear();
-                }
-                if (g) cudaGraphDestroy(g);
+        if (!dr || er.rc != HEAT_OK) return;
+        // record the same sequence once more, unexecuted, for later epochs
+        // (this epoch also warmed every launch-configuration cache)
+        if (h->gexec) cudaGraphExecDestroy(h->gexec);
+        h->gexec = nullptr;
+        h->gkey.clear();
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(h->cstream[0], cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+            enqueue_epoch(h->cstream[0]);
+            const cudaError_t ce = cudaStreamEndCapture(h->cstream[0], &g);
+            if (ce == cudaSuccess && er.rc == HEAT_OK &&
+                cudaGraphInstantiate(&h->gexec, g, 0) == cudaSuccess) {
+                h->gkey = key;
+            } else {  // the epoch itself ran: stay on direct launches, no error
+                h->gexec = nullptr;
+                h->graphs = false;
+                er.rc = HEAT_OK;
+                h->err.clear();
             }
-            cudaGetLastError();
+            if (g) cudaGraphDestroy(g);
         }
+        cudaGetLastError();
     }
 
-    // the epoch's counts come back once for the statistics and the overflow check
-    if (nsteps > 0)
-        er.cuda(cudaMemcpyAsync(h->hstep_counts, h->step_counts, nsteps * W * sizeof(int64_t),
-                                cudaMemcpyDeviceToHost, caller), "counts to host");
-    er.cuda(cudaStreamSynchronize(caller), "epoch");
-    if (er.rc != HEAT_OK) return er.rc;
-
-    heat_shard_stats st{};
-    for (int64_t s = 0; s < nsteps; ++s) {
-        int64_t cmax = 0;
-        for (int q = 0; q < W; ++q) {
-            const int64_t c = h->hstep_counts[s * W + q];
-            cmax = std::max(cmax, c);
-            st.entries += std::min(c, cap);
+    // the epoch's counts come back once for the statistics; a log that
+    // overflowed is reported (the capacity is the exact worst case, so this
+    // is a defensive check, not a mode of operation)
+    int finish(heat_shard_stats *stats) {
+        if (nsteps > 0)
+            er.cuda(cudaMemcpyAsync(h->hstep_counts, counts_row(0), nsteps * W * sizeof(int64_t),
+                                    cudaMemcpyDeviceToHost, caller), "counts to host");
+        er.cuda(cudaStreamSynchronize(caller), "epoch");
+        if (er.rc != HEAT_OK) return er.rc;
+        heat_shard_stats st{};
+        for (int64_t s = 0; s < nsteps; ++s) {
+            int64_t cmax = 0;
+            for (int q = 0; q < W; ++q) {
+                const int64_t c = h->hstep_counts[s * W + q];
+                cmax = std::max(cmax, c);
+                st.entries += std::min(c, cap);
+            }
+            if (cmax > cap) {
+                er.invalid("delta log overflow (" + std::to_string(cmax) + " > " +
+                           std::to_string(cap) + " entries on some rank in step " +
+                           std::to_string(s) + ")");
+            }
+            st.max_entries = std::max(st.max_entries, cmax);
+            st.steps += 1;
         }
-        if (cmax > cap) {
-            er.invalid("delta log overflow (" + std::to_string(cmax) + " > " +
-                       std::to_string(cap) + " entries on some rank in step " +
-                       std::to_string(s) + "); raise the capacity");
-        }
-        st.max_entries = std::max(st.max_entries, cmax);
-        st.steps += 1;
+        // bytes that crossed between GPUs: every rank reads every other rank's log
+        st.exchanged_bytes = (W > 1 ? (W - 1) : 0) * st.entries * (4 * K + 4);
+        if (stats) *stats = st;
+        return er.rc;
     }
-    // bytes that crossed between GPUs: every rank reads every other rank's log
-    st.exchanged_bytes = (W > 1 ? (W - 1) : 0) * st.entries * (4 * K + 4);
-    if (stats) *stats = st;
-    return er.rc;
+};
+
+static int epoch_args_ok(heat_shard *h, const heat_sgd_params *p, const int64_t *step_bounds,
+                         int64_t nsteps, int64_t capacity) {
+    if (!h || !p || !step_bounds || nsteps < 0 || capacity < 1) return HEAT_ERR_INVALID;
+    if (p->mode != HEAT_MODE_DELTA) {
+        h->err = "heat_shard_epoch runs HEAT_MODE_DELTA steps";
+        return HEAT_ERR_INVALID;
+    }
+    return HEAT_OK;
+}
+
+}  // namespace heat
+
+extern "C" {
+
+int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t t_rows,
+                     const int32_t *local_users, const int32_t *local_items,
+                     const int64_t *pair_index, const int64_t *step_bounds, int64_t nsteps,
+                     int64_t capacity, const heat_sgd_params *p, heat_counters *counters,
+                     heat_shard_stats *stats, void *stream) {
+    if (const int rc = epoch_args_ok(h, p, step_bounds, nsteps, capacity)) return rc;
+    if (h->loopback) {
+        h->err = "a loopback rank runs through heat_shard_epoch_loopback";
+        return HEAT_ERR_INVALID;
+    }
+    cudaSetDevice(h->device);
+    EpochRun run;
+    run.h = h;
+    run.er = ShardErr{h};
+    run.S = S; run.s_rows = s_rows; run.T = T; run.t_rows = t_rows;
+    run.users = local_users; run.items = local_items; run.pidx = pair_index;
+    run.bounds = step_bounds; run.nsteps = nsteps; run.p = p; run.counters = counters;
+    run.caller = (cudaStream_t)stream;
+    run.W = h->world;
+    run.K = p->dim;
+    // every rank must run the same number of steps with the same log layout:
+    // agree (max capacity) and check, before any per-step collective
+    int64_t cap = capacity;
+    if (run.W > 1) {
+        const int64_t mine[3] = {capacity, nsteps, run.K};
+        std::vector<int64_t> all(3 * run.W);
+        if (!host_all_gather(h, run.er, mine, 3, all.data())) return run.er.rc;
+        for (int q = 0; q < run.W; ++q) {
+            if (all[3 * q + 1] != nsteps || all[3 * q + 2] != run.K) {
+                run.er.invalid("ranks disagree on the epoch's step count or dim (steps " +
+                               std::to_string(nsteps) + " vs " + std::to_string(all[3 * q + 1]) +
+                               " on rank " + std::to_string(q) + ")");
+                return run.er.rc;
+            }
+            cap = std::max(cap, all[3 * q]);
+        }
+    }
+    if (run.setup(cap) != HEAT_OK) return run.er.rc;
+    run.run_single();
+    return run.finish(stats);
+}
+
+int heat_shard_create_loopback(int32_t world, int32_t device, heat_shard **out) {
+    if (!out || world < 1 || world > kMaxWorld) return HEAT_ERR_INVALID;
+    for (int r = 0; r < world; ++r) {
+        heat_shard *h = nullptr;
+        int rc = heat_shard_create(1, 0, nullptr, device, &h);
+        if (rc == HEAT_OK) {
+            h->world = world;
+            h->rank = r;
+            h->loopback = true;
+            h->graphs = false;
+            for (int k = 0; k < kSlots && rc == HEAT_OK; ++k)
+                if (cudaEventCreateWithFlags(&h->arrive[k], cudaEventDisableTiming) != cudaSuccess)
+                    rc = HEAT_ERR_CUDA;
+        }
+        if (rc != HEAT_OK) {
+            if (h) heat_shard_destroy(h);
+            for (int q = 0; q < r; ++q) heat_shard_destroy(out[q]);
+            return rc;
+        }
+        out[r] = h;
+    }
+    return HEAT_OK;
+}
+
+int heat_shard_epoch_loopback(heat_shard **hs, int32_t world, const heat_shard_rank *ranks,
+                              int64_t nsteps, const heat_sgd_params *p, heat_shard_stats *stats,
+                              void *stream) {
+    if (!hs || !ranks || world < 1 || world > kMaxWorld) return HEAT_ERR_INVALID;
+    for (int r = 0; r < world; ++r) {
+        if (!hs[r] || !hs[r]->loopback || hs[r]->world != world || hs[r]->rank != r)
+            return HEAT_ERR_INVALID;
+        if (const int rc = epoch_args_ok(hs[r], p, ranks[r].step_bounds, nsteps,
+                                         ranks[r].capacity))
+            return rc;
+    }
+    cudaSetDevice(hs[0]->device);
+    std::vector<EpochRun> runs(world);
+    std::vector<EpochRun *> group(world);
+    int64_t cap = 1;
+    for (int r = 0; r < world; ++r) cap = std::max(cap, ranks[r].capacity);
+    for (int r = 0; r < world; ++r) {
+        EpochRun &run = runs[r];
+        group[r] = &run;
+        const heat_shard_rank &a = ranks[r];
+        run.h = hs[r];
+        run.er = ShardErr{hs[r]};
+        run.S = a.S; run.s_rows = a.s_rows; run.T = a.T; run.t_rows = a.t_rows;
+        run.users = a.local_users; run.items = a.local_items; run.pidx = a.pair_index;
+        run.bounds = a.step_bounds; run.nsteps = nsteps; run.p = p; run.counters = a.counters;
+        run.caller = (cudaStream_t)stream;
+        run.W = world;
+        run.K = p->dim;
+        run.group = group.data();
+    }
+    // the group's count rows, owned by rank 0
+    heat_shard *h0 = hs[0];
+    if (!ensure_epoch_buffers(h0, runs[0].er, ranks[0].t_rows, p->dim, nsteps)) return runs[0].er.rc;
+    for (int r = 0; r < world; ++r) hs[r]->shared_counts = h0->step_counts;
+    for (int r = 0; r < world; ++r)
+        if (runs[r].setup(cap) != HEAT_OK) return runs[r].er.rc;
+    // peers' logs through plain device pointers (one address space)
+    for (int k = 0; k < kSlots; ++k) {
+        std::vector<const void *> ids(world), rows(world);
+        for (int q = 0; q < world; ++q) {
+            ids[q] = hs[q]->slot[k].ids;
+            rows[q] = hs[q]->slot[k].rows;
+        }
+        for (int r = 0; r < world; ++r) {
+            if (!runs[r].er.cuda(cudaMemcpy((void *)hs[r]->slot[k].pids, ids.data(),
+                                            world * sizeof(void *), cudaMemcpyHostToDevice),
+                                 "peer table") ||
+                !runs[r].er.cuda(cudaMemcpy((void *)hs[r]->slot[k].prows, rows.data(),
+                                            world * sizeof(void *), cudaMemcpyHostToDevice),
+                                 "peer table"))
+                return runs[r].er.rc;
+        }
+    }
+    auto ok = [&] {
+        for (auto &r : runs)
+            if (r.er.rc != HEAT_OK) return false;
+        return true;
+    };
+    for (auto &r : runs) r.fork(r.caller);
+    const bool direct = runs[0].direct;
+    auto count_all = [&](int64_t s) {
+        for (auto &r : runs) r.count_arrive(s);
+        for (auto &r : runs) r.count_complete(s);
+    };
+    for (int64_t s = 0; s < nsteps && ok(); ++s) {
+        for (auto &r : runs) r.compute(s);
+        if (direct) {
+            count_all(s);
+            for (auto &r : runs) r.apply(s);
+        } else {
+            if (s >= 1)
+                for (auto &r : runs) r.apply(s - 1);
+            count_all(s);
+        }
+    }
+    if (!direct && nsteps >= 1 && ok())
+        for (auto &r : runs) r.apply(nsteps - 1);
+    for (auto &r : runs) r.join(r.caller);
+    int rc = HEAT_OK;
+    for (int r = 0; r < world; ++r) {
+        const int e = runs[r].finish(stats ? stats + r : nullptr);
+        if (rc == HEAT_OK) rc = e;
+    }
+    for (int r = 0; r < world; ++r) hs[r]->shared_counts = nullptr;
+    return rc;
 }
 
 }  // extern "C"

@@ -56,11 +56,38 @@ def shard_epoch(ep_users: np.ndarray, world: int, rank: int, step_pairs: int):
     return mine, bounds
 
 
-def delta_capacity(local_pairs_max: int, n_neg: int, l2: float, margin: int = 16) -> int:
-    """Entries a step can log: the positive plus active negatives per pair
-    (every negative when l2 != 0, which makes negative writes dense)."""
-    per_pair = (n_neg + 1) if l2 != 0.0 else 1 + min(n_neg, margin)
-    return max(1, local_pairs_max * per_pair)
+def delta_capacity(local_pairs_max: int, n_neg: int, l2: float = 0.0) -> int:
+    """Entries a step can log, exactly at worst: a pair writes its positive
+    and at most every one of its N negatives (all of them when theta <= 0 or
+    the tables collapse, or when l2 != 0 makes negative writes dense), so
+    N + 1 per pair.  The log can therefore never overflow: no entry is ever
+    dropped and no replica diverges.  Memory is the price (c4, B = 2048 per
+    rank: 2.1 M entries x 516 B = 1.06 GB per log slot); `check_log_memory`
+    refuses an epoch that would not fit before anything is mutated."""
+    return max(1, int(local_pairs_max) * (int(n_neg) + 1))
+
+
+def log_bytes(capacity: int, dim: int, slots: int, world: int, gather: bool) -> int:
+    """Device bytes of a rank's delta logs: `slots` rotating logs of
+    `capacity` (id, row) entries, plus the gathered copies of every rank's log
+    in the gather exchange."""
+    per = capacity * (4 * dim + 4)
+    return slots * per * (1 + (world if gather else 0))
+
+
+def check_log_memory(capacity: int, dim: int, slots: int, world: int, gather: bool,
+                     device) -> None:
+    """ValueError (before the epoch mutates anything) when the logs would not
+    fit in 90 % of the device's free memory; a smaller exchange period
+    (pairs between exchanges) shrinks them proportionally."""
+    if torch.device(device).type != "cuda":
+        return
+    need = log_bytes(capacity, dim, slots, world, gather)
+    free, _ = torch.cuda.mem_get_info(device)
+    if need > 0.9 * free:
+        raise ValueError(f"delta logs need {need / 2**30:.1f} GiB ({slots} slots x {capacity} "
+                         f"entries x {4 * dim + 4} B{' x (1 + world) gathered' if gather else ''})"
+                         f" but {free / 2**30:.1f} GiB are free: lower the exchange period")
 
 
 def merge_order(all_ids: torch.Tensor, valid: torch.Tensor) -> torch.Tensor:
@@ -167,9 +194,15 @@ class ShardedTrainer:
         self.bounds = bounds
         local_max = int(np.diff(bounds).max()) if len(bounds) > 1 else 0
         self.cap = delta_capacity(local_max, params.n_neg, params.l2)
+        slots, gather = self._log_layout()
+        check_log_memory(self.cap, self.model.dim, slots, self.world, gather, dev)
         self._buffers(self.cap)
         self.params = N.SgdParams.from_buffer_copy(params)
         self.params.mode = N.MODE_DELTA
+
+    def _log_layout(self):
+        """(log slots, whether every rank's log is also gathered locally)."""
+        return 1, True
 
     @property
     def num_steps(self) -> int:
@@ -315,6 +348,9 @@ class PipelinedShardTrainer(ShardedTrainer):
     def _buffers(self, cap: int):  # logs live in the two pipeline slots
         return None
 
+    def _log_layout(self):
+        return 2, True
+
     def _alloc_slots(self, cap: int) -> None:
         K, dev, W = self.model.dim, self.model.device, self.world
         if self._slots is not None and self._slots[0]["ids"].numel() >= cap:
@@ -426,6 +462,11 @@ class NativeShardTrainer(ShardedTrainer):
     def _buffers(self, cap: int):  # logs live in the native runtime
         return None
 
+    def _log_layout(self):
+        import os
+        gather = self.world > 1 and os.environ.get("HEAT_SHARD_EXCHANGE") == "gather"
+        return 4, gather  # heat_shard.cu allocates kSlots = 4 logs
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             N.lib().heat_shard_destroy(self._h)
@@ -453,3 +494,63 @@ class NativeShardTrainer(ShardedTrainer):
             raise (ValueError if rc in (N.HEAT_ERR_INVALID, N.HEAT_ERR_UNSUPPORTED)
                    else N.HeatError)(msg)
         return self.stats
+
+
+class LoopbackShardGroup:
+    """`world` ranks of the native runtime (csrc/heat_shard.cu) in ONE process
+    on one GPU — the multi-rank step logic under test where only one device
+    exists.  Each rank has its own DeviceModel (S and a T replica); the NCCL
+    collectives of the per-process runtime become event-ordered copies
+    (heat_shard_epoch_loopback), so nothing spins on another rank's kernel."""
+
+    def __init__(self, models: list):
+        self.models = models
+        self.world = len(models)
+        dev = models[0].device
+        arr = (ctypes.c_void_p * self.world)()
+        N.check(N.lib().heat_shard_create_loopback(self.world, dev.index or 0, arr))
+        self._hs = arr
+        self.stats = (N.ShardStats * self.world)()
+
+    def close(self) -> None:
+        if getattr(self, "_hs", None) is not None:
+            for h in self._hs:
+                if h:
+                    N.lib().heat_shard_destroy(h)
+            self._hs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def train_epoch(self, ep_users: np.ndarray, ep_items: np.ndarray, params: N.SgdParams,
+                    step_pairs: int):
+        W = self.world
+        keep, ranks = [], (N.ShardRank * W)()
+        nsteps = None
+        for r, m in enumerate(self.models):
+            mine, bounds = shard_epoch(ep_users, W, r, step_pairs)
+            dev = m.device
+            lu = torch.from_numpy(np.ascontiguousarray(ep_users[mine], dtype=np.int32)).to(dev)
+            li = torch.from_numpy(np.ascontiguousarray(ep_items[mine], dtype=np.int32)).to(dev)
+            lp = torch.from_numpy(mine).to(dev)
+            b = np.ascontiguousarray(bounds, dtype=np.int64)
+            local_max = int(np.diff(b).max()) if len(b) > 1 else 0
+            cap = delta_capacity(local_max, params.n_neg, params.l2)
+            check_log_memory(cap, m.dim, 4, W, False, dev)
+            keep += [lu, li, lp, b]
+            ranks[r] = N.ShardRank(_p(m.S), m.S.shape[0], _p(m.T), m.T.shape[0], _p(lu), _p(li),
+                                   _p(lp), b.ctypes.data, cap, m.counters.ptr())
+            nsteps = len(b) - 1
+        q = N.SgdParams.from_buffer_copy(params)
+        q.mode = N.MODE_DELTA
+        rc = N.lib().heat_shard_epoch_loopback(self._hs, W, ranks, nsteps, ctypes.byref(q),
+                                               self.stats, _stream(self.models[0].device))
+        if rc != N.HEAT_OK:
+            msg = N.lib().heat_shard_last_error(self._hs[0]).decode(errors="replace")
+            raise (ValueError if rc in (N.HEAT_ERR_INVALID, N.HEAT_ERR_UNSUPPORTED)
+                   else N.HeatError)(msg)
+        del keep
+        return list(self.stats)

@@ -1,0 +1,141 @@
+"""The native multi-GPU runtime (csrc/heat_shard.cu) at world > 1, as
+`world` ranks of one process on one GPU (heat_shard_epoch_loopback; the
+B200 box of this build has one GPU, and ranks whose kernels wait on one
+another must not share a GPU — here nothing spins: every cross-rank
+dependency is an event wait).
+
+Exercised: the rank-local DELTA steps, the count "collective" as the
+cross-rank fence, the fused gather+apply reading the peers' logs through
+device pointers, the gather fallback, the log-slot rotation under each lag,
+the exact-capacity logs, and replica bit-identity.  Not exercised here: the
+CUDA IPC mapping and the NCCL calls themselves (they need two GPUs).
+
+Determinism argument used by the first test: with one pair in flight per
+rank (one warp per pair) and lag 1, step s of every rank reads T as left by the apply of step
+s-1, users are disjoint between ranks and the fixed-point apply is
+order-free, so the sharded epoch does not depend on the number of ranks —
+the world-G tables equal the world-1 tables bit for bit.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2304_07334_b200 import _native
+    _native.lib()
+    return torch
+
+
+def _setup(K, scale=0.02):
+    from paper_2304_07334_b200.embeddings import InitSpec, init_matrix
+    from workloads import make_dataset
+    train, _, _ = make_dataset("c2", scale=scale)
+    S = init_matrix(train.num_users, K, InitSpec(seed=0)).values
+    T = init_matrix(train.num_items, K, InitSpec(seed=0)).values
+    return train, S, T
+
+
+def _params(m, e, window, N=100, theta=0.3):
+    from paper_2304_07334_b200 import _native as NN
+    from paper_2304_07334_b200.rng import epoch_stream
+    return m.params(n_neg=N, lr=0.01, l2=0.0, mu=20.0, theta=theta, cosine=True,
+                    mode=NN.MODE_DELTA, stream_base=epoch_stream(0, e), window=window)
+
+
+@pytest.mark.parametrize("G,K", [(2, 64), (3, 128)])
+def test_world_g_equals_world_1_bit_exact(torch_cuda, monkeypatch, G, K):
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.parallel import LoopbackShardGroup, NativeShardTrainer
+    from paper_2304_07334_b200.rng import shuffle_seed
+    monkeypatch.setenv("HEAT_SHARD_LAG", "1")
+    monkeypatch.setenv("HEAT_SHARD_GRAPH", "0")
+    # one warp per pair (the register-streamed kernel): with one pair in
+    # flight its user-row update is a single add per element, so a run is
+    # deterministic (the pair-per-CTA kernel adds four warps' shares in
+    # arrival order)
+    monkeypatch.setenv("HEAT_HOGWILD_IMPL", "wide")
+    train, S, T = _setup(K)
+    ref = DeviceModel(S, T)
+    one = NativeShardTrainer(ref, 1, 0)
+    grp = LoopbackShardGroup([DeviceModel(S, T) for _ in range(G)])
+    for e in range(2):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        ref.counters.reset()
+        one.train_epoch(u, i, _params(ref, e, 1), 256)
+        for m in grp.models:
+            m.counters.reset()
+        st = grp.train_epoch(u, i, _params(grp.models[0], e, 1), 256)
+        assert sum(m.counters.read().pairs for m in grp.models) == len(u)
+        assert all(s.steps == st[0].steps for s in st) and st[0].entries >= len(u)
+        assert st[0].exchanged_bytes > 0
+        T0 = grp.models[0].T.cpu().numpy()
+        for m in grp.models[1:]:
+            assert m.T.cpu().numpy().tobytes() == T0.tobytes()  # replicas identical
+        assert T0.tobytes() == ref.T.cpu().numpy().tobytes()  # = the world-1 epoch
+        S_ref = ref.S.cpu().numpy()
+        for r, m in enumerate(grp.models):  # each rank owns users u % G
+            mine = np.arange(train.num_users) % G == r
+            assert m.S.cpu().numpy()[mine].tobytes() == S_ref[mine].tobytes()
+        loss = sum(m.counters.read().loss for m in grp.models)
+        assert abs(loss - ref.counters.read().loss) <= 1e-9 * abs(loss)
+    grp.close()
+    one.close()
+
+
+@pytest.mark.parametrize("lag,exchange", [("2", "p2p"), ("3", "p2p"), ("1", "gather"),
+                                          ("2", "gather")])
+def test_world_2_concurrent_steps_keep_replicas_identical(torch_cuda, monkeypatch, lag, exchange):
+    """Many pairs in flight, every staleness bound, both exchanges (the
+    gather fallback runs lag >= 2 whatever HEAT_SHARD_LAG says): every pair
+    trained once, replicas bit-identical, loss within 3 % of the world-1
+    runtime at the same settings."""
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.parallel import LoopbackShardGroup, NativeShardTrainer
+    from paper_2304_07334_b200.rng import shuffle_seed
+    monkeypatch.setenv("HEAT_SHARD_LAG", lag)
+    monkeypatch.setenv("HEAT_SHARD_EXCHANGE", exchange)
+    train, S, T = _setup(64, scale=0.05)
+    grp = LoopbackShardGroup([DeviceModel(S, T) for _ in range(2)])
+    ref = DeviceModel(S, T)
+    one = NativeShardTrainer(ref, 1, 0)
+    for e in range(3):
+        u, i = epoch_pairs(train, shuffle_seed(0, e))
+        for m in grp.models:
+            m.counters.reset()
+        grp.train_epoch(u, i, _params(grp.models[0], e, 256), 1024)
+        ref.counters.reset()
+        one.train_epoch(u, i, _params(ref, e, 256), 1024)
+        assert sum(m.counters.read().pairs for m in grp.models) == len(u)
+        assert (grp.models[0].T.cpu().numpy().tobytes() ==
+                grp.models[1].T.cpu().numpy().tobytes())
+    loss = sum(m.counters.read().loss for m in grp.models)
+    want = ref.counters.read().loss
+    assert np.isfinite(loss) and abs(loss - want) <= 0.03 * abs(want), (loss, want)
+    grp.close()
+    one.close()
+
+
+def test_theta_below_zero_fills_the_log_without_loss(torch_cuda):
+    """theta -1 makes every negative active: each pair logs N + 1 entries, the
+    exact worst case the capacity is sized for.  Nothing is dropped (the
+    applied entry count is exactly pairs x (N + 1)) and the replicas agree."""
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.parallel import LoopbackShardGroup
+    from paper_2304_07334_b200.rng import shuffle_seed
+    train, S, T = _setup(64)
+    grp = LoopbackShardGroup([DeviceModel(S, T) for _ in range(2)])
+    u, i = epoch_pairs(train, shuffle_seed(0, 0))
+    st = grp.train_epoch(u, i, _params(grp.models[0], 0, 128, N=40, theta=-1.0), 512)
+    assert st[0].entries == len(u) * 41
+    assert st[0].max_entries <= 512 * 41
+    assert (grp.models[0].T.cpu().numpy().tobytes() == grp.models[1].T.cpu().numpy().tobytes())
+    grp.close()

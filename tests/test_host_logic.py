@@ -218,7 +218,7 @@ def test_shard_epoch_partitions_pairs_by_owner():
                 assert np.all((seg >= s * B) & (seg < (s + 1) * B))
             seen[mine] += 1
         assert np.all(seen == 1)
-    assert delta_capacity(100, 50, 0.0) == 100 * 17
+    assert delta_capacity(100, 50, 0.0) == 100 * 51  # N + 1 per pair: never overflows
     assert delta_capacity(100, 50, 0.1) == 100 * 51
 
 
