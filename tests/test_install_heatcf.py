@@ -80,3 +80,31 @@ def test_installed_bench_skips_the_tiling_sampler():
     assert "tiling" in warnings[0] and warnings[1:] == ["w"] and "tiling" in logs[0]
     rows, warnings = _bench_without_tiling(fake_run_bench)(None, Cfg(("uniform",)))
     assert seen[-1] == ("uniform",) and warnings == ["w"]
+
+
+def test_kernels_spec_restatement_matches_reference(heatcf_mod):
+    """oracle/kernels_spec.py (the A13 checker used by tests/test_gpu_math_spec.py)
+    against heatcf.kernels itself: identical cosine reductions, loss and
+    gradients on random inputs, and the same degenerate handling."""
+    import numpy as np
+    import heatcf.kernels as RK
+    from oracle import kernels_spec as KS
+    rng = np.random.default_rng(7)
+    for dim in (2, 33, 128):
+        for _ in range(20):
+            u = rng.standard_normal(dim)
+            v = rng.standard_normal(dim)
+            c = RK.cosine_forward(u, v)
+            assert KS.cosine_forward(u, v) == (c.ss, c.tt, c.st, c.sim, c.degenerate)
+            assert np.array_equal(KS.cosine_grad_user(u, v), RK.cosine_grad_user(u, v, c))
+            assert np.array_equal(KS.cosine_grad_item(u, v), RK.cosine_grad_item(u, v, c))
+            mu, theta = float(rng.uniform(0, 3)), float(rng.uniform(-0.9, 0.9))
+            negs = rng.uniform(-1, 1, int(rng.integers(1, 9)))
+            p = RK.LossParams(mu=mu, theta=theta)
+            assert KS.ccl_loss(0.3, negs, mu, theta) == RK.ccl_loss(0.3, negs, p)
+            dp, dn = KS.ccl_loss_grad(0.3, negs, mu, theta)
+            rdp, rdn = RK.ccl_loss_grad(0.3, negs, p)
+            assert dp == rdp and np.array_equal(dn, rdn)
+    z = np.zeros(4)
+    assert KS.cosine_forward(z, np.ones(4))[3:] == (0.0, True)
+    assert not KS.cosine_grad_user(z, np.ones(4)).any()
