@@ -21,16 +21,18 @@
 //    8-lane butterfly (4 shuffles per group of 4 rows): lanes 0-3 of a row
 //    reduce tt while lanes 4-7 reduce st;
 //  * the similarity screen is fp32 (error < 1e-6 for K <= 128; the band is
-//    1e-5).  Rows inside the band — every candidate for sim > theta, the
-//    positive, and rows whose fp32 v.v underflows — get tt and st recomputed
-//    in binary64 from the same registers, so the margin decisions are the
-//    reference's binary64 decisions (trainer.py:184-221), not fp32 ones;
-//  * rows to write (positive, sim > theta, decay rows when l2 != 0) are copied
-//    from registers into a per-warp shared-memory snapshot with their binary64
-//    scalars; if it fills, it is parked in a per-worker global spill area.
-//    At the end of the pair every write is applied (red.global.add.v4, or
-//    logged in DELTA mode) — all reads of a pair precede its writes, the
-//    reference's snapshot semantics (trainer.py:118-146, 257-293);
+//    1e-5).  Rows that may be written — every candidate for sim > theta, the
+//    positive, rows whose fp32 v.v underflows, decay rows when l2 != 0 — are
+//    only RECORDED (id + flags) while streaming, so no row data is held past
+//    its FFMA2s;
+//  * after the pair's last round the recorded rows are re-read into a per-warp
+//    shared-memory snapshot (a per-worker global spill area past its
+//    capacity), and the band rows get tt and st in binary64 (warp-cooperative
+//    sums; the user's u.u is the reference's sequential binary64 sum), so the
+//    margin decisions are binary64 decisions (trainer.py:184-221), not fp32
+//    ones.  Then every write is applied (red.global.add.v4, or logged in DELTA
+//    mode) — all reads of a pair precede its writes, the reference's snapshot
+//    semantics (trainer.py:118-146, 257-293);
 //  * workers claim pairs from a per-launch atomic counter in epoch order, so
 //    SMs that host fewer workers take more pairs (no tail from the uneven
 //    window / 148 split).  Pairs in flight never exceed the worker count,
@@ -194,18 +196,30 @@ __global__ void __launch_bounds__(32, MINB)
         // in buffer rd & 1 and is loaded two rounds ahead
         float4 R[2][2][V];
         int32_t rid[2][2];
-        auto issue = [&](int b, int rd, int32_t z) {  // rd & 3 selects the rows of idv
+        // the row ids of round rd (rd & 3 selects them in idv) and the loads
+        // of a round into buffer b, split so the id shuffles run ahead of the
+        // arithmetic that frees the buffer
+        auto round_ids = [&](int rd, int32_t (&ids)[2]) {
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+                ids[x] = __shfl_sync(kFull, idv, ((rd & 3) << 3) + 4 * x + g);
+        };
+        auto load = [&](int b, const int32_t (&ids)[2], int32_t z) {
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
-                const int32_t id = __shfl_sync(kFull, idv, ((rd & 3) << 3) + 4 * x + g) + z;
-                rid[b][x] = id;
-                const float *src = a.T + (int64_t)id * K + 4 * c;
+                rid[b][x] = ids[x];
+                const float *src = a.T + (int64_t)ids[x] * K + 4 * c + z;
 #pragma unroll
                 for (int j = 0; j < V; ++j) R[b][x][j] = ld_row4(src + 32 * j, pol);
             }
         };
-        issue(0, 0, 0);
-        issue(1, 1, 0);
+        {
+            int32_t ids[2];
+            round_ids(0, ids);
+            load(0, ids, 0);
+            round_ids(1, ids);
+            load(1, ids, 0);
+        }
         nx = fetch(claim_next());
 
         // fp32 u.u for the screen; the exact binary64 ss (trainer.py:176-178)
@@ -243,6 +257,8 @@ __global__ void __launch_bounds__(32, MINB)
         // (id + flags); the resolve below re-reads them, so no row data is
         // held past its FFMA2s.
         auto round = [&](int b, int rd, bool refill) {
+            int32_t nids[2];
+            if (refill) round_ids(rd + 2, nids);
             float2 tl[2], th[2], sl[2], sh[2];
 #pragma unroll
             for (int x = 0; x < 2; ++x) tl[x] = th[x] = sl[x] = sh[x] = make_float2(0.f, 0.f);
@@ -263,7 +279,7 @@ __global__ void __launch_bounds__(32, MINB)
             }
             const int32_t id0 = rid[b][0], id1 = rid[b][1];
             // refill only after every FFMA2 of the round consumed the buffer
-            if (refill) issue(b, rd + 2, opaque_zero(th[1].x) + opaque_zero(sh[1].y));
+            if (refill) load(b, nids, opaque_zero(th[1].x) + opaque_zero(sh[1].y));
             float q[4];  // tt(x=0), st(x=0), tt(x=1), st(x=1)
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
@@ -316,62 +332,57 @@ __global__ void __launch_bounds__(32, MINB)
             round(1, rd + 3, more);
         }
 
-        // resolve, four recorded rows at a time (one per row slot g): re-read
-        // the row into its snapshot slot (shared memory, then the worker's
-        // spill rows), then lanes c = 0 / 1 sum tt = v.v / st = u.v in binary64
-        // in the reference's k order (trainer.py:176-197) and lane c = 0 takes
-        // the reference's cosine, degenerate test, hinge and weight
-        // (trainer.py:184-227).  A band row that is not written becomes a
-        // hole (id -1).  Every read of the pair precedes every write.
+        // resolve: re-read every recorded row into its snapshot slot (shared
+        // memory, then the worker's spill rows; four rows per pass, one per
+        // row slot g), then decide each band row from binary64 v.v and u.v
+        // (warp-cooperative, heat_row_update.cuh) with the reference's
+        // cosine, degenerate test, hinge and weight (trainer.py:184-227).  A
+        // band row that is not written becomes a hole (id -1).  Every read
+        // of the pair precedes every write.
         __syncwarp();
         const float irs = ss > 0.0 ? rsqrtf((float)ss) : 0.f;
         const double wneg = a.mu * (1.0 / (double)N);
         double hinge = 0.0, sim_p = 0.0;
-        if (!screen) {  // rows the screen never saw: the degenerate query
-            // counted per row below (every row is recorded)
-        }
 #pragma unroll 1
         for (int e0 = 0; e0 < cnt; e0 += 4) {
             const int e = e0 + g;
-            WriteEntry ent{};
             if (e < cnt) {
-                ent = ents[e];
                 float *dst = slot_row(e) + 4 * c;
-                const float *src = a.T + (int64_t)ent.id * K + 4 * c;
+                const float *src = a.T + (int64_t)ents[e].id * K + 4 * c;
 #pragma unroll
                 for (int j = 0; j < V; ++j)
                     *reinterpret_cast<float4 *>(dst + 32 * j) = ldcg4(src + 32 * j);
             }
-            __syncwarp();
-            double sum = 0.0;
-            if (e < cnt && (ent.pad & 1) && c < 2)
-                sum = seq_dot<K>(slot_row(e), c == 0 ? slot_row(e) : urow);
-            const double st = __shfl_down_sync(kFull, sum, 1);
-            if (e < cnt && c == 0) {
-                if (ent.pad & 1) {
-                    const double tt = sum;
-                    const bool degenerate = ss <= 0.0 || tt <= 0.0;
-                    const double sim = degenerate ? 0.0 : st / (sqrt(ss) * sqrt(tt));
-                    if (degenerate) ++degen;
-                    double w = 0.0;
-                    bool write;
-                    if (ent.pad & 2) {  // the positive
-                        sim_p = sim;
-                        w = -1.0;
-                        write = !degenerate || a.l2 != 0.f;
-                    } else {
-                        if (sim - a.theta > 0.0) {
-                            hinge += sim - a.theta;
-                            w = wneg;
-                            if (w != 0.0) ++active;
-                        }
-                        write = (w != 0.0 && !degenerate) || (w == 0.0 && a.l2 != 0.f);
-                    }
-                    ents[e] = WriteEntry{tt, st, w, write ? ent.id : -1, 0};
-                }  // decay-only rows keep w = 0
-            }
-            __syncwarp();
         }
+        __syncwarp();
+#pragma unroll 1
+        for (int e = 0; e < cnt; ++e) {
+            const WriteEntry ent = ents[e];
+            if (!(ent.pad & 1)) continue;  // decay-only rows keep w = 0
+            double unused, tt, st;
+            warp_dots64<K>(urow, slot_row(e), ContiguousCols{}, false, unused, tt, st);
+            if (lane == 0) {
+                const bool degenerate = ss <= 0.0 || tt <= 0.0;
+                const double sim = degenerate ? 0.0 : st / (sqrt(ss) * sqrt(tt));
+                if (degenerate) ++degen;
+                double w = 0.0;
+                bool write;
+                if (ent.pad & 2) {  // the positive
+                    sim_p = sim;
+                    w = -1.0;
+                    write = !degenerate || a.l2 != 0.f;
+                } else {
+                    if (sim - a.theta > 0.0) {
+                        hinge += sim - a.theta;
+                        w = wneg;
+                        if (w != 0.0) ++active;
+                    }
+                    write = (w != 0.0 && !degenerate) || (w == 0.0 && a.l2 != 0.f);
+                }
+                ents[e] = WriteEntry{tt, st, w, write ? ent.id : -1, 0};
+            }
+        }
+        __syncwarp();
 
         float4 ug[V];
 #pragma unroll
