@@ -13,9 +13,10 @@ its full 10 M x 2 M tables with a 2 % user sample of its interactions).
 JSON line keys beyond the base contract:
   roofline      algorithmic bytes of the fused kernel / its CUDA-event time.
                 bound "l2" when S+T fit the 126 MB L2 (c1-c4; ncu: >=98.6 %
-                L2 hit rate), against the L2 streaming-read ceiling measured
-                live in this run (heat_probe_l2_read); bound "hbm" otherwise
-                (c5), against MEASURED_PEAKS.json hbm_gbs
+                L2 hit rate), against the L2 ceiling measured live in this run
+                (best of a streaming read and random-row gathers of T in the
+                kernels' access pattern); bound "hbm" otherwise (c5), against
+                MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the C oracle port (restatement of trainer.py:103-466, pthreads
                 Hogwild, all host cores) on a bounded sample of the same pairs
   e2e           the same metric through the public drop-in API
@@ -247,11 +248,16 @@ def _ncu_traffic(config: str):
 L2_BYTES = 126 * 1024 * 1024
 
 
-def l2_probe(dev, table_bytes: int) -> dict:
-    """The L2 read ceiling measured live on this GPU: heat_probe_l2_read
-    streams a 48 MB buffer (and one the size of S+T when that fits L2) 50
-    times after a warming pass, timed with CUDA events on the launching
-    stream; the best of 3 runs per size."""
+def l2_probe(dev, table_bytes: int, T=None) -> dict:
+    """The L2 read ceiling measured live on this GPU, the best of:
+    * "48MB" / "tables": heat_probe_l2_read streaming a 48 MB buffer (and one
+      the size of S+T) 50 times after a warming pass;
+    * "gather": heat_probe_l2_gather, random rows of the item table T itself
+      in the training kernels' access pattern (8 lanes x 16 B per row) with no
+      arithmetic — random 512-byte gathers sustain MORE than the streaming
+      read on B200 (r02_gather_ceiling.txt), so it is the honest ceiling of a
+      gather-bound kernel;
+    each timed with CUDA events on the launching stream, best of 5 runs."""
     import ctypes
 
     import torch
@@ -267,7 +273,7 @@ def l2_probe(dev, table_bytes: int) -> dict:
     for name, nbytes in sizes.items():
         buf = torch.ones(nbytes // 4, dtype=torch.float32, device=dev)
         best = 0.0
-        for _ in range(3):
+        for _ in range(5):
             N.check(L.heat_probe_l2_read(buf.data_ptr(), buf.numel(), 1, sink.data_ptr(),
                                          ctypes.c_void_p(stream.cuda_stream)))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -279,6 +285,20 @@ def l2_probe(dev, table_bytes: int) -> dict:
             best = max(best, buf.numel() * 4.0 * 50 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
         out[name] = best
         del buf
+    if T is not None and T.shape[1] in (64, 128):
+        rows_read = ctypes.c_int64(0)
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            N.check(L.heat_probe_l2_gather(T.data_ptr(), T.shape[0], T.shape[1], 200,
+                                           sink.data_ptr(), ctypes.byref(rows_read),
+                                           ctypes.c_void_p(stream.cuda_stream)))
+            e1.record(stream)
+            e1.synchronize()
+            best = max(best, rows_read.value * T.shape[1] * 4.0 /
+                       (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        out["gather"] = best
     return out
 
 
@@ -489,11 +509,12 @@ def main():
         if table_bytes < L2_BYTES * 0.9:
             # S+T stay in L2 (ncu: >= 98.6 % sector hit rate on c2-c4): the L2
             # read ceiling, measured live, bounds the kernel; HBM frac kept beside
-            probe = l2_probe(dev, table_bytes)
+            probe = l2_probe(dev, table_bytes, model.T)
             l2_peak = max(probe.values())
             roofline = {"bound": "l2", "achieved": achieved, "peak": l2_peak,
-                        "peak_kind": "measured live: heat_probe_l2_read streaming read, best of "
-                                     "48 MB and S+T-sized buffers " +
+                        "peak_kind": "measured live (GB/s): best of heat_probe_l2_read streaming "
+                                     "reads (48 MB, S+T-sized) and heat_probe_l2_gather random-row "
+                                     "gathers of T " +
                                      json.dumps({k: round(v, 1) for k, v in probe.items()}),
                         "unit": "GB/s", "frac": achieved / l2_peak, **hbm}
         else:

@@ -260,6 +260,11 @@ int heat_exact_stats(unsigned long long *out, int reset);
  * L2 on `stream`; bench.py times it to measure the L2 read ceiling that
  * bounds the L2-resident configurations (not a reference interface). */
 int heat_probe_l2_read(const float *buf, int64_t n, int32_t passes, float *sink, void *stream);
+/* Diagnostic: random-row gathers over a rows x dim table (dim 64 or 128) in
+ * the training kernels' access pattern, no arithmetic; *rows_read = rows
+ * gathered.  bench.py times it for the L2 roofline of gather-bound kernels. */
+int heat_probe_l2_gather(const float *table, int64_t rows, int32_t dim, int32_t iters,
+                         float *sink, int64_t *rows_read, void *stream);
 
 const char *heat_last_error(void);
 int heat_version(void);

@@ -26,7 +26,7 @@ EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
            "heat_epoch_pairs", "heat_aggregate_users", "heat_agg_scratch_bytes",
            "heat_exact_stats", "heat_nccl_unique_id", "heat_shard_create", "heat_shard_epoch",
            "heat_shard_last_error", "heat_shard_destroy", "heat_shard_create_loopback",
-           "heat_shard_epoch_loopback", "heat_probe_l2_read", "heat_last_error", "heat_version")
+           "heat_shard_epoch_loopback", "heat_probe_l2_read", "heat_probe_l2_gather", "heat_last_error", "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -156,6 +156,8 @@ def lib():
     L.heat_exact_stats.argtypes = [P, ctypes.c_int]
     L.heat_probe_l2_read.restype = ctypes.c_int
     L.heat_probe_l2_read.argtypes = [P, i64, i32, P, P]
+    L.heat_probe_l2_gather.restype = ctypes.c_int
+    L.heat_probe_l2_gather.argtypes = [P, i64, i32, i32, P, P, P]
     L.heat_last_error.restype = ctypes.c_char_p
     L.heat_last_error.argtypes = []
     L.heat_version.restype = ctypes.c_int

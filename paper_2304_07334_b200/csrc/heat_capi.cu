@@ -241,9 +241,71 @@ __global__ void l2_probe_kernel(const float4 *__restrict__ a, long long n4, int 
     if (acc == 1234.5f) sink[0] = acc;  // keeps the loads live
 }
 
+// Random-row gather probe: the access pattern of the training kernels'
+// reads (8 lanes per row, V float4 per lane, two groups of 4 rows in flight
+// per warp, rows drawn by a hash), with no arithmetic beyond a sum.  It
+// measures what this GPU's L2 delivers to gathers of dim-float rows — the
+// ceiling a gather-bound kernel is compared against (scripts/gather_ceiling.cu
+// sweeps the configurations; 28 one-warp CTAs per SM is the best of them).
+template <int V>
+__global__ void __launch_bounds__(32) l2_gather_probe_kernel(const float4 *__restrict__ T,
+                                                             unsigned rows, int iters,
+                                                             float *sink) {
+    const int lane = threadIdx.x, g = lane >> 3, c = lane & 7;
+    unsigned h = blockIdx.x * 0x9E3779B9u + 0x7F4A7C15u;
+    auto row = [&](int it, int u) {
+        unsigned x = h + (unsigned)(it * 2 + u) * 4u + (unsigned)g;
+        x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+        return T + (size_t)(x % rows) * (V * 8) + c;
+    };
+    float acc = 0.f;
+    float4 b[2][V];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) b[u][j] = __ldcg(row(0, u) + 8 * j);
+    for (int it = 1; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc += (b[u][j].x + b[u][j].y) + (b[u][j].z + b[u][j].w);
+#pragma unroll
+            for (int j = 0; j < V; ++j) b[u][j] = __ldcg(row(it, u) + 8 * j);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc += b[u][j].x;
+    if (acc == 1234.5f) sink[0] = acc;
+}
+
 extern "C" {
 
 const char *heat_last_error(void) { return g_err.c_str(); }
+
+/* Random-row gather probe over a rows x dim table (dim 64 or 128): one-warp
+ * CTAs, 28 per SM, each `iters` x 8 rows; *rows_read gets the row count. */
+int heat_probe_l2_gather(const float *table, int64_t rows, int32_t dim, int32_t iters,
+                         float *sink, int64_t *rows_read, void *stream) {
+    if (!table || !sink || rows < 1 || rows > 0xFFFFFFFFll || iters < 2 ||
+        (dim != 64 && dim != 128))
+        return fail(HEAT_ERR_INVALID, "bad gather probe args");
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = sms * 28;
+    const float4 *t4 = reinterpret_cast<const float4 *>(table);
+    if (dim == 128)
+        l2_gather_probe_kernel<4><<<grid, 32, 0, (cudaStream_t)stream>>>(t4, (unsigned)rows, iters,
+                                                                         sink);
+    else
+        l2_gather_probe_kernel<2><<<grid, 32, 0, (cudaStream_t)stream>>>(t4, (unsigned)rows, iters,
+                                                                         sink);
+    if (rows_read) *rows_read = (int64_t)grid * iters * 8;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HEAT_OK : cuda_fail(e, "gather probe launch");
+}
 
 int heat_version(void) { return 1; }
 
