@@ -142,6 +142,9 @@ __global__ void __launch_bounds__(32, MINB)
     unsigned char *mine_area = a.spill + (size_t)blockIdx.x * a.spill_stride;
     float *sp_rows = reinterpret_cast<float *>(mine_area);
     WriteEntry *ents = reinterpret_cast<WriteEntry *>(mine_area + (size_t)a.spill_cap * K * 4);
+    // (id, flags) of each recorded row, written while streaming (one 8-byte
+    // store); the full entries are filled by the resolve
+    int2 *recs = reinterpret_cast<int2 *>(ents + a.spill_cap);
     auto slot_row = [&](int e) -> float * {
         return e < snap_cap ? snap + (size_t)e * K : sp_rows + (size_t)(e - snap_cap) * K;
     };
@@ -314,8 +317,7 @@ __global__ void __launch_bounds__(32, MINB)
             const unsigned mrec = __ballot_sync(kFull, rec & ((c & 3) == 0));
             if (rec & ((c & 3) == 0)) {
                 const int idx = cnt + __popc(mrec & ((1u << lane) - 1u));
-                ents[idx] = WriteEntry{0.0, 0.0, 0.0, b2 ? id1 : id0,
-                                       band ? (r == 0 ? 3 : 1) : 0};
+                recs[idx] = make_int2(b2 ? id1 : id0, band ? (r == 0 ? 3 : 1) : 0);
             }
             cnt += __popc(mrec);
         };
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(32, MINB)
             const int e = e0 + g;
             if (e < cnt) {
                 float *dst = slot_row(e) + 4 * c;
-                const float *src = a.T + (int64_t)ents[e].id * K + 4 * c;
+                const float *src = a.T + (int64_t)recs[e].x * K + 4 * c;
 #pragma unroll
                 for (int j = 0; j < V; ++j)
                     *reinterpret_cast<float4 *>(dst + 32 * j) = ldcg4(src + 32 * j);
@@ -357,8 +359,11 @@ __global__ void __launch_bounds__(32, MINB)
         __syncwarp();
 #pragma unroll 1
         for (int e = 0; e < cnt; ++e) {
-            const WriteEntry ent = ents[e];
-            if (!(ent.pad & 1)) continue;  // decay-only rows keep w = 0
+            const int2 rec = recs[e];
+            if (!(rec.y & 1)) {  // a decay-only row: w = 0
+                if (lane == 0) ents[e] = WriteEntry{0.0, 0.0, 0.0, rec.x, 0};
+                continue;
+            }
             double unused, tt, st;
             warp_dots64<K>(urow, slot_row(e), ContiguousCols{}, false, unused, tt, st);
             if (lane == 0) {
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(32, MINB)
                 if (degenerate) ++degen;
                 double w = 0.0;
                 bool write;
-                if (ent.pad & 2) {  // the positive
+                if (rec.y & 2) {  // the positive
                     sim_p = sim;
                     w = -1.0;
                     write = !degenerate || a.l2 != 0.f;
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(32, MINB)
                     }
                     write = (w != 0.0 && !degenerate) || (w == 0.0 && a.l2 != 0.f);
                 }
-                ents[e] = WriteEntry{tt, st, w, write ? ent.id : -1, 0};
+                ents[e] = WriteEntry{tt, st, w, write ? rec.x : -1, 0};
             }
         }
         __syncwarp();
@@ -495,7 +500,7 @@ static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *w
     HogwildArgs b = a;
     // spill area: a pair writes at most N+1 rows (all of them when l2 != 0)
     b.spill_cap = a.N + 1;
-    b.spill_stride = ((int64_t)b.spill_cap * (K * sizeof(float) + sizeof(WriteEntry)) + 255) &
+    b.spill_stride = ((int64_t)b.spill_cap * (K * sizeof(float) + sizeof(WriteEntry) + sizeof(int2)) + 255) &
                      ~(int64_t)255;
     b.spill = static_cast<unsigned char *>(stream_scratch(1, (size_t)(b.spill_stride * nw), st));
     unsigned long long *claim = stream_claim(st);

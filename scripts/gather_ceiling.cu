@@ -121,7 +121,8 @@ static void run(const char *name, F kern, int warps_per_sm, size_t smem, const f
            cudaGetLastError() == cudaSuccess ? "" : "  ERROR");
 }
 
-int main() {
+int main(int argc, char **argv) {
+    (void)argv;
     const int rows = 92000;  // c4's item table: 92k x 128 fp32 = 47 MB
     float4 *T;
     float *sink;
@@ -129,6 +130,17 @@ int main() {
     cudaMalloc(&sink, 4);
     cudaMemset(T, 0, (size_t)rows * 512);
     const int iters = 2000;
+    if (argc > 1) {  // lanes-per-row sweep at the wide kernel's 12 warps/SM
+        for (int w : {12, 16}) {
+            run("ldg LPR4 U1", gather_ldg<4, 1>, w, 0, T, rows, iters, 1 * 8, sink);
+            run("ldg LPR4 U2", gather_ldg<4, 2>, w, 0, T, rows, iters, 2 * 8, sink);
+            run("ldg LPR8 U2", gather_ldg<8, 2>, w, 0, T, rows, iters, 2 * 4, sink);
+            run("ldg LPR8 U4", gather_ldg<8, 4>, w, 0, T, rows, iters, 4 * 4, sink);
+            run("ldg LPR16 U4", gather_ldg<16, 4>, w, 0, T, rows, iters, 4 * 2, sink);
+            run("ldg LPR16 U8", gather_ldg<16, 8>, w, 0, T, rows, iters, 8 * 2, sink);
+        }
+        return 0;
+    }
     for (int w : {8, 12, 16, 24, 32}) {
         run("ldg LPR8 U2", gather_ldg<8, 2>, w, 0, T, rows, iters, 2 * 4, sink);
         run("ldg LPR8 U4", gather_ldg<8, 4>, w, 0, T, rows, iters, 4 * 4, sink);
