@@ -9,12 +9,17 @@
 //                   group, consumed by an FADD chain (registers only)
 //   sts  <D>     : LDGSTS (cp.async 16 B) of 16-row stages into a D-deep ring,
 //                   then LDS.128 reads of every byte (the staged kernel's path)
+//   tma4 <D>     : TMA tile::gather4 (4 rows per instruction, one lane issues,
+//                   mbarrier completion) of 16-row stages into a D-deep ring,
+//                   then LDS.128 reads of every byte (`./gather_ceiling tma`)
 //
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o gather_ceiling gather_ceiling.cu
 // Run:   ./gather_ceiling   (prints one line per variant: rows/s, GB/s, pairs/s at 1002 rows)
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -90,6 +95,57 @@ __global__ void __launch_bounds__(32) gather_sts(const float4 *__restrict__ T, i
     if (acc == 12345.f) sink[0] = acc;
 }
 
+// ---- TMA tile::gather4 into shared memory ----------------------------------
+__device__ __forceinline__ uint32_t s32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int D>
+__global__ void __launch_bounds__(32) gather_tma4(const __grid_constant__ CUtensorMap tmap,
+                                                  int rows, int iters, float *sink) {
+    extern __shared__ __align__(128) float4 ring4[];  // D stages x 16 rows x 32 float4
+    __shared__ __align__(8) uint64_t bar[D];
+    const int lane = threadIdx.x;
+    uint32_t seed = blockIdx.x * 7919u + 17u;
+    if (lane == 0)
+        for (int i = 0; i < D; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    float acc = 0.f;
+    auto issue = [&](int stage, int it) {
+        if (lane != 0) return;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(&bar[stage])),
+                     "r"(16 * 512) : "memory");
+        float4 *dst = ring4 + stage * 16 * 32;
+        for (int q = 0; q < 4; ++q) {
+            int r[4];
+            for (int k = 0; k < 4; ++k) r[k] = (int)(hash32(seed + (uint32_t)it * 16 + q * 4 + k) % (uint32_t)rows);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(s32(dst + q * 4 * 32)),
+                "l"(&tmap), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(s32(&bar[stage]))
+                : "memory");
+        }
+    };
+    for (int s = 0; s < D; ++s) issue(s, s);
+    for (int it = 0; it < iters; ++it) {
+        const int st = it % D;
+        const uint32_t parity = (uint32_t)((it / D) & 1);
+        asm volatile(
+            "{\n.reg .pred P1;\nW_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@!P1 bra W_%=;\n}\n" ::"r"(s32(&bar[st])), "r"(parity) : "memory");
+        const float4 *src = ring4 + st * 16 * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const float4 v = src[k * 32];
+            acc += v.x + v.y + v.z + v.w;
+        }
+        __syncwarp();
+        issue(st, it + D);
+    }
+    if (acc == 12345.f) sink[0] = acc;
+}
+
 template <typename F>
 static void run(const char *name, F kern, int warps_per_sm, size_t smem, const float4 *T,
                 int rows, int iters, int rows_per_iter, float *sink) {
@@ -122,7 +178,6 @@ static void run(const char *name, F kern, int warps_per_sm, size_t smem, const f
 }
 
 int main(int argc, char **argv) {
-    (void)argv;
     const int rows = 92000;  // c4's item table: 92k x 128 fp32 = 47 MB
     float4 *T;
     float *sink;
@@ -130,6 +185,52 @@ int main(int argc, char **argv) {
     cudaMalloc(&sink, 4);
     cudaMemset(T, 0, (size_t)rows * 512);
     const int iters = 2000;
+    if (argc > 1 && argv[1][0] == 't') {  // TMA gather4 into shared memory
+        PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q);
+        if (!encode) { printf("no cuTensorMapEncodeTiled\n"); return 1; }
+        CUtensorMap tmap;
+        cuuint64_t gdim[2] = {128, (cuuint64_t)rows};
+        cuuint64_t gstride[1] = {512};
+        cuuint32_t box[2] = {128, 1};
+        cuuint32_t estride[2] = {1, 1};
+        CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)T, gdim, gstride, box,
+                            estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
+        for (int w : {8, 12, 16}) {
+            auto k2 = [&](const float4 *, int rws, int its, float *sk, int grid, size_t smem) {
+                gather_tma4<2><<<grid, 32, smem>>>(tmap, rws, its, sk);
+            };
+            auto k4 = [&](const float4 *, int rws, int its, float *sk, int grid, size_t smem) {
+                gather_tma4<4><<<grid, 32, smem>>>(tmap, rws, its, sk);
+            };
+            for (int d : {2, 4}) {
+                const size_t smem = (size_t)d * 16 * 512;
+                auto kern = d == 2 ? (const void *)gather_tma4<2> : (const void *)gather_tma4<4>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                int occ = 0, sms = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                const int per_sm = std::min(occ, w), grid = per_sm * sms;
+                auto launch = [&](int its) { if (d == 2) k2(T, rows, its, sink, grid, smem); else k4(T, rows, its, sink, grid, smem); };
+                launch(4);
+                cudaEvent_t a, b;
+                cudaEventCreate(&a); cudaEventCreate(&b);
+                float best = 1e30f;
+                for (int rep = 0; rep < 3; ++rep) {
+                    cudaEventRecord(a); launch(iters); cudaEventRecord(b); cudaEventSynchronize(b);
+                    float ms; cudaEventElapsedTime(&ms, a, b); best = std::min(best, ms);
+                }
+                const double nrows = (double)grid * iters * 16, sec = best * 1e-3;
+                printf("tma4 D%d           warps/SM %2d (occ %2d)  %8.3f Grows/s  %8.1f GB/s  %6.2f M pairs/s (1002 rows)%s\n",
+                       d, per_sm, occ, nrows / sec / 1e9, nrows * 512 / sec / 1e9, nrows / 1002 / sec / 1e6,
+                       cudaGetLastError() == cudaSuccess ? "" : "  ERROR");
+            }
+        }
+        return 0;
+    }
     if (argc > 1) {  // lanes-per-row sweep at the wide kernel's 12 warps/SM
         for (int w : {12, 16}) {
             run("ldg LPR4 U1", gather_ldg<4, 1>, w, 0, T, rows, iters, 1 * 8, sink);
