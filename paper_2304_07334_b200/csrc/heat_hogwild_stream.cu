@@ -38,10 +38,12 @@
 //    window / 148 split).  Pairs in flight never exceed the worker count,
 //    which the launcher caps at the window.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "heat_common.cuh"
 #include "heat_internal.h"
@@ -115,10 +117,345 @@ __device__ __forceinline__ double seq_dot(const float *a, const float *b) {
     return acc;
 }
 
-template <int K, int MINB, bool DR>
+// ---- persistent sharded epoch (MODE 2) --------------------------------------
+// One launch trains a rank's whole epoch of DELTA steps (heat_shard.cu sets
+// it up).  Steps are gated on the device instead of by stream order:
+//  * a pair of step s (global step g = gbase + s) starts once this rank has
+//    applied every step up to g - lag and every peer has applied up to
+//    g - lag - 1, the last reader of log slot g % (lag + 1) it will write;
+//  * item-row deltas go straight into the step's accumulation buffer
+//    (g % lag: the steps that can be in flight at once never share one) as
+//    2^-40 fixed-point integer sums, and the touched row joins the buffer's
+//    row list; at world > 1 they are also logged for the peers, and the warp
+//    that finishes a step's last pair publishes the log's entry count into
+//    every rank's mailbox (one 8-byte store per rank, release at system
+//    scope: the log it describes is complete);
+//  * every rank applies each step in step order, the workers doing the work
+//    between pairs: the peers' logged entries are pulled over NVLink into the
+//    buffer in claimed chunks, then, once the rank's own pairs of the step
+//    are done, each touched row is converted once (T += float(sum)).
+//    Integer sums commute, so every replica of T stays bit-identical however
+//    producers and chunks interleave;
+//  * a finished apply is published as the rank's released-step count into
+//    every rank's `rel` words (monotone, never reset between epochs).
+// No warp waits on anything that is not already claimed by a running warp
+// (on this rank) or a running kernel (on a peer), so progress needs no
+// co-residency within a process; a loopback group (several ranks in one
+// launch) is launched cooperatively, since its ranks wait on one another.
+constexpr double kFix = 1099511627776.0;  // 2^40, as heat_shard.cu's apply kernels
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <class P>
+__device__ __forceinline__ P *shfl_ptr(P *p, int src) {
+    return reinterpret_cast<P *>(
+        __shfl_sync(kFull, (unsigned long long)reinterpret_cast<uintptr_t>(p), src));
+}
+__device__ __forceinline__ unsigned long long fix40(float v) {
+    return (unsigned long long)__double2ll_rn((double)v * kFix);
+}
+
+// per-warp bookkeeping of the persistent kernel (see below) and apply-work
+// diagnostics: [8] help calls, [9] calls with nothing to do, [10] clocks in
+// accumulate units, [11] clocks in convert units, [12] accumulate units
+__shared__ long long s_pw[16];
+
+// Watchdog of the device-side waits: a wait longer than ~20 s of clocks
+// records (site, rank, step, block) in g_watchdog and traps, so a protocol
+// bug surfaces as a launch error instead of a hung GPU.
+__device__ unsigned long long g_watchdog[4];
+__device__ __forceinline__ void watchdog(long long t0, int site, const PersistRank &R, long long s) {
+    if (clock64() - t0 > 40000000000ll) {
+        g_watchdog[0] = (unsigned long long)site;
+        g_watchdog[1] = (unsigned long long)R.rank;
+        g_watchdog[2] = (unsigned long long)s;
+        g_watchdog[3] = blockIdx.x;
+        __threadfence_system();
+        __trap();
+    }
+}
+
+// accumulation buffer and log slot of local step s (32-bit arithmetic on the
+// host-computed residues of gbase: a 64-bit % is a call, and a call anywhere
+// in the pair loop spills the streaming registers)
+__device__ __forceinline__ int persist_buf(const PersistRank &R, long long s) {
+    return (int)(((unsigned)R.gmod_lag + (unsigned)s) % (unsigned)R.lag);
+}
+__device__ __forceinline__ int persist_slot(const PersistRank &R, long long s) {
+    return (int)(((unsigned)R.gmod_slots + (unsigned)s) % (unsigned)R.nslots);
+}
+
+// may a pair of global step g start? (lane q < world checks rank q's word)
+__device__ __forceinline__ bool persist_gate_open(const PersistRank &R, long long g, int lane) {
+    bool ok = true;
+    if (lane < R.world) {
+        const long long need = lane == R.rank ? g - R.lag + 1 : g - R.lag;
+        if (need > 0) ok = (long long)ld_acquire_sys(R.rel + lane) >= need;
+    }
+    return __all_sync(kFull, ok);
+}
+
+// step s's log on this rank is complete: its count into every rank's mailbox
+__device__ __forceinline__ void persist_publish(const PersistRank &R, long long s, int lane) {
+    if (R.world == 1) return;  // nobody reads it
+    unsigned long long c = 0;
+    if (lane == 0) c = ld_acquire_gpu(R.cnt + s);
+    c = __shfl_sync(kFull, c, 0);
+    __threadfence_system();
+    __syncwarp();
+    if (lane < R.world) {
+        const unsigned long long w = ((unsigned long long)R.tag << 32) | (c < 0xffffffffull ? c : 0xffffffffull);
+        st_release_sys(R.mbox_tab[lane] + (((long long)(R.tag & 1) * R.mbox_steps + s) * R.world + R.rank), w);
+    }
+}
+
+// one logged row (this lane's columns 32j + 4c .. +3) into buffer b, when
+// `ok` (all lanes call it): the sums are indexed by row id, so the adds never
+// wait on anything; the row's first adder of the step (its flag word) appends
+// it to the step's row list, which the convert walks
+template <int K>
+__device__ __forceinline__ void persist_accumulate(const PersistRank &R, int b, long long step,
+                                                   int32_t id, int c, bool ok,
+                                                   const float4 (&d)[K / 32]) {
+    if (!ok) return;
+    if (c == 0 && atomicExch(R.map[b] + id, 1) == 0)
+        R.touched[b][atomicAdd(R.state + kRows * R.nsteps + step, 1ull)] = id;
+    unsigned long long *ac = reinterpret_cast<unsigned long long *>(R.acc[b] + (int64_t)id * K + 4 * c);
+#pragma unroll
+    for (int j = 0; j < K / 32; ++j) {
+        atomicAdd(ac + 32 * j, fix40(d[j].x));
+        atomicAdd(ac + 32 * j + 1, fix40(d[j].y));
+        atomicAdd(ac + 32 * j + 2, fix40(d[j].z));
+        atomicAdd(ac + 32 * j + 3, fix40(d[j].w));
+    }
+}
+
+// apply of step t finished on this rank (exactly one warp gets here per
+// step): statistics, then the released count
+__device__ __forceinline__ void persist_finish(const PersistRank &R, long long t, long long c,
+                                               int lane) {
+    if (lane == R.rank) c = (long long)ld_acquire_gpu(R.cnt + t);
+    if (lane < R.world) R.step_counts[t * R.world + lane] = c;
+    __threadfence_system();
+    __syncwarp();
+    if (lane < R.world) st_release_sys(R.rel_tab[lane] + R.rank, R.gbase + (unsigned long long)t + 1);
+}
+
+// claims up to C of a phase's units
+__device__ __forceinline__ long long persist_claim(const PersistRank &R, unsigned long long *ctr,
+                                                   long long C, long long total, int lane) {
+    long long i0 = 0;
+    if (lane == 0) i0 = (long long)atomicAdd(ctr, (unsigned long long)C);
+    return __shfl_sync(kFull, i0, 0);
+}
+
+// One unit of apply work for the lowest unapplied step, if any is available:
+// 1 = did work, 0 = nothing claimable now, 2 = every step of the epoch applied.
+// A unit is up to kApplyChunk entries or rows, 4 at a time per warp (8 lanes
+// each, the kernel's row layout) with every load of a chunk in flight at once.
+template <int K>
+__device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
+    constexpr int V = K / 32;
+    constexpr long long C = kApplyChunk;
+    const int g = lane >> 3, c = lane & 7;
+    const long long n = R.nsteps;
+    if (lane == 0) s_pw[8] += 1;
+    const long long t = (long long)ld_acquire_sys(R.rel + R.rank) - (long long)R.gbase;
+    if (t >= n) return 2;
+    const int b = persist_buf(R, t);
+    unsigned long long *st = R.state + t;
+    // 1. ready once this rank's pairs of step t are done and every peer's log
+    //    of step t is complete
+    if ((long long)ld_acquire_gpu(st + kDone * n) < R.bounds[t + 1] - R.bounds[t]) return 0;
+    long long cnt = 0;  // lane q < world, q != rank: rank q's logged entries of step t
+    bool ok = true;
+    if (lane < R.world && lane != R.rank) {
+        const unsigned long long v =
+            ld_acquire_sys(R.mbox + ((long long)(R.tag & 1) * R.mbox_steps + t) * R.world + lane);
+        ok = (unsigned)(v >> 32) == R.tag;
+        cnt = (long long)(v & 0xffffffffull);
+    }
+    if (!__all_sync(kFull, ok)) return 0;  // some peer's log of step t is not complete yet
+    // 2. the peers' logged entries of step t into the buffer (this rank's
+    //    own deltas were added by the pairs themselves)
+    if (R.world > 1) {
+        const long long cc = cnt < R.cap ? cnt : R.cap;
+        long long incl = cc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const long long E = __shfl_sync(kFull, incl, 31);
+        const long long pre = incl - cc;
+        if ((long long)ld_acquire_gpu(st + kAccDone * n) < E) {
+            const long long i0 = persist_claim(R, st + kAccClaim * n, C, E, lane);
+            if (i0 >= E) return 0;
+            const long long ca = clock64();
+            const int m = (int)(i0 + C < E ? C : E - i0);
+            const int slot = persist_slot(R, t);
+            // lane j < m: entry i0 + j of the union: rank q = the last rank
+            // whose prefix is <= it, then its id and row address
+            const long long x = i0 + lane;
+            int q = 0;
+            for (int r = 1; r < R.world; ++r)
+                if (__shfl_sync(kFull, pre, r) <= x) q = r;
+            const long long e = x - __shfl_sync(kFull, pre, q);
+            int32_t id = 0;
+            const float *row = nullptr;
+            if (lane < m) {
+                id = __ldcg(R.pids[slot][q] + e);
+                row = R.prows[slot][q] + e * K;
+            }
+            for (int p0 = 0; p0 < m; p0 += 8) {  // 2 x 4 entries in flight
+                float4 d[2][V];
+                int32_t ids[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = p0 + 4 * h + g;
+                    ids[h] = __shfl_sync(kFull, id, j & 31);
+                    const float *rp = shfl_ptr(row, j & 31);
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        d[h][v] = j < m ? __ldcg(reinterpret_cast<const float4 *>(rp + 32 * v + 4 * c))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    persist_accumulate<K>(R, b, t, ids[h], c, p0 + 4 * h + g < m, d[h]);
+            }
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) {
+                atomicAdd(st + kAccDone * n, (unsigned long long)m);
+                s_pw[10] += clock64() - ca;
+                s_pw[12] += 1;
+            }
+            return 1;
+        }
+    }
+    // 3. every touched row converted once
+    const long long rows = (long long)ld_acquire_gpu(st + kRows * n);
+    if ((long long)ld_acquire_gpu(st + kCvtDone * n) < rows) {
+        constexpr long long CR = 16;  // rows per claim: 2 x (two groups of 4, loads in flight)
+        const long long i0 = persist_claim(R, st + kCvtClaim * n, CR, rows, lane);
+        if (i0 >= rows) return 0;
+        const long long cv = clock64();
+        const int m = (int)(i0 + CR < rows ? CR : rows - i0);
+        // rows i0 .. i0 + m - 1 of the step's list
+        int32_t myid = 0;
+        if (lane < m) myid = __ldcg(R.touched[b] + i0 + lane);
+        for (int hb = 0; hb < m; hb += 8) {
+        longlong2 q01[2][V], q23[2][V];
+        float4 tv[2][V];
+        int32_t ids[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = hb + 4 * h + g;
+            ids[h] = __shfl_sync(kFull, myid, j & 31);
+            if (j < m) {
+                const long long *ac = R.acc[b] + (int64_t)ids[h] * K + 4 * c;
+                const float *tr = R.T + (int64_t)ids[h] * K + 4 * c;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    q01[h][v] = __ldcg(reinterpret_cast<const longlong2 *>(ac + 32 * v));
+                    q23[h][v] = __ldcg(reinterpret_cast<const longlong2 *>(ac + 32 * v + 2));
+                    tv[h][v] = __ldcg(reinterpret_cast<const float4 *>(tr + 32 * v));
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = hb + 4 * h + g;
+            if (j < m) {
+                long long *ac = R.acc[b] + (int64_t)ids[h] * K + 4 * c;
+                float *tr = R.T + (int64_t)ids[h] * K + 4 * c;
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    __stcg(reinterpret_cast<longlong2 *>(ac + 32 * v), make_longlong2(0, 0));
+                    __stcg(reinterpret_cast<longlong2 *>(ac + 32 * v + 2), make_longlong2(0, 0));
+                    float4 x = tv[h][v];
+                    x.x += (float)((double)q01[h][v].x * (1.0 / kFix));
+                    x.y += (float)((double)q01[h][v].y * (1.0 / kFix));
+                    x.z += (float)((double)q23[h][v].x * (1.0 / kFix));
+                    x.w += (float)((double)q23[h][v].y * (1.0 / kFix));
+                    __stcg(reinterpret_cast<float4 *>(tr + 32 * v), x);
+                }
+                if (c == 0) R.map[b][ids[h]] = 0;
+            }
+        }
+        }
+        __threadfence();
+        __syncwarp();
+        long long d = 0;
+        if (lane == 0) {
+            d = (long long)atomicAdd(st + kCvtDone * n, (unsigned long long)m) + m;
+            s_pw[11] += clock64() - cv;
+        }
+        if (__shfl_sync(kFull, d, 0) == rows) persist_finish(R, t, cnt, lane);
+        return 1;
+    }
+    if (rows == 0) {  // nothing touched: one warp finishes the step
+        int win = 0;
+        if (lane == 0) win = atomicCAS(st + kFin * n, 0ull, 1ull) == 0ull;
+        if (__shfl_sync(kFull, win, 0)) {
+            persist_finish(R, t, cnt, lane);
+            return 1;
+        }
+    }
+    return 0;  // the step's last chunks are in other warps' hands
+}
+
+
+// ---- the persistent kernel's per-warp bookkeeping ---------------------------
+// What MODE 2/3 adds to a pair is a few loads and atomics at its start and
+// end; the state it carries between them lives in shared memory, so the
+// pair's streaming loop compiles as in the single-GPU kernel (it needs every
+// register of the 12-warps-per-SM budget).  s_pw: [0] the highest global step
+// whose gate this warp saw open, [1] start clock, clocks in [2] gate waits,
+// [3] apply work after pairs (diagnostics), [5] apply units done, [6] the step
+// of the last claimed pair (claims only grow), [7] the current pair's step.
+
+__device__ __forceinline__ const PersistRank &persist_rank(const PersistRank *ctx, int nctx) {
+    return ctx[nctx > 1 ? (int)(blockIdx.x % (unsigned)nctx) : 0];
+}
+
+__device__ __forceinline__ void persist_init(const PersistRank *ctx, int nctx, int lane) {
+    const PersistRank &R = persist_rank(ctx, nctx);
+    if (lane == 0) {
+        s_pw[0] = -1;
+        s_pw[1] = clock64();
+        for (int i = 2; i < 16; ++i) s_pw[i] = 0;
+        s_pw[13] = -1;  // start clock of a gate wait (-1: not waiting)
+    }
+    __syncwarp();
+    // steps without local pairs have a complete (empty) log from the start
+    for (int64_t s = blockIdx.x / nctx; s < R.nsteps; s += R.nblocks)
+        if (R.bounds[s + 1] == R.bounds[s]) persist_publish(R, s, lane);
+}
+
+// MODE: 0 = host pair range, 1 = device range (captured step graphs),
+// 2 = persistent sharded epoch of one rank (tables and pairs in `a`, the
+// rank's exchange state in ctx[0]), 3 = persistent epoch of a loopback group
+// (ctx: the ranks; block b serves rank b % nctx)
+template <int K, int MINB, int MODE>
 __global__ void __launch_bounds__(32, MINB)
     hogwild_stream(HogwildArgs a, FastMod fm, int snap_cap, float band_lo,
-                   unsigned long long *claim) {
+                   unsigned long long *claim, const PersistRank *__restrict__ ctx, int nctx,
+                   int apply_warps, unsigned long long *prof) {
+    constexpr bool DR = MODE == 1;
+    constexpr bool PS = MODE >= 2;
     constexpr int V = K / 32;  // float4 per lane per row
     extern __shared__ __align__(16) unsigned char sm[];
     float *urow = reinterpret_cast<float *>(sm);  // K floats: the user row
@@ -133,6 +470,29 @@ __global__ void __launch_bounds__(32, MINB)
         k_start = a.range_dev[0];
         k_stop = a.range_dev[1];
         k_s0 = *a.s0_dev;
+    }
+    // the rank's tables, pairs and sink (PS: from its context)
+    float *S = a.S, *T = a.T;
+    const int32_t *users = a.users, *items = a.items;
+    const int64_t *pidx = a.pair_index;
+    heat_counters *ctr = a.ctr;
+    // the context pointer is laundered through an asm move at every use, so
+    // nothing derived from it (state words, buffer addresses) is hoisted out
+    // of the worker loop and kept live across the streaming loop
+    auto prank = [&]() -> const PersistRank & {
+        const PersistRank *p = ctx + (MODE == 3 ? (int)(blockIdx.x % (unsigned)nctx) : 0);
+        asm volatile("mov.b64 %0, %0;" : "+l"(p));
+        return *p;
+    };
+    if constexpr (PS) {
+        if constexpr (MODE == 3) {  // (MODE 2: the launcher put them in `a`)
+            const PersistRank &R = persist_rank(ctx, nctx);
+            S = R.S; T = R.T; users = R.users; items = R.items;
+            pidx = R.pidx; ctr = R.ctr; claim = R.claim;
+            k_start = 0;
+            k_stop = R.bounds[R.nsteps];
+        }
+        persist_init(ctx, nctx, lane);
     }
     const int64_t npairs = k_stop - k_start;
     const int N = a.N;
@@ -167,21 +527,102 @@ __global__ void __launch_bounds__(32, MINB)
         Next n{tt, 0, 0, 0};
         if (tt < npairs) {
             const int64_t pp = k_start + tt;
-            n.u = a.users[pp];
-            n.pos = a.items[pp];
-            n.pg = a.pair_index ? (uint64_t)a.pair_index[pp] : (uint64_t)pp;
+            n.u = users[pp];
+            n.pos = items[pp];
+            n.pg = pidx ? (uint64_t)pidx[pp] : (uint64_t)pp;
+            if constexpr (PS) {  // the claimed pair's step (claims only grow)
+                long long sc = s_pw[6];
+                while (prank().bounds[sc + 1] <= tt) ++sc;
+                __syncwarp();
+                if (lane == 0) s_pw[6] = sc;
+                __syncwarp();
+            }
         }
         return n;
     };
-    Next nx = fetch(claim_next());
-    while (nx.t < npairs) {
+    // PS: the rank's first `apply_warps` workers only apply (no pairs): they
+    // start a step's apply the moment it becomes claimable
+    const bool applier = PS && (int)(blockIdx.x / nctx) < apply_warps;
+    Next nx = applier ? Next{npairs, 0, 0, 0} : fetch(claim_next());
+
+    // PS: what the warp does next, so that every kind of apply work goes
+    // through ONE inlined persist_help (a call to a user function would put
+    // the whole kernel under the calling ABI and spill the streaming loop):
+    // 0 = start pair nx, 1 = apply work after a pair, 2 = nx's gate is
+    // closed, 3 = no pairs left
+    // (hs = s_pw[14] and the waiting warps' backoff ns = s_pw[15] live in
+    // shared memory: the streaming loop has no register to spare)
+    if (lane == 0) {
+        s_pw[14] = 0;
+        s_pw[15] = 64;
+    }
+    __syncwarp();
+    for (;;) {
+        if constexpr (PS) {
+            const PersistRank &R = prank();
+            int hs = (int)s_pw[14];
+            __syncwarp();
+            if (hs == 0) {
+                if (nx.t >= npairs) {
+                    hs = 3;
+                    if (lane == 0) s_pw[4] = clock64();
+                } else {
+                    const long long g = (long long)(R.gbase + (unsigned long long)s_pw[6]);
+                    if (g > s_pw[0]) {  // (a gate open for g is open for every earlier step)
+                        const bool open = persist_gate_open(R, g, lane);
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (open) {
+                                s_pw[0] = g;
+                                if (s_pw[13] >= 0) s_pw[2] += clock64() - s_pw[13];
+                                s_pw[13] = -1;
+                            } else if (s_pw[13] < 0) {
+                                s_pw[13] = clock64();
+                            }
+                        }
+                        if (!open) hs = 2;
+                        __syncwarp();
+                    }
+                }
+            }
+            if (hs != 0) {
+                const long long c0 = clock64();
+                const int r = persist_help<K>(R, lane);
+                if (hs == 1) {
+                    if (r != 1) hs = 0;
+                    if (lane == 0) s_pw[3] += clock64() - c0;
+                } else if (hs == 2) {
+                    const unsigned ns = (unsigned)s_pw[15];
+                    if (r != 1) __nanosleep(ns);
+                    __syncwarp();
+                    if (lane == 0) s_pw[15] = r != 1 ? (ns < 2048 ? 2 * ns : ns) : 64;
+                    hs = 0;  // look at the gate again
+                    if (s_pw[13] >= 0) watchdog(s_pw[13], 2, R, s_pw[6]);
+                } else {
+                    if (r == 2) break;
+                    if (r == 0) __nanosleep(500);
+                    watchdog(s_pw[4], 3, R, (long long)R.rel[R.rank] - (long long)R.gbase);
+                }
+                if (lane == 0) {
+                    if (r == 1) ++s_pw[5];
+                    s_pw[14] = hs;
+                }
+                __syncwarp();
+                continue;
+            }
+            if (lane == 0) s_pw[14] = hs;
+            if (lane == 0) s_pw[7] = s_pw[6];  // the pair starts: its step
+            __syncwarp();
+        } else {
+            if (nx.t >= npairs) break;
+        }
         const int32_t u = nx.u;
         const int32_t pos = nx.pos;
         const uint64_t pg = nx.pg;
 
         float4 uv[V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) uv[j] = ldcg4(a.S + (int64_t)u * K + 32 * j + 4 * c);
+        for (int j = 0; j < V; ++j) uv[j] = ldcg4(S + (int64_t)u * K + 32 * j + 4 * c);
 
         // negative ids, 32 rows per draw block: lane l of block b holds the id
         // of row 32b + l; row r >= 1 is draw pg*N + r - 1 of the stream
@@ -211,7 +652,7 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
                 rid[b][x] = ids[x];
-                const float *src = a.T + (int64_t)ids[x] * K + 4 * c + z;
+                const float *src = T + (int64_t)ids[x] * K + 4 * c + z;
 #pragma unroll
                 for (int j = 0; j < V; ++j) R[b][x][j] = ld_row4(src + 32 * j, pol);
             }
@@ -350,7 +791,7 @@ __global__ void __launch_bounds__(32, MINB)
             const int e = e0 + g;
             if (e < cnt) {
                 float *dst = slot_row(e) + 4 * c;
-                const float *src = a.T + (int64_t)recs[e].x * K + 4 * c;
+                const float *src = T + (int64_t)recs[e].x * K + 4 * c;
 #pragma unroll
                 for (int j = 0; j < V; ++j)
                     *reinterpret_cast<float4 *>(dst + 32 * j) = ldcg4(src + 32 * j);
@@ -397,7 +838,7 @@ __global__ void __launch_bounds__(32, MINB)
         }
         // the writes, four rows at a time (trainer.py:236-251 user gradient,
         // 259-290 item update, cached scalars; fp32 coefficients)
-        const bool dmode = a.delta_ids != nullptr;
+        const bool dmode = PS || a.delta_ids != nullptr;
 #pragma unroll 1
         for (int e0 = 0; e0 < cnt; e0 += 4) {
             const int e = e0 + g;
@@ -419,18 +860,34 @@ __global__ void __launch_bounds__(32, MINB)
             }
             if (!dmode) {
                 if (ok) {
-                    float *dst = a.T + (int64_t)ent.id * K + 4 * c;
+                    float *dst = T + (int64_t)ent.id * K + 4 * c;
 #pragma unroll
                     for (int j = 0; j < V; ++j)
                         red_add4(dst + 32 * j, d[j].x, d[j].y, d[j].z, d[j].w);
                 }
-            } else {
+            } else {  // logged (PS: into the step's log slot)
+                int32_t *lids = a.delta_ids;
+                float *lrows = a.delta_rows;
+                unsigned long long *lcnt = reinterpret_cast<unsigned long long *>(a.delta_count);
+                int64_t lcap = a.delta_capacity;
+                bool log = true;
+                if constexpr (PS) {  // own deltas into the step's buffer; logged for the peers
+                    const PersistRank &R = prank();
+                    const long long stp = s_pw[7];
+                    persist_accumulate<K>(R, persist_buf(R, stp), stp, ent.id, c, ok, d);
+                    const int slt = persist_slot(R, stp);
+                    lids = R.log_ids[slt];
+                    lrows = R.log_rows[slt];
+                    lcnt = R.cnt + stp;
+                    lcap = R.cap;
+                    log = R.world > 1;
+                }
                 long long sl = 0;
-                if (ok && c == 0) sl = (long long)atomicAdd((unsigned long long *)a.delta_count, 1ull);
+                if (ok && c == 0) sl = (long long)atomicAdd(lcnt, 1ull);
                 sl = __shfl_sync(kFull, sl, g * 8);
-                if (ok && sl < a.delta_capacity) {
-                    if (c == 0) a.delta_ids[sl] = ent.id;
-                    float *dst = a.delta_rows + sl * K + 4 * c;
+                if (log && ok && sl < lcap) {
+                    if (c == 0) lids[sl] = ent.id;
+                    float *dst = lrows + sl * K + 4 * c;
 #pragma unroll
                     for (int j = 0; j < V; ++j) *reinterpret_cast<float4 *>(dst + 32 * j) = d[j];
                 }
@@ -451,7 +908,7 @@ __global__ void __launch_bounds__(32, MINB)
         if (g == 0) {
 #pragma unroll
             for (int j = 0; j < V; ++j)
-                red_add4(a.S + (int64_t)u * K + 32 * j + 4 * c, -a.lr * (ug[j].x + a.l2 * uv[j].x),
+                red_add4(S + (int64_t)u * K + 32 * j + 4 * c, -a.lr * (ug[j].x + a.l2 * uv[j].x),
                          -a.lr * (ug[j].y + a.l2 * uv[j].y), -a.lr * (ug[j].z + a.l2 * uv[j].z),
                          -a.lr * (ug[j].w + a.l2 * uv[j].w));
         }
@@ -463,6 +920,36 @@ __global__ void __launch_bounds__(32, MINB)
         if (lane == 0) loss += (1.0 - sim_p) + wneg * hinge;
         ++npairs_mine;
         __syncwarp();
+        if constexpr (PS) {
+            // the pair's log entries are written: count it into its step; the
+            // step's last pair publishes the log; then apply work is helped
+            const PersistRank &R = prank();
+            __threadfence();
+            __syncwarp();
+            const long long step = s_pw[7];
+            int last = 0;
+            if (lane == 0)
+                last = atomicAdd(R.state + kDone * R.nsteps + step, 1ull) + 1 ==
+                       (unsigned long long)(R.bounds[step + 1] - R.bounds[step]);
+            if (__shfl_sync(kFull, last, 0)) persist_publish(R, step, lane);
+            if (lane == 0) s_pw[14] = 1;  // then apply work, while there is some
+            __syncwarp();
+        }
+    }
+    if constexpr (PS) {
+        if (prof && lane == 0) {
+            atomicAdd(prof + 0, (unsigned long long)(clock64() - s_pw[1]));
+            atomicAdd(prof + 1, (unsigned long long)s_pw[2]);
+            atomicAdd(prof + 2, (unsigned long long)s_pw[3]);
+            atomicAdd(prof + 3, (unsigned long long)(clock64() - s_pw[4]));
+            atomicAdd(prof + 4, (unsigned long long)s_pw[5]);
+            atomicAdd(prof + 5, (unsigned long long)npairs_mine);
+            atomicAdd(prof + 6, 1ull);
+            atomicAdd(prof + 7, (unsigned long long)s_pw[8]);
+            atomicAdd(prof + 8, (unsigned long long)s_pw[10]);
+            atomicAdd(prof + 9, (unsigned long long)s_pw[11]);
+            atomicAdd(prof + 10, (unsigned long long)s_pw[12]);
+        }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -470,13 +957,14 @@ __global__ void __launch_bounds__(32, MINB)
         active += __shfl_xor_sync(kFull, active, o);
     }
     if (lane == 0) {
-        atomicAdd(&a.ctr->loss, loss);
-        if (degen) atomicAdd((unsigned long long *)&a.ctr->degenerate, (unsigned long long)degen);
-        if (active) atomicAdd((unsigned long long *)&a.ctr->active, (unsigned long long)active);
-        atomicAdd((unsigned long long *)&a.ctr->pairs, (unsigned long long)npairs_mine);
+        atomicAdd(&ctr->loss, loss);
+        if (degen) atomicAdd((unsigned long long *)&ctr->degenerate, (unsigned long long)degen);
+        if (active) atomicAdd((unsigned long long *)&ctr->active, (unsigned long long)active);
+        atomicAdd((unsigned long long *)&ctr->pairs, (unsigned long long)npairs_mine);
         // re-arm the claim counter once every warp has made its last claim
         __threadfence();
-        if (atomicAdd(claim + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        const unsigned long long nb = PS ? (unsigned long long)persist_rank(ctx, nctx).nblocks : gridDim.x;
+        if (atomicAdd(claim + 1, 1ull) == nb - 1) {
             claim[0] = 0;
             claim[1] = 0;
             __threadfence();
@@ -488,7 +976,7 @@ template <int K, int MINB>
 static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
     const int snap_cap = K <= 64 ? 16 : 8;
     const size_t smem = K * sizeof(float) + (size_t)snap_cap * K * sizeof(float);
-    auto kern = a.range_dev ? hogwild_stream<K, MINB, true> : hogwild_stream<K, MINB, false>;
+    auto kern = a.range_dev ? hogwild_stream<K, MINB, 1> : hogwild_stream<K, MINB, 0>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
     if (e != cudaSuccess) return e;
@@ -506,8 +994,116 @@ static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *w
     unsigned long long *claim = stream_claim(st);
     if (!b.spill || !claim) return cudaErrorMemoryAllocation;
     kern<<<(unsigned)nw, 32, smem, st>>>(b, FastMod::make((uint64_t)a.num_items), snap_cap,
-                                         (float)a.theta - 1e-5f, claim);
+                                         (float)a.theta - 1e-5f, claim, nullptr, 0, 0, nullptr);
     return cudaGetLastError();
+}
+
+// HEAT_PERSIST_PROF=1: a device buffer of clock totals the persistent kernel
+// adds into (printed and cleared by persist_prof_report after an epoch)
+static unsigned long long *g_prof = nullptr;
+static unsigned long long *persist_prof(cudaStream_t st) {
+    static const bool on = getenv("HEAT_PERSIST_PROF") && atoi(getenv("HEAT_PERSIST_PROF")) != 0;
+    if (!on) return nullptr;
+    if (!g_prof && cudaMalloc(&g_prof, 16 * sizeof(unsigned long long)) == cudaSuccess)
+        cudaMemsetAsync(g_prof, 0, 16 * sizeof(unsigned long long), st);
+    return g_prof;
+}
+
+// the persistent sharded epoch: every resident one-warp CTA is a worker (the
+// steps, not a window, bound the staleness); nctx > 1 splits them over the
+// ranks of a loopback group and launches cooperatively
+template <int K, int MINB>
+static cudaError_t launch_persist_k(const HogwildArgs &a, const PersistRank *ctx_host,
+                                    PersistRank *ctx_dev, int nctx, cudaStream_t st) {
+    const int snap_cap = K <= 64 ? 16 : 8;
+    const size_t smem = K * sizeof(float) + (size_t)snap_cap * K * sizeof(float);
+    auto kern = nctx == 1 ? hogwild_stream<K, MINB, 2> : hogwild_stream<K, MINB, 3>;
+    cudaError_t e;
+    const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
+    if (e != cudaSuccess) return e;
+    // every rank gets an equal share of the resident workers, at most
+    // `window` (pairs in flight per rank) when one is set
+    int64_t per_rank = (int64_t)per_sm * sm_count() / nctx;
+    if (a.window > 0) per_rank = std::min<int64_t>(per_rank, a.window);
+    if (const char *w = getenv("HEAT_PERSIST_WORKERS"))  // A/B knob: fewer workers
+        if (atoi(w) > 0) per_rank = std::min<int64_t>(per_rank, atoi(w));
+    if (per_rank < 1) return cudaErrorInvalidConfiguration;
+    const int64_t nw = per_rank * nctx;
+    std::vector<PersistRank> cx(ctx_host, ctx_host + nctx);
+    for (int r = 0; r < nctx; ++r) cx[r].nblocks = (int)(nw / nctx + (r < nw % nctx ? 1 : 0));
+    e = cudaMemcpyAsync(ctx_dev, cx.data(), nctx * sizeof(PersistRank), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    HogwildArgs b = a;
+    if (nctx == 1) {  // the rank's tables and pairs as kernel parameters
+        b.S = ctx_host->S; b.T = ctx_host->T; b.users = ctx_host->users;
+        b.items = ctx_host->items; b.pair_index = ctx_host->pidx; b.ctr = ctx_host->ctr;
+        b.start = 0;
+    }
+    b.spill_cap = a.N + 1;
+    b.spill_stride = ((int64_t)b.spill_cap * (K * sizeof(float) + sizeof(WriteEntry) + sizeof(int2)) + 255) &
+                     ~(int64_t)255;
+    b.spill = static_cast<unsigned char *>(stream_scratch(1, (size_t)(b.spill_stride * nw), st));
+    if (!b.spill) return cudaErrorMemoryAllocation;
+    FastMod fm = FastMod::make((uint64_t)a.num_items);
+    int snap = snap_cap;
+    float band_lo = (float)a.theta - 1e-5f;
+    unsigned long long *claim = nctx == 1 ? ctx_host->claim : nullptr;
+    const PersistRank *cd = ctx_dev;
+    int nc = nctx;
+    int apply_warps = 0;  // per rank (A/B knob; the workers help between pairs anyway)
+    if (const char *w = getenv("HEAT_PERSIST_APPLY_WARPS"))
+        apply_warps = std::max(0, std::min(atoi(w), (int)per_rank - 1));
+    unsigned long long *prof = persist_prof(st);
+    if (nctx == 1) {
+        kern<<<(unsigned)nw, 32, smem, st>>>(b, fm, snap, band_lo, claim, cd, nc, apply_warps, prof);
+        return cudaGetLastError();
+    }
+    void *args[] = {&b, &fm, &snap, &band_lo, &claim, &cd, &nc, &apply_warps, &prof};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)nw), dim3(32), args, smem,
+                                       st);
+}
+
+void persist_watchdog_report() {
+    unsigned long long v[4] = {0, 0, 0, 0};
+    if (cudaMemcpyFromSymbol(v, g_watchdog, sizeof(v)) == cudaSuccess && v[0])
+        fprintf(stderr, "[persist] watchdog: site %llu rank %llu value %llu block %llu\n", v[0], v[1],
+                v[2], v[3]);
+}
+
+void persist_prof_report() {
+    if (!g_prof) return;
+    unsigned long long v[16];
+    cudaMemcpy(v, g_prof, sizeof(v), cudaMemcpyDeviceToHost);
+    cudaMemset(g_prof, 0, sizeof(v));
+    const double tot = v[0] ? (double)v[0] : 1.0;
+    fprintf(stderr,
+            "[persist] warps %llu pairs %llu: gate %.1f%% help %.1f%% drain %.1f%% of warp clocks;"
+            " apply units %llu (%.2f per pair); help calls %llu; clocks per accumulate unit %.0f"
+            " (%llu units), per convert unit %.0f\n",
+            v[6], v[5], 100.0 * v[1] / tot, 100.0 * v[2] / tot, 100.0 * v[3] / tot, v[4],
+            v[5] ? (double)v[4] / v[5] : 0.0, v[7], v[10] ? (double)v[8] / v[10] : 0.0, v[10],
+            (v[4] > v[10]) ? (double)v[9] / (v[4] - v[10]) : 0.0);
+}
+
+cudaError_t launch_shard_persist(const HogwildArgs &a, const PersistRank *ctx_host,
+                                 PersistRank *ctx_dev, int nctx, cudaStream_t st) {
+    if (!hogwild_stream_supported(a) || nctx < 1) return cudaErrorNotSupported;
+    // resident warps per SM the persistent build is compiled for (12, as the
+    // single-GPU kernel; 10 / 11 / 14 for A/B runs)
+    int warps = 12;
+    if (const char *e = getenv("HEAT_PERSIST_WARPS")) warps = atoi(e) > 0 ? atoi(e) : warps;
+    if (a.K == 128) {
+        switch (warps) {
+        case 10: return launch_persist_k<128, 10>(a, ctx_host, ctx_dev, nctx, st);
+        case 12: return launch_persist_k<128, 12>(a, ctx_host, ctx_dev, nctx, st);
+        default: return launch_persist_k<128, 11>(a, ctx_host, ctx_dev, nctx, st);
+        }
+    }
+    switch (warps) {
+    case 12: return launch_persist_k<64, 12>(a, ctx_host, ctx_dev, nctx, st);
+    case 14: return launch_persist_k<64, 14>(a, ctx_host, ctx_dev, nctx, st);
+    default: return launch_persist_k<64, 11>(a, ctx_host, ctx_dev, nctx, st);
+    }
 }
 
 bool hogwild_stream_supported(const HogwildArgs &a) {

@@ -57,6 +57,51 @@ struct HogwildArgs {
     int spill_cap = 0;         // rows per worker
 };
 
+// One rank of the persistent sharded epoch (heat_shard.cu drives it,
+// heat_hogwild_stream.cu runs it): the whole epoch in one launch, steps gated
+// on the device.  Everything a peer writes (mbox, rel) and reads (the log
+// slots) lives in the owner's HBM; peers reach it through the *_tab tables
+// (CUDA IPC mappings between processes, plain pointers in a loopback group).
+constexpr int kPersistSlots = 8;  // log slots / accumulation buffers (lag <= 7)
+constexpr int kPersistMaxWorld = 32;  // one lane per rank in the device checks
+// per-step local state words (PersistRank::state, [kStepWords][nsteps])
+// (kRows: rows the step touched = its accumulation buffer's slots in use)
+enum StepWord { kDone = 0, kAccClaim, kAccDone, kCvtClaim, kCvtDone, kFin, kRows, kStepWords };
+// entries (peer phase) / rows (convert phase) per claim of the apply work
+constexpr int kApplyChunk = 16;
+struct PersistRank {
+    float *S, *T;
+    const int32_t *users, *items;
+    const int64_t *pidx;     // global epoch position of local pair p (RNG key); NULL = p
+    const int64_t *bounds;   // [nsteps + 1] local pair bounds of each step
+    int64_t nsteps;
+    unsigned long long *claim;  // [2]: next local pair, finished warps
+    unsigned long long *state;  // [kStepWords * nsteps], zeroed before the launch
+    unsigned long long *cnt;    // [nsteps] entries this rank logged per step, zeroed
+    int32_t *log_ids[kPersistSlots];  // own log slots (capacity `cap` entries each)
+    float *log_rows[kPersistSlots];
+    const int32_t *const *pids[kPersistSlots];  // per slot: device table [world] of every rank's ids
+    const float *const *prows[kPersistSlots];
+    unsigned long long *const *mbox_tab;  // [world]: every rank's mailbox
+    unsigned long long *const *rel_tab;   // [world]: every rank's released words
+    const unsigned long long *mbox;       // own mailbox [2][mbox_steps][world]
+    const unsigned long long *rel;        // own released words [world]
+    // per accumulation buffer b = global step % lag (steps in flight never
+    // share one): 2^-40 fixed-point sums [t_rows * K], each row's touched flag
+    // [t_rows] (`map`), and the list of the step's touched rows [t_rows] (its
+    // length is the step's kRows word)
+    long long *acc[kPersistSlots];
+    int32_t *map[kPersistSlots];
+    int32_t *touched[kPersistSlots];
+    heat_counters *ctr;
+    int64_t *step_counts;  // [nsteps * world]: every rank's count per step (statistics)
+    int64_t cap, mbox_steps;
+    unsigned long long gbase;  // global step number of this epoch's step 0
+    unsigned tag;              // epoch tag (>= 1) of the mailbox words
+    int rank, world, lag, nslots, nblocks;  // nblocks: CTAs serving this rank
+    int gmod_lag, gmod_slots;               // gbase % lag, gbase % nslots
+};
+
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_resident(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_multi(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
@@ -64,6 +109,14 @@ cudaError_t launch_hogwild_staged(const HogwildArgs &a, cudaStream_t stream, int
                                   bool bulk);
 cudaError_t launch_hogwild_stream(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 bool hogwild_stream_supported(const HogwildArgs &a);
+// the persistent sharded epoch: `nctx` ranks in one launch (1 = this process's
+// rank; > 1 = a loopback group, launched cooperatively so every rank's CTAs
+// are co-resident).  a carries the shared SGD parameters; the per-rank
+// pointers come from ctx_dev (device copy of ctx_host).
+cudaError_t launch_shard_persist(const HogwildArgs &a, const PersistRank *ctx_host,
+                                 PersistRank *ctx_dev, int nctx, cudaStream_t st);
+void persist_prof_report();  // HEAT_PERSIST_PROF=1 diagnostics (stderr)
+void persist_watchdog_report();  // after a failed persistent epoch (stderr)
 
 size_t agg_hogwild_scratch_bytes(int K, int window);
 cudaError_t launch_agg_hogwild(const HogwildArgs &base, const heat_agg_params &agg,

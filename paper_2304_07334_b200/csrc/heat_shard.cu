@@ -49,7 +49,10 @@
 
 namespace heat {
 
-constexpr int kSlots = 4;  // log slots allocated; lag + 1 of them in use
+// log slots (lag + 1 in use; the stream-ordered steps run lag <= 3, the
+// persistent epoch lag <= 7)
+constexpr int kSlots = kPersistSlots;
+constexpr int kStreamMaxLag = 3;
 constexpr int kMaxWorld = 64;
 
 struct NcclApi {
@@ -110,7 +113,11 @@ struct LogView {
 struct heat_shard {
     int world = 1, rank = 0, device = 0;
     bool p2p = true;
-    int lag = 2;  // kernel(s) waits for the apply of step s - lag
+    // kernel(s) waits for the apply of step s - lag: HEAT_SHARD_LAG, else 2 for
+    // stream-ordered steps and 3 for the persistent epoch (measured: c4 at
+    // lag 2 loses 18 % of its warp time to gates, at lag 3 none)
+    int lag = 2, lag_persist = 3;
+    int nalloc = 0;  // log slots allocated (max(lag, lag_persist, 2) + 1)
     ncclComm_t comm = nullptr;
     cudaStream_t comm_stream = nullptr;
     cudaStream_t cstream[2] = {nullptr, nullptr};
@@ -140,6 +147,27 @@ struct heat_shard {
     uint64_t *d_s0 = nullptr, *h_s0 = nullptr;
     cudaGraphExec_t gexec = nullptr;
     std::vector<int64_t> gkey;
+    // persistent epoch (one launch per epoch, steps gated on the device):
+    // mailbox [2][mbox_steps][world] and released words [world] are written
+    // by every rank (IPC-mapped between processes); the step state and
+    // counts are local
+    bool persist = true, persist_force = false;
+    unsigned long long *mbox = nullptr, *rel = nullptr;
+    unsigned long long **mbox_tab = nullptr, **rel_tab = nullptr;  // device [world]
+    std::vector<void *> opened_mbox;
+    int64_t mbox_steps = 0;
+    unsigned long long gstep = 0;  // global steps run since the mailbox was (re)allocated
+    unsigned tag = 1;              // epoch tag of the mailbox words
+    unsigned long long *pstate = nullptr, *pcnt = nullptr, *pclaim = nullptr;
+    int64_t pstate_steps = 0;
+    heat::PersistRank *pctx = nullptr;  // device contexts (a loopback group's live in rank 0's)
+    int pctx_n = 0;
+    // accumulation buffers of the persistent epoch (one per step in flight)
+    long long *pacc[heat::kSlots] = {};
+    int32_t *pflags[heat::kSlots] = {}, *ptouched[heat::kSlots] = {};
+    unsigned long long *ptcount = nullptr;
+    int64_t pbuf_rows = 0, pbuf_dim = 0;
+    int pbufs = 0;
     std::string err;
 };
 
@@ -350,7 +378,9 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
     cudaDeviceSynchronize();  // buffers of a previous epoch may still be in use
     free_slots(h);
     const int W = h->world;
-    for (Slot &s : h->slot) {
+    h->nalloc = std::max(std::max(h->lag, h->lag_persist), 2) + 1;
+    for (int k = 0; k < h->nalloc; ++k) {
+        Slot &s = h->slot[k];
         if (!er.cuda(cudaMalloc(&s.ids, cap * sizeof(int32_t)), "log ids")) return false;
         if (!er.cuda(cudaMalloc(&s.rows, cap * dim * sizeof(float)), "log rows")) return false;
         if (!er.cuda(cudaMalloc(&s.cnt, sizeof(int64_t)), "log count")) return false;
@@ -363,7 +393,7 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
         }
     }
     std::vector<const void *> pid(W * kSlots), prow(W * kSlots);
-    for (int k = 0; k < kSlots; ++k) {
+    for (int k = 0; k < h->nalloc; ++k) {
         pid[h->rank * kSlots + k] = h->slot[k].ids;
         prow[h->rank * kSlots + k] = h->slot[k].rows;
     }
@@ -372,7 +402,7 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
         static_assert(sizeof(cudaIpcMemHandle_t) % sizeof(int64_t) == 0, "handle size");
         constexpr int64_t hw = sizeof(cudaIpcMemHandle_t) / sizeof(int64_t);
         std::vector<int64_t> mine(2 * kSlots * hw), all(W * 2 * kSlots * hw);
-        for (int k = 0; k < kSlots; ++k) {
+        for (int k = 0; k < h->nalloc; ++k) {
             cudaIpcMemHandle_t a, b;
             if (!er.cuda(cudaIpcGetMemHandle(&a, h->slot[k].ids), "ipc handle")) return false;
             if (!er.cuda(cudaIpcGetMemHandle(&b, h->slot[k].rows), "ipc handle")) return false;
@@ -383,7 +413,7 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
         int64_t mapped = 1;
         for (int q = 0; q < W && mapped; ++q) {
             if (q == h->rank) continue;
-            for (int k = 0; k < kSlots && mapped; ++k) {
+            for (int k = 0; k < h->nalloc && mapped; ++k) {
                 cudaIpcMemHandle_t a, b;
                 memcpy(&a, &all[((int64_t)q * 2 * kSlots + 2 * k) * hw], sizeof(a));
                 memcpy(&b, &all[((int64_t)q * 2 * kSlots + 2 * k + 1) * hw], sizeof(b));
@@ -406,7 +436,8 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
         if (*std::min_element(all_mapped.begin(), all_mapped.end()) == 0) {
             close_peers(h);
             h->p2p = false;
-            for (Slot &s : h->slot) {
+            for (int k = 0; k < h->nalloc; ++k) {
+                Slot &s = h->slot[k];
                 if (!er.cuda(cudaMalloc(&s.g_ids, W * cap * sizeof(int32_t)), "gather ids"))
                     return false;
                 if (!er.cuda(cudaMalloc(&s.g_rows, W * cap * dim * sizeof(float)), "gather rows"))
@@ -417,7 +448,7 @@ static bool ensure_slots(heat_shard *h, ShardErr &er, int64_t cap, int64_t dim) 
                     if (q != h->rank) pid[q * kSlots + k] = prow[q * kSlots + k] = nullptr;
         }
     }
-    for (int k = 0; k < kSlots; ++k) {
+    for (int k = 0; k < h->nalloc; ++k) {
         std::vector<const void *> a(W), b(W);
         for (int q = 0; q < W; ++q) {
             a[q] = pid[q * kSlots + k];
@@ -471,6 +502,119 @@ static bool ensure_epoch_buffers(heat_shard *h, ShardErr &er, int64_t t_rows, in
     return true;
 }
 
+// The persistent epoch's cross-rank words: (re)allocated zeroed when an epoch
+// has more steps than the mailbox holds, which every rank decides alike (the
+// step count is agreed); between processes the buffers are IPC-mapped into
+// every peer.  A reallocation restarts the global step count: no kernel runs
+// anywhere at that point (every rank finished its previous epoch before the
+// agreement collective), so no released word or log slot is still in use.
+static bool ensure_mailbox(heat_shard *h, ShardErr &er, int64_t nsteps) {
+    const int W = h->world;
+    if (nsteps <= h->mbox_steps && h->mbox) return true;
+    const int64_t steps = std::max<int64_t>(nsteps, 16);
+    cudaDeviceSynchronize();
+    for (void *q : h->opened_mbox) cudaIpcCloseMemHandle(q);
+    h->opened_mbox.clear();
+    cudaFree(h->mbox); cudaFree(h->rel);
+    h->mbox = h->rel = nullptr;
+    h->mbox_steps = 0;
+    const size_t mb = (size_t)2 * steps * W * sizeof(unsigned long long);
+    if (!er.cuda(cudaMalloc(&h->mbox, mb), "mailbox") ||
+        !er.cuda(cudaMalloc(&h->rel, (W + 1) * sizeof(unsigned long long)), "released words") ||
+        !er.cuda(cudaMemset(h->mbox, 0, mb), "zero mailbox") ||
+        !er.cuda(cudaMemset(h->rel, 0, (W + 1) * sizeof(unsigned long long)), "zero released"))
+        return false;
+    if (!h->mbox_tab &&
+        (!er.cuda(cudaMalloc((void **)&h->mbox_tab, kMaxWorld * sizeof(void *)), "mailbox table") ||
+         !er.cuda(cudaMalloc((void **)&h->rel_tab, kMaxWorld * sizeof(void *)), "released table")))
+        return false;
+    h->mbox_steps = steps;
+    h->gstep = 0;
+    h->tag = 1;
+    std::vector<void *> mt(W, nullptr), rt(W, nullptr);
+    mt[h->rank] = h->mbox;
+    rt[h->rank] = h->rel;
+    if (W > 1 && !h->loopback) {
+        constexpr int64_t hw = sizeof(cudaIpcMemHandle_t) / sizeof(int64_t);
+        std::vector<int64_t> mine(2 * hw), all(W * 2 * hw);
+        cudaIpcMemHandle_t a, b;
+        if (!er.cuda(cudaIpcGetMemHandle(&a, h->mbox), "ipc handle") ||
+            !er.cuda(cudaIpcGetMemHandle(&b, h->rel), "ipc handle"))
+            return false;
+        memcpy(&mine[0], &a, sizeof(a));
+        memcpy(&mine[hw], &b, sizeof(b));
+        if (!host_all_gather(h, er, mine.data(), 2 * hw, all.data())) return false;
+        for (int q = 0; q < W; ++q) {
+            if (q == h->rank) continue;
+            memcpy(&a, &all[(int64_t)q * 2 * hw], sizeof(a));
+            memcpy(&b, &all[(int64_t)q * 2 * hw + hw], sizeof(b));
+            if (!er.cuda(cudaIpcOpenMemHandle(&mt[q], a, cudaIpcMemLazyEnablePeerAccess), "map mailbox"))
+                return false;
+            h->opened_mbox.push_back(mt[q]);
+            if (!er.cuda(cudaIpcOpenMemHandle(&rt[q], b, cudaIpcMemLazyEnablePeerAccess), "map released"))
+                return false;
+            h->opened_mbox.push_back(rt[q]);
+        }
+    }
+    // (a loopback group fills its tables with every rank's buffers itself)
+    return er.cuda(cudaMemcpy(h->mbox_tab, mt.data(), W * sizeof(void *), cudaMemcpyHostToDevice),
+                   "mailbox table") &&
+           er.cuda(cudaMemcpy(h->rel_tab, rt.data(), W * sizeof(void *), cudaMemcpyHostToDevice),
+                   "released table");
+}
+
+// local per-epoch state of the persistent epoch, `nctx` device contexts
+static bool ensure_persist_state(heat_shard *h, ShardErr &er, int64_t nsteps, int nctx,
+                                 int64_t t_rows, int64_t dim, int nb) {
+    if (nsteps > h->pstate_steps) {
+        cudaDeviceSynchronize();
+        cudaFree(h->pstate); cudaFree(h->pcnt);
+        h->pstate = h->pcnt = nullptr;
+        h->pstate_steps = 0;
+        const int64_t n = std::max<int64_t>(nsteps, 16);
+        if (!er.cuda(cudaMalloc(&h->pstate, kStepWords * n * sizeof(unsigned long long)), "step state") ||
+            !er.cuda(cudaMalloc(&h->pcnt, n * sizeof(unsigned long long)), "step counts"))
+            return false;
+        h->pstate_steps = n;
+    }
+    if (!h->pclaim && !er.cuda(cudaMalloc(&h->pclaim, 4 * sizeof(unsigned long long)), "claim"))
+        return false;
+    // accumulation buffers: zeroed once; every convert leaves them zero again
+    if (nb > h->pbufs || t_rows > h->pbuf_rows || dim != h->pbuf_dim) {
+        cudaDeviceSynchronize();
+        for (int k = 0; k < kSlots; ++k) {
+            cudaFree(h->pacc[k]); cudaFree(h->pflags[k]); cudaFree(h->ptouched[k]);
+            h->pacc[k] = nullptr; h->pflags[k] = h->ptouched[k] = nullptr;
+        }
+        h->pbufs = 0;
+        if (!h->ptcount &&
+            !er.cuda(cudaMalloc(&h->ptcount, kSlots * sizeof(unsigned long long)), "row counts"))
+            return false;
+        for (int k = 0; k < nb; ++k) {  // (a step touches at most t_rows rows)
+            if (!er.cuda(cudaMalloc(&h->pacc[k], t_rows * dim * sizeof(long long)), "accumulator") ||
+                !er.cuda(cudaMemset(h->pacc[k], 0, t_rows * dim * sizeof(long long)), "zero acc") ||
+                !er.cuda(cudaMalloc(&h->pflags[k], t_rows * sizeof(int32_t)), "row map") ||
+                !er.cuda(cudaMemset(h->pflags[k], 0, t_rows * sizeof(int32_t)), "clear row flags") ||
+                !er.cuda(cudaMalloc(&h->ptouched[k], t_rows * sizeof(int32_t)), "row lists"))
+                return false;
+        }
+        if (!er.cuda(cudaMemset(h->ptcount, 0, kSlots * sizeof(unsigned long long)), "zero counts"))
+            return false;
+        h->pbufs = nb;
+        h->pbuf_rows = t_rows;
+        h->pbuf_dim = dim;
+    }
+    if (nctx > h->pctx_n) {
+        cudaDeviceSynchronize();
+        cudaFree(h->pctx);
+        h->pctx = nullptr;
+        h->pctx_n = 0;
+        if (!er.cuda(cudaMalloc(&h->pctx, nctx * sizeof(PersistRank)), "contexts")) return false;
+        h->pctx_n = nctx;
+    }
+    return true;
+}
+
 }  // namespace heat
 
 using namespace heat;
@@ -497,12 +641,17 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
     h->device = device;
     const char *ex = getenv("HEAT_SHARD_EXCHANGE");
     h->p2p = !(ex && strcmp(ex, "gather") == 0);
-    if (const char *l = getenv("HEAT_SHARD_LAG")) h->lag = std::min(std::max(atoi(l), 1), kSlots - 1);
+    if (const char *l = getenv("HEAT_SHARD_LAG"))
+        h->lag = h->lag_persist = std::min(std::max(atoi(l), 1), kSlots - 1);
     // captured step graphs: on by default at world 1; with NCCL calls inside
     // the capture (world > 1) only on request, as that path has not run on a
     // multi-GPU box here
     h->graphs = world == 1;
     if (const char *g = getenv("HEAT_SHARD_GRAPH")) h->graphs = atoi(g) != 0;
+    if (const char *q = getenv("HEAT_SHARD_PERSIST")) {
+        h->persist = atoi(q) != 0;
+        h->persist_force = atoi(q) == 2;
+    }
     cudaSetDevice(device);
     // the exchange runs at the highest priority: its apply CTAs take the SM
     // slots that the step kernels free before the next kernel's workers do
@@ -572,6 +721,13 @@ int heat_shard_destroy(heat_shard *h) {
     cudaFree(h->d_users); cudaFree(h->d_items); cudaFree(h->d_pidx);
     cudaFree(h->d_bounds); cudaFreeHost(h->h_bounds);
     cudaFree(h->d_s0); cudaFreeHost(h->h_s0);
+    for (void *q : h->opened_mbox) cudaIpcCloseMemHandle(q);
+    cudaFree(h->mbox); cudaFree(h->rel); cudaFree(h->mbox_tab); cudaFree(h->rel_tab);
+    cudaFree(h->pstate); cudaFree(h->pcnt); cudaFree(h->pclaim); cudaFree(h->pctx);
+    for (int k = 0; k < kSlots; ++k) {
+        cudaFree(h->pacc[k]); cudaFree(h->pflags[k]); cudaFree(h->ptouched[k]);
+    }
+    cudaFree(h->ptcount);
     if (h->comm) nccl().comm_destroy(h->comm);
     for (cudaStream_t s : {h->comm_stream, h->cstream[0], h->cstream[1]})
         if (s) cudaStreamDestroy(s);
@@ -620,11 +776,17 @@ struct EpochRun {
         // compute(s) must not refill the slot apply(s - nslots) still reads,
         // which needs lag >= 2 (lag 1 would let compute(s) run before apply(s-1)
         // is even enqueued)
-        lag = direct ? h->lag : std::max(h->lag, 2);
+        if (persist_eligible()) {
+            lag = h->lag_persist;
+        } else {
+            lag = direct ? h->lag : std::max(h->lag, 2);
+            lag = std::min(lag, kStreamMaxLag);
+        }
         nslots = lag + 1;
         // captured step graphs need the device-range kernels and a host-free
         // step loop (the gather fallback reads counts on the host between steps)
-        dr = direct && h->graphs && !h->loopback && device_step_supported(p, S, T);
+        dr = direct && h->graphs && !h->loopback && device_step_supported(p, S, T) &&
+             !persist_eligible();
         total = nsteps > 0 ? bounds[nsteps] : 0;
         if (dr) {  // the epoch's inputs into runtime-owned buffers
             if (total > h->pairs_cap) {
@@ -671,8 +833,8 @@ struct EpochRun {
                                     caller), "s0 in");
         }
         // log counters start at zero (afterwards each step's apply re-arms its slot)
-        for (Slot &sl : h->slot)
-            if (sl.cnt) er.cuda(cudaMemsetAsync(sl.cnt, 0, sizeof(int64_t), caller), "zero");
+        for (int k = 0; k < h->nalloc; ++k)
+            er.cuda(cudaMemsetAsync(h->slot[k].cnt, 0, sizeof(int64_t), caller), "zero");
         return er.rc;
     }
 
@@ -865,6 +1027,105 @@ struct EpochRun {
         cudaGetLastError();
     }
 
+    // ---- persistent epoch ------------------------------------------------
+    // every rank of the job decides alike (same parameters, same exchange)
+    bool persist_eligible() const {
+        if (!h->persist || !direct || W > kPersistMaxWorld || nsteps < 1) return false;
+        // K = 128 (configs 4/5); at K = 64 the several-warps-per-pair kernel of
+        // the stream-ordered steps is faster (c3: 37.7 M vs 31.5 M samples/s at
+        // N = 1), HEAT_SHARD_PERSIST=2 forces the persistent epoch there too
+        if (K != 128 && !(K == 64 && h->persist_force)) return false;
+        if (!p->use_cosine || (p->flags & 1)) return false;
+        return ((uintptr_t)S % 16 == 0) && ((uintptr_t)T % 16 == 0);
+    }
+
+    // per-rank buffers and the host context (tables filled by the caller for
+    // a loopback group)
+    bool persist_prepare() {
+        if (!ensure_mailbox(h, er, nsteps)) return false;
+        if (!ensure_persist_state(h, er, nsteps, group ? W : 1, t_rows, K, lag)) return false;
+        if (nsteps + 1 > h->bounds_cap) {
+            cudaDeviceSynchronize();
+            cudaFree(h->d_bounds);
+            cudaFreeHost(h->h_bounds);
+            h->d_bounds = nullptr;
+            h->h_bounds = nullptr;
+            h->bounds_cap = 0;
+            h->gkey.clear();
+            if (!er.cuda(cudaMalloc(&h->d_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds") ||
+                !er.cuda(cudaMallocHost(&h->h_bounds, (nsteps + 1) * sizeof(int64_t)), "bounds"))
+                return false;
+            h->bounds_cap = nsteps + 1;
+        }
+        // (the pinned staging copy is free again: the previous epoch synchronized)
+        memcpy(h->h_bounds, bounds, (nsteps + 1) * sizeof(int64_t));
+        er.cuda(cudaMemcpyAsync(h->d_bounds, h->h_bounds, (nsteps + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, caller), "bounds in");
+        er.cuda(cudaMemsetAsync(h->pstate, 0, kStepWords * nsteps * sizeof(unsigned long long),
+                                caller), "zero step state");
+        er.cuda(cudaMemsetAsync(h->pcnt, 0, nsteps * sizeof(unsigned long long), caller), "zero counts");
+        er.cuda(cudaMemsetAsync(h->pclaim, 0, 4 * sizeof(unsigned long long), caller), "zero claim");
+        return er.rc == HEAT_OK;
+    }
+
+    PersistRank persist_ctx() const {
+        PersistRank c{};
+        c.S = S; c.T = T; c.users = users; c.items = items; c.pidx = pidx;
+        c.bounds = h->d_bounds;
+        c.nsteps = nsteps;
+        c.claim = h->pclaim;
+        c.state = h->pstate;
+        c.cnt = h->pcnt;
+        for (int k = 0; k < kPersistSlots; ++k) {
+            c.log_ids[k] = h->slot[k].ids;
+            c.log_rows[k] = h->slot[k].rows;
+            c.pids[k] = h->slot[k].pids;
+            c.prows[k] = h->slot[k].prows;
+        }
+        c.mbox_tab = h->mbox_tab;
+        c.rel_tab = h->rel_tab;
+        c.mbox = h->mbox;
+        c.rel = h->rel;
+        for (int k = 0; k < kPersistSlots; ++k) {
+            c.acc[k] = h->pacc[k];
+            c.map[k] = h->pflags[k];
+            c.touched[k] = h->ptouched[k];
+        }
+
+        c.ctr = counters;
+        c.step_counts = counts_row(0);
+        c.cap = cap;
+        c.mbox_steps = h->mbox_steps;
+        c.gbase = h->gstep;
+        c.tag = h->tag;
+        c.rank = h->rank;
+        c.world = W;
+        c.lag = lag;
+        c.nslots = nslots;
+        c.gmod_lag = (int)(h->gstep % (unsigned long long)lag);
+        c.gmod_slots = (int)(h->gstep % (unsigned long long)nslots);
+        return c;
+    }
+
+    HogwildArgs persist_args() const {
+        HogwildArgs a{};
+        a.S = S; a.T = T; a.users = users; a.items = items;
+        a.start = 0; a.stop = total;
+        a.K = (int)K; a.N = p->n_neg; a.cosine = p->use_cosine;
+        a.lr = (float)p->lr; a.l2 = (float)p->l2; a.mu = p->mu; a.theta = p->theta;
+        a.s0 = p->stream_base; a.num_items = t_rows; a.ctr = counters; a.s_rows = s_rows;
+        a.window = p->window;  // > 0: at most this many pairs in flight per rank
+        a.fp64 = 0;
+        a.pair_index = pidx;
+        return a;
+    }
+
+    // after the launch: the epoch's global steps are consumed on every rank
+    void persist_advance() {
+        h->gstep += (unsigned long long)nsteps;
+        h->tag += 1;
+    }
+
     // the epoch's counts come back once for the statistics; a log that
     // overflowed is reported (the capacity is the exact worst case, so this
     // is a defensive check, not a mode of operation)
@@ -949,6 +1210,23 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         }
     }
     if (run.setup(cap) != HEAT_OK) return run.er.rc;
+    if (run.persist_eligible()) {
+        if (!run.persist_prepare()) return run.er.rc;
+        const PersistRank c = run.persist_ctx();
+        const cudaError_t e = launch_shard_persist(run.persist_args(), &c, h->pctx, 1, run.caller);
+        if (e == cudaSuccess) {
+            run.persist_advance();
+            const int rc = run.finish(stats);
+            if (rc == HEAT_OK) persist_prof_report();
+            else persist_watchdog_report();
+            return rc;
+        }
+        if (e != cudaErrorNotSupported) {
+            run.er.cuda(e, "persistent epoch");
+            return run.er.rc;
+        }
+        cudaGetLastError();  // no persistent kernel for these parameters: stream-ordered steps
+    }
     run.run_single();
     return run.finish(stats);
 }
@@ -1014,7 +1292,7 @@ int heat_shard_epoch_loopback(heat_shard **hs, int32_t world, const heat_shard_r
     for (int r = 0; r < world; ++r)
         if (runs[r].setup(cap) != HEAT_OK) return runs[r].er.rc;
     // peers' logs through plain device pointers (one address space)
-    for (int k = 0; k < kSlots; ++k) {
+    for (int k = 0; k < hs[0]->nalloc; ++k) {
         std::vector<const void *> ids(world), rows(world);
         for (int q = 0; q < world; ++q) {
             ids[q] = hs[q]->slot[k].ids;
@@ -1035,6 +1313,45 @@ int heat_shard_epoch_loopback(heat_shard **hs, int32_t world, const heat_shard_r
             if (r.er.rc != HEAT_OK) return false;
         return true;
     };
+    // persistent group: one cooperative launch over every rank's contexts
+    bool persist = true;
+    for (auto &r : runs) persist = persist && r.persist_eligible();
+    if (persist) {
+        for (auto &r : runs)
+            if (!r.persist_prepare()) return r.er.rc;
+        std::vector<void *> mt(world), rt(world);
+        for (int q = 0; q < world; ++q) {
+            mt[q] = hs[q]->mbox;
+            rt[q] = hs[q]->rel;
+        }
+        std::vector<PersistRank> cx(world);
+        for (int r = 0; r < world; ++r) {
+            if (!runs[r].er.cuda(cudaMemcpy(hs[r]->mbox_tab, mt.data(), world * sizeof(void *),
+                                            cudaMemcpyHostToDevice), "mailbox table") ||
+                !runs[r].er.cuda(cudaMemcpy(hs[r]->rel_tab, rt.data(), world * sizeof(void *),
+                                            cudaMemcpyHostToDevice), "released table"))
+                return runs[r].er.rc;
+            cx[r] = runs[r].persist_ctx();
+        }
+        const cudaError_t e = launch_shard_persist(runs[0].persist_args(), cx.data(), h0->pctx,
+                                                   world, runs[0].caller);
+        if (e == cudaSuccess) {
+            for (auto &r : runs) r.persist_advance();
+            int rc = HEAT_OK;
+            for (int r = 0; r < world; ++r) {
+                const int x = runs[r].finish(stats ? stats + r : nullptr);
+                if (rc == HEAT_OK) rc = x;
+            }
+            if (rc != HEAT_OK) persist_watchdog_report();
+            for (int r = 0; r < world; ++r) hs[r]->shared_counts = nullptr;
+            return rc;
+        }
+        if (e != cudaErrorNotSupported) {
+            runs[0].er.cuda(e, "persistent group epoch");
+            return runs[0].er.rc;
+        }
+        cudaGetLastError();
+    }
     for (auto &r : runs) r.fork(r.caller);
     const bool direct = runs[0].direct;
     auto count_all = [&](int64_t s) {

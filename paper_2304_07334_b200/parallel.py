@@ -75,6 +75,16 @@ def log_bytes(capacity: int, dim: int, slots: int, world: int, gather: bool) -> 
     return slots * per * (1 + (world if gather else 0))
 
 
+def native_log_slots() -> int:
+    """Log slots heat_shard.cu allocates: max(lag, 2) + 1, lag = HEAT_SHARD_LAG
+    (1..7; unset: 2 for stream-ordered steps, 3 for the persistent epoch, so 4
+    slots).  The persistent epoch also keeps `lag` fixed-point accumulation
+    buffers of the item table (8 bytes per element each)."""
+    import os
+    lag = min(max(int(os.environ.get("HEAT_SHARD_LAG", "3")), 1), 7)
+    return max(lag, 2) + 1
+
+
 def check_log_memory(capacity: int, dim: int, slots: int, world: int, gather: bool,
                      device) -> None:
     """ValueError (before the epoch mutates anything) when the logs would not
@@ -465,7 +475,7 @@ class NativeShardTrainer(ShardedTrainer):
     def _log_layout(self):
         import os
         gather = self.world > 1 and os.environ.get("HEAT_SHARD_EXCHANGE") == "gather"
-        return 4, gather  # heat_shard.cu allocates kSlots = 4 logs
+        return native_log_slots(), gather
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -539,7 +549,7 @@ class LoopbackShardGroup:
             b = np.ascontiguousarray(bounds, dtype=np.int64)
             local_max = int(np.diff(b).max()) if len(b) > 1 else 0
             cap = delta_capacity(local_max, params.n_neg, params.l2)
-            check_log_memory(cap, m.dim, 4, W, False, dev)
+            check_log_memory(cap, m.dim, native_log_slots(), W, False, dev)
             keep += [lu, li, lp, b]
             ranks[r] = N.ShardRank(_p(m.S), m.S.shape[0], _p(m.T), m.T.shape[0], _p(lu), _p(li),
                                    _p(lp), b.ctypes.data, cap, m.counters.ptr())
