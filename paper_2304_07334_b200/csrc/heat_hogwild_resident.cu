@@ -85,7 +85,16 @@ __device__ __forceinline__ void rs_red(float *p, const float (&d)[VW]) {
 // warp signals as soon as its own copies land, before it scores, so the wait
 // before the writes rarely stalls.
 // DR: the pair range and stream base come from HogwildArgs::range_dev/s0_dev
-template <int K, int NB, bool EARLY, bool SPLIT, bool IDPF, bool DR>
+// PIPE (with SPLIT and IDPF, not at window 1): a warp whose stage has at most
+// two rows to write computes their deltas into registers right after scoring,
+// issues the NEXT pair's copies into its stage (now free), and only then waits
+// for the pair's mbarrier and writes — the wait overlaps the next copies
+// instead of spinning (round 1: ~470 of 2198 instructions per c2 pair were the
+// wait loop).  A stage with more rows to write takes the unpipelined order.
+// Measured on c2: 303.6 M samples/s against 346.2 M without it (the next
+// pair's copies, issued ahead of the writes, delay them; the wait was not the
+// binding cost), so HEAT_RESIDENT_PIPE=1 only.
+template <int K, int NB, bool EARLY, bool SPLIT, bool IDPF, bool DR, bool PIPE>
 // 7 resident CTAs per SM (the window allows ~7 pairs per SM), but never
 // fewer than 64 registers per thread
 __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB : 1) : 7))
@@ -150,6 +159,23 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
     uint32_t nx_id = (uint32_t)nx_pos;
     if (IDPF && r > 0) nx_id = (uint32_t)fm.mod(mix64(k_s0 + (uint64_t)nx_pg * pair_step + lane_off));
 
+    // this warp's stage copies (row ids: lane j holds row j's) and its user row
+    auto issue_copies = [&](uint32_t ids, int64_t uid, float *udst) {
+        const float *srcb = a.T + my_ch * 4;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int row = i * RPI + my_rsub;
+            const uint32_t rid = __shfl_sync(0xffffffffu, ids, row & 31);
+            if (row < nvalid)
+                cp_async16_hint(my_stage + row * G::SLOTF + my_ch * 4, srcb + (size_t)rid * K, pol);
+        }
+        if (EARLY || w == 0)
+            for (int ch = lane; ch < G::CH; ch += 32)
+                cp_async16(udst + ch * 4, a.S + uid * K + ch * 4);
+        cp_async_commit();
+    };
+    bool pre = false;  // PIPE: this pair's copies were issued by the previous one
+
     for (; p < k_stop; p += n_workers, parity ^= 1) {
         ++mine;
         float *urow = EARLY ? ubuf + w * K : ubuf + parity * K;
@@ -157,7 +183,8 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
         const int32_t pos = nx_pos;
         const int64_t u = nx_u;
         const int64_t pg = nx_pg;
-        if (p + n_workers < k_stop) {
+        const bool has_next = p + n_workers < k_stop;
+        if (has_next) {
             nx_pos = a.items[p + n_workers];
             nx_u = a.users[p + n_workers];
             nx_pg = a.pair_index ? a.pair_index[p + n_workers] : p + n_workers;
@@ -168,19 +195,7 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
         else if (r > 0)
             id = (uint32_t)fm.mod(mix64(k_s0 + (uint64_t)pg * pair_step + lane_off));
         {
-            const float *srcb = a.T + my_ch * 4;
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-                const int row = i * RPI + my_rsub;
-                const uint32_t rid = __shfl_sync(0xffffffffu, id, row & 31);
-                if (row < nvalid)
-                    cp_async16_hint(my_stage + row * G::SLOTF + my_ch * 4,
-                                    srcb + (size_t)rid * K, pol);
-            }
-            if (EARLY || w == 0)
-                for (int ch = lane; ch < G::CH; ch += 32)
-                    cp_async16(urow + ch * 4, a.S + u * K + ch * 4);
-            cp_async_commit();
+            if (!pre) issue_copies(id, u, urow);
             if (IDPF) {
                 nx_id = (uint32_t)nx_pos;
                 if (r > 0)
@@ -269,6 +284,41 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
             }
         }
         loss += wneg * hinge;
+        unsigned m = __ballot_sync(0xffffffffu, write);
+        // PIPE: deltas of at most two written rows into registers, then the
+        // next pair's copies, then the wait
+        const bool pipe = PIPE && !strict && has_next && __popc(m) <= 2;
+        pre = pipe;
+        float dq[2][VW], ugp[VW];
+        int32_t idq[2] = {0, 0};
+        if (pipe) {
+#pragma unroll
+            for (int i = 0; i < VW; ++i) ugp[i] = 0.f;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int src = m ? __ffs(m) - 1 : 0;
+                const bool live = m != 0;
+                m &= m ? m - 1 : 0u;
+                const double tt_s = __shfl_sync(0xffffffffu, ttx, src);
+                const double st_s = __shfl_sync(0xffffffffu, stx, src);
+                const double ss_s = __shfl_sync(0xffffffffu, ssx, src);
+                const float w_s = (float)__shfl_sync(0xffffffffu, wt, src);
+                idq[q] = live ? (int32_t)__shfl_sync(0xffffffffu, id, src) : -1;
+                if (live) {
+                    const WriteEntry we{tt_s, st_s, (double)w_s, idq[q], 0};
+                    const RowCoef co = row_coef_f(we, ss_s, rss, a.lr, a.l2, a.cosine);
+                    const float *srow = my_stage + src * G::SLOTF;
+#pragma unroll
+                    for (int i = 0; i < VW; ++i) {
+                        const int col = lane * VW + i;
+                        const float v = lane < G::ACT ? srow[col] : 0.f;
+                        row_apply(co, uu[i], v, dq[q][i], ugp[i]);
+                    }
+                }
+            }
+            __syncwarp();  // every lane's reads of the stage are done
+            issue_copies(nx_id, nx_u, urow);
+        }
         if (SPLIT) {  // every read of the pair precedes every write
             if (kSleepWait)
                 mbar_wait_sleep(&reads_done, phase);
@@ -279,8 +329,35 @@ __global__ void __launch_bounds__(32 * NB, (32 / NB < 7 ? (32 / NB > 0 ? 32 / NB
             __syncthreads();
         }
 
+        if (pipe) {  // ---- C (pipelined): the registered deltas
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (idq[q] < 0) continue;
+                if (!dmode) {
+                    if (lane < G::ACT) rs_red<VW>(a.T + (int64_t)idq[q] * K + lane * VW, dq[q]);
+                } else {
+                    long long sl = 0;
+                    if (lane == 0) sl = (long long)atomicAdd((unsigned long long *)a.delta_count, 1ull);
+                    sl = __shfl_sync(0xffffffffu, sl, 0);
+                    if (sl < a.delta_capacity) {
+                        if (lane == 0) a.delta_ids[sl] = idq[q];
+                        if (lane < G::ACT) {
+#pragma unroll
+                            for (int i = 0; i < VW; ++i) a.delta_rows[sl * K + lane * VW + i] = dq[q][i];
+                        }
+                    }
+                }
+            }
+            if (idq[0] >= 0 && lane < G::ACT) {
+                float d[VW];
+#pragma unroll
+                for (int i = 0; i < VW; ++i) d[i] = -a.lr * ugp[i];
+                rs_red<VW>(a.S + u * K + lane * VW, d);
+            }
+            m = 0;
+        }
+
         // ---- C: apply my stage's written rows from their resident snapshots
-        unsigned m = __ballot_sync(0xffffffffu, write);
         if (m) {
             float ug[VW];
 #pragma unroll
@@ -370,11 +447,18 @@ static cudaError_t launch_resident_kn(const HogwildArgs &a, cudaStream_t st, int
         const char *e = getenv("HEAT_RESIDENT_IDPF");
         return e ? atoi(e) != 0 : true;  // measured c2: 357.7 M vs 355.9 M
     }();
-    auto kern = a.range_dev ? hogwild_resident<K, NB, true, true, true, true>
-                : early == 2 ? (idpf ? hogwild_resident<K, NB, true, true, true, false>
-                                     : hogwild_resident<K, NB, true, true, false, false>)
-                : early == 1 ? hogwild_resident<K, NB, true, false, false, false>
-                             : hogwild_resident<K, NB, false, false, false, false>;
+    // PIPE measured slower on c2 (303.6 M vs 346.2 M samples/s): opt-in only
+    static const bool pipe = [] {
+        const char *e = getenv("HEAT_RESIDENT_PIPE");
+        return e ? atoi(e) != 0 : false;
+    }();
+    auto kern = a.range_dev ? (pipe ? hogwild_resident<K, NB, true, true, true, true, true>
+                                    : hogwild_resident<K, NB, true, true, true, true, false>)
+                : early == 2 ? (idpf ? (pipe ? hogwild_resident<K, NB, true, true, true, false, true>
+                                             : hogwild_resident<K, NB, true, true, true, false, false>)
+                                     : hogwild_resident<K, NB, true, true, false, false, false>)
+                : early == 1 ? hogwild_resident<K, NB, true, false, false, false, false>
+                             : hogwild_resident<K, NB, false, false, false, false, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32 * NB, smem, &e);
     if (e != cudaSuccess) return e;
