@@ -200,6 +200,10 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "quality":
         quality()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "eval":
+        for c in sys.argv[2:] or ["c2"]:
+            evaluation(c)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "agg":
         agg_hogwild()
         sys.exit(0)
