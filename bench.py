@@ -302,6 +302,13 @@ def l2_probe(dev, table_bytes: int, T=None) -> dict:
     return out
 
 
+def shard_lag(persistent: bool) -> int:
+    """The staleness bound heat_shard.cu runs with (HEAT_SHARD_LAG, else 3 for
+    the persistent epoch and 2 for stream-ordered steps)."""
+    v = os.environ.get("HEAT_SHARD_LAG")
+    return min(max(int(v), 1), 7 if persistent else 3) if v else (3 if persistent else 2)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,8 +409,11 @@ def main():
             trainer.train_epoch(u, i, params(e), exchange_pairs, prepared=True)
             ev1.record(stream)
             ev1.synchronize()
-            # per step: the DELTA kernel + two apply kernels
-            launches_per_epoch = 3 * trainer.num_steps
+            # the persistent epoch: one launch; stream-ordered steps: the DELTA
+            # kernel + two apply kernels per step
+            st = getattr(trainer, "stats", None)
+            launches_per_epoch = (int(st.launches) if isinstance(st, N.ShardStats)
+                                  else 3 * trainer.num_steps)
             return ev0.elapsed_time(ev1) / 1e3, model.counters.read()
 
     for e in range(args.warmup):
@@ -538,7 +548,11 @@ def main():
                     "l2_flush": "512 MiB write before every timed epoch; S+T "
                                 f"{(S.nbytes + T.nbytes) / 1e6:.1f} MB",
                     "parallelism": (f"users sharded x{world}, item-delta exchange every "
-                                    f"{exchange_pairs} global pairs (P2P gather+apply)"
+                                    f"{exchange_pairs} global pairs ("
+                                    + ("persistent epoch: one launch, device-gated steps"
+                                       if launches_per_epoch == 1
+                                       else "stream-ordered steps, P2P gather+apply")
+                                    + f", lag {shard_lag(launches_per_epoch == 1)})"
                                     if sharded else "single GPU")},
             "roofline": roofline,
             "cpu_baseline": cpu,

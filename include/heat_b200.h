@@ -174,7 +174,17 @@ int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int
                                 int64_t stride, int64_t *acc, int32_t *flags, void *stream);
 
 /* ---- multi-GPU runtime --------------------------------
- * One rank per GPU.  A heat_shard owns the rank's exchange state: rotating
+ * One rank per GPU.  For dim 128 (HEAT_SHARD_PERSIST=1, the default) an
+ * epoch is ONE persistent kernel launch: steps are gated on the device (a
+ * pair of global step g starts once this rank applied step g - lag and every
+ * peer step g - lag - 1; lag 3, HEAT_SHARD_LAG 1..7), the workers add their
+ * own item deltas into per-step fixed-point buffers and log them for the
+ * peers, publish each finished step's entry count into every rank's mailbox
+ * (IPC-mapped; st.release.sys), and between pairs pull the peers' logs and
+ * convert the touched rows; each rank publishes its applied-step count the
+ * same way.  Otherwise (dim 64, HEAT_SHARD_PERSIST=0, or the gather
+ * exchange) the stream-ordered steps below run.
+ * A heat_shard owns the rank's exchange state: rotating
  * log slots, the fixed-point accumulator, two compute streams, a
  * top-priority comm stream and (world > 1) an NCCL communicator created from
  * a unique id that rank 0 makes with heat_nccl_unique_id and the caller
@@ -196,6 +206,7 @@ typedef struct heat_shard_stats {
     int64_t entries;         /* delta rows applied (sum over ranks and steps) */
     int64_t exchanged_bytes; /* bytes each rank read from its peers' logs     */
     int64_t max_entries;     /* largest per-rank log of a step                */
+    int64_t launches;        /* kernel launches of the epoch (1: persistent)  */
 } heat_shard_stats;
 
 int heat_nccl_unique_id(unsigned char *out128);

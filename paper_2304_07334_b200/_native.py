@@ -80,6 +80,7 @@ class ShardStats(ctypes.Structure):
         ("entries", ctypes.c_int64),
         ("exchanged_bytes", ctypes.c_int64),
         ("max_entries", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
     ]
 
 

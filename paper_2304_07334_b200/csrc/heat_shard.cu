@@ -760,6 +760,7 @@ struct EpochRun {
     int W = 1, lag = 2, nslots = 3;
     std::vector<int64_t> key;
     EpochRun **group = nullptr;  // loopback: every rank's run
+    bool persisted = false;      // the epoch ran as one persistent launch
 
     const int32_t *tr_users() const { return dr ? h->d_users : users; }
     const int32_t *tr_items() const { return dr ? h->d_items : items; }
@@ -1124,6 +1125,7 @@ struct EpochRun {
     void persist_advance() {
         h->gstep += (unsigned long long)nsteps;
         h->tag += 1;
+        persisted = true;
     }
 
     // the epoch's counts come back once for the statistics; a log that
@@ -1153,6 +1155,9 @@ struct EpochRun {
         }
         // bytes that crossed between GPUs: every rank reads every other rank's log
         st.exchanged_bytes = (W > 1 ? (W - 1) : 0) * st.entries * (4 * K + 4);
+        // persistent: one launch; stream-ordered: a DELTA kernel and the two
+        // apply kernels per step
+        st.launches = persisted ? 1 : 3 * nsteps;
         if (stats) *stats = st;
         return er.rc;
     }
