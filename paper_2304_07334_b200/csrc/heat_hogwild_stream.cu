@@ -162,6 +162,27 @@ __device__ __forceinline__ P *shfl_ptr(P *p, int src) {
     return reinterpret_cast<P *>(
         __shfl_sync(kFull, (unsigned long long)reinterpret_cast<uintptr_t>(p), src));
 }
+// accumulator traffic with an evict-first L2 policy, so it does not displace
+// the tables' evict-last lines (HEAT_PERSIST_ACC_EF=0: default policy)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void red_u64_ef(unsigned long long *p, unsigned long long v, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ longlong2 ld_acc2(const long long *p, uint64_t pol) {
+    longlong2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.s64 {%0, %1}, [%2], %3;"
+                 : "=l"(v.x), "=l"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void zero_acc2(long long *p, uint64_t pol) {
+    asm volatile("st.global.cg.L2::cache_hint.v2.s64 [%0], {%1, %1}, %2;" ::"l"(p), "l"(0ll), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ unsigned long long fix40(float v) {
     return (unsigned long long)__double2ll_rn((double)v * kFix);
 }
@@ -232,12 +253,13 @@ __device__ __forceinline__ void persist_accumulate(const PersistRank &R, int b, 
     if (c == 0 && atomicExch(R.map[b] + id, 1) == 0)
         R.touched[b][atomicAdd(R.state + kRows * R.nsteps + step, 1ull)] = id;
     unsigned long long *ac = reinterpret_cast<unsigned long long *>(R.acc[b] + (int64_t)id * K + 4 * c);
+    const uint64_t pol = policy_evict_first();
 #pragma unroll
     for (int j = 0; j < K / 32; ++j) {
-        atomicAdd(ac + 32 * j, fix40(d[j].x));
-        atomicAdd(ac + 32 * j + 1, fix40(d[j].y));
-        atomicAdd(ac + 32 * j + 2, fix40(d[j].z));
-        atomicAdd(ac + 32 * j + 3, fix40(d[j].w));
+        red_u64_ef(ac + 32 * j, fix40(d[j].x), pol);
+        red_u64_ef(ac + 32 * j + 1, fix40(d[j].y), pol);
+        red_u64_ef(ac + 32 * j + 2, fix40(d[j].z), pol);
+        red_u64_ef(ac + 32 * j + 3, fix40(d[j].w), pol);
     }
 }
 
@@ -356,6 +378,7 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
         // rows i0 .. i0 + m - 1 of the step's list
         int32_t myid = 0;
         if (lane < m) myid = __ldcg(R.touched[b] + i0 + lane);
+        const uint64_t pef = policy_evict_first();
         for (int hb = 0; hb < m; hb += 8) {
         longlong2 q01[2][V], q23[2][V];
         float4 tv[2][V];
@@ -369,8 +392,8 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
                 const float *tr = R.T + (int64_t)ids[h] * K + 4 * c;
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    q01[h][v] = __ldcg(reinterpret_cast<const longlong2 *>(ac + 32 * v));
-                    q23[h][v] = __ldcg(reinterpret_cast<const longlong2 *>(ac + 32 * v + 2));
+                    q01[h][v] = ld_acc2(ac + 32 * v, pef);
+                    q23[h][v] = ld_acc2(ac + 32 * v + 2, pef);
                     tv[h][v] = __ldcg(reinterpret_cast<const float4 *>(tr + 32 * v));
                 }
             }
@@ -383,8 +406,8 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
                 float *tr = R.T + (int64_t)ids[h] * K + 4 * c;
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    __stcg(reinterpret_cast<longlong2 *>(ac + 32 * v), make_longlong2(0, 0));
-                    __stcg(reinterpret_cast<longlong2 *>(ac + 32 * v + 2), make_longlong2(0, 0));
+                    zero_acc2(ac + 32 * v, pef);
+                    zero_acc2(ac + 32 * v + 2, pef);
                     float4 x = tv[h][v];
                     x.x += (float)((double)q01[h][v].x * (1.0 / kFix));
                     x.y += (float)((double)q01[h][v].y * (1.0 / kFix));

@@ -226,3 +226,28 @@ def test_persistent_epoch_full_occupancy(torch_cuda, monkeypatch, G, K, lag):
     lp = run("2")
     ls = run("0")
     assert np.isfinite(lp) and abs(lp - ls) <= 0.03 * abs(ls), (lp, ls)
+
+
+@pytest.mark.parametrize("K,launches_one", [(128, True), (64, False)])
+def test_default_mode_by_dim(torch_cuda, monkeypatch, K, launches_one):
+    """The runtime's default: the persistent epoch (one launch) at K = 128,
+    the stream-ordered steps (a DELTA kernel and two apply kernels per step)
+    at K = 64; both train every pair once."""
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.parallel import NativeShardTrainer
+    from paper_2304_07334_b200.rng import shuffle_seed
+    for v in ("HEAT_SHARD_PERSIST", "HEAT_SHARD_LAG", "HEAT_SHARD_GRAPH", "HEAT_HOGWILD_IMPL"):
+        monkeypatch.delenv(v, raising=False)
+    train, S, T = _setup(K)
+    m = DeviceModel(S, T)
+    tr = NativeShardTrainer(m, 1, 0)
+    u, i = epoch_pairs(train, shuffle_seed(0, 0))
+    m.counters.reset()
+    st = tr.train_epoch(u, i, _params(m, 0, 0), 512)
+    assert m.counters.read().pairs == len(u)
+    assert st.steps > 1
+    assert (st.launches == 1) == launches_one, (st.launches, st.steps)
+    if not launches_one:
+        assert st.launches == 3 * st.steps
+    tr.close()
