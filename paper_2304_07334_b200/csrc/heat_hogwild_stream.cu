@@ -119,23 +119,26 @@ __device__ __forceinline__ double seq_dot(const float *a, const float *b) {
 
 // ---- persistent sharded epoch (MODE 2) --------------------------------------
 // One launch trains a rank's whole epoch of DELTA steps (heat_shard.cu sets
-// it up).  Steps are gated on the device instead of by stream order:
-//  * a pair of step s (global step g = gbase + s) starts once this rank has
-//    applied every step up to g - lag and every peer has applied up to
-//    g - lag - 1, the last reader of log slot g % (lag + 1) it will write;
-//  * item-row deltas go straight into the step's accumulation buffer
-//    (g % lag: the steps that can be in flight at once never share one) as
-//    2^-40 fixed-point integer sums, and the touched row joins the buffer's
-//    row list; at world > 1 they are also logged for the peers, and the warp
-//    that finishes a step's last pair publishes the log's entry count into
-//    every rank's mailbox (one 8-byte store per rank, release at system
-//    scope: the log it describes is complete);
-//  * every rank applies each step in step order, the workers doing the work
-//    between pairs: the peers' logged entries are pulled over NVLink into the
-//    buffer in claimed chunks, then, once the rank's own pairs of the step
-//    are done, each touched row is converted once (T += float(sum)).
-//    Integer sums commute, so every replica of T stays bit-identical however
-//    producers and chunks interleave;
+// it up).  Item row id belongs to rank id % world (its OWNER), which alone
+// computes the row's new value each step and stores it into every replica.
+// Steps are gated on the device instead of by stream order:
+//  * a pair of step s (global step g = gbase + s) starts once every rank has
+//    applied its rows of every step up to g - lag (which also frees the log
+//    slot g % (lag + 1) it will write);
+//  * a written row's deltas go, if this rank owns the row, straight into the
+//    step's accumulation buffer (g % lag: the steps that can be in flight at
+//    once never share one) as 2^-40 fixed-point integer sums, the row joining
+//    the buffer's row list; otherwise they are logged.  The warp that
+//    finishes a step's last pair publishes the step's counts into every
+//    rank's mailbox (one 8-byte store per rank, release at system scope: the
+//    log it describes is complete);
+//  * every rank applies its rows of each step in step order, the workers
+//    doing the work between pairs: the peers' logged entries for its rows are
+//    pulled over NVLink into the buffer in claimed chunks, then each touched
+//    row is converted once (T += float(sum)) and the new row is stored into
+//    every peer's replica.  Integer sums commute and each row has one
+//    writer, so the replicas stay bit-identical, and a rank's apply work does
+//    not grow with the world size;
 //  * a finished apply is published as the rank's released-step count into
 //    every rank's `rel` words (monotone, never reset between epochs).
 // No warp waits on anything that is not already claimed by a running warp
@@ -220,8 +223,8 @@ __device__ __forceinline__ int persist_slot(const PersistRank &R, long long s) {
 // may a pair of global step g start? (lane q < world checks rank q's word)
 __device__ __forceinline__ bool persist_gate_open(const PersistRank &R, long long g, int lane) {
     bool ok = true;
-    if (lane < R.world) {
-        const long long need = lane == R.rank ? g - R.lag + 1 : g - R.lag;
+    if (lane < R.world) {  // every owner applied its rows of step g - lag
+        const long long need = g - R.lag + 1;
         if (need > 0) ok = (long long)ld_acquire_sys(R.rel + lane) >= need;
     }
     return __all_sync(kFull, ok);
@@ -230,13 +233,18 @@ __device__ __forceinline__ bool persist_gate_open(const PersistRank &R, long lon
 // step s's log on this rank is complete: its count into every rank's mailbox
 __device__ __forceinline__ void persist_publish(const PersistRank &R, long long s, int lane) {
     if (R.world == 1) return;  // nobody reads it
-    unsigned long long c = 0;
-    if (lane == 0) c = ld_acquire_gpu(R.cnt + s);
+    unsigned long long c = 0, wr = 0;
+    if (lane == 0) {
+        c = ld_acquire_gpu(R.cnt + s);                         // logged
+        wr = ld_acquire_gpu(R.state + kWritten * R.nsteps + s);  // written
+    }
     c = __shfl_sync(kFull, c, 0);
+    wr = __shfl_sync(kFull, wr, 0);
     __threadfence_system();
     __syncwarp();
     if (lane < R.world) {
-        const unsigned long long w = ((unsigned long long)R.tag << 32) | (c < 0xffffffffull ? c : 0xffffffffull);
+        const unsigned long long w = ((unsigned long long)(R.tag & 0xffffu) << 48) |
+                                     ((wr & 0xffffffull) << 24) | (c & 0xffffffull);
         st_release_sys(R.mbox_tab[lane] + (((long long)(R.tag & 1) * R.mbox_steps + s) * R.world + R.rank), w);
     }
 }
@@ -267,7 +275,8 @@ __device__ __forceinline__ void persist_accumulate(const PersistRank &R, int b, 
 // step): statistics, then the released count
 __device__ __forceinline__ void persist_finish(const PersistRank &R, long long t, long long c,
                                                int lane) {
-    if (lane == R.rank) c = (long long)ld_acquire_gpu(R.cnt + t);
+    // statistics: the item rows each rank's pairs of the step wrote
+    if (lane == R.rank) c = (long long)ld_acquire_gpu(R.state + kWritten * R.nsteps + t);
     if (lane < R.world) R.step_counts[t * R.world + lane] = c;
     __threadfence_system();
     __syncwarp();
@@ -300,17 +309,19 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
     // 1. ready once this rank's pairs of step t are done and every peer's log
     //    of step t is complete
     if ((long long)ld_acquire_gpu(st + kDone * n) < R.bounds[t + 1] - R.bounds[t]) return 0;
-    long long cnt = 0;  // lane q < world, q != rank: rank q's logged entries of step t
+    long long cnt = 0;   // lane q < world, q != rank: rank q's logged entries of step t
+    long long wrote = 0;  // ... and the rows its pairs wrote (statistics)
     bool ok = true;
     if (lane < R.world && lane != R.rank) {
         const unsigned long long v =
             ld_acquire_sys(R.mbox + ((long long)(R.tag & 1) * R.mbox_steps + t) * R.world + lane);
-        ok = (unsigned)(v >> 32) == R.tag;
-        cnt = (long long)(v & 0xffffffffull);
+        ok = (unsigned)(v >> 48) == (R.tag & 0xffffu);
+        cnt = (long long)(v & 0xffffffull);
+        wrote = (long long)((v >> 24) & 0xffffffull);
     }
     if (!__all_sync(kFull, ok)) return 0;  // some peer's log of step t is not complete yet
-    // 2. the peers' logged entries of step t into the buffer (this rank's
-    //    own deltas were added by the pairs themselves)
+    // 2. the peers' logged entries of step t for the rows this rank owns
+    //    into the buffer (its own pairs added theirs directly)
     if (R.world > 1) {
         const long long cc = cnt < R.cap ? cnt : R.cap;
         long long incl = cc;
@@ -355,7 +366,8 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
-                    persist_accumulate<K>(R, b, t, ids[h], c, p0 + 4 * h + g < m, d[h]);
+                    persist_accumulate<K>(R, b, t, ids[h], c,
+                                          p0 + 4 * h + g < m && ids[h] % R.world == R.rank, d[h]);
             }
             __threadfence();
             __syncwarp();
@@ -414,11 +426,16 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
                     x.z += (float)((double)q23[h][v].x * (1.0 / kFix));
                     x.w += (float)((double)q23[h][v].y * (1.0 / kFix));
                     __stcg(reinterpret_cast<float4 *>(tr + 32 * v), x);
+                    // the owner's new row into every peer's replica (NVLink)
+                    for (int p = 0; p < R.world; ++p)
+                        if (p != R.rank)
+                            *reinterpret_cast<float4 *>(R.t_tab[p] + (int64_t)ids[h] * K + 4 * c + 32 * v) = x;
                 }
                 if (c == 0) R.map[b][ids[h]] = 0;
             }
         }
         }
+        if (R.world > 1) __threadfence_system();  // the peers' replicas too
         __threadfence();
         __syncwarp();
         long long d = 0;
@@ -426,14 +443,14 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
             d = (long long)atomicAdd(st + kCvtDone * n, (unsigned long long)m) + m;
             s_pw[11] += clock64() - cv;
         }
-        if (__shfl_sync(kFull, d, 0) == rows) persist_finish(R, t, cnt, lane);
+        if (__shfl_sync(kFull, d, 0) == rows) persist_finish(R, t, wrote, lane);
         return 1;
     }
     if (rows == 0) {  // nothing touched: one warp finishes the step
         int win = 0;
         if (lane == 0) win = atomicCAS(st + kFin * n, 0ull, 1ull) == 0ull;
         if (__shfl_sync(kFull, win, 0)) {
-            persist_finish(R, t, cnt, lane);
+            persist_finish(R, t, wrote, lane);
             return 1;
         }
     }
@@ -894,19 +911,22 @@ __global__ void __launch_bounds__(32, MINB)
                 unsigned long long *lcnt = reinterpret_cast<unsigned long long *>(a.delta_count);
                 int64_t lcap = a.delta_capacity;
                 bool log = true;
-                if constexpr (PS) {  // own deltas into the step's buffer; logged for the peers
+                bool mine = true;
+                if constexpr (PS) {  // owned rows into the step's buffer; the others logged
                     const PersistRank &R = prank();
                     const long long stp = s_pw[7];
-                    persist_accumulate<K>(R, persist_buf(R, stp), stp, ent.id, c, ok, d);
+                    mine = ent.id % R.world == R.rank;
+                    persist_accumulate<K>(R, persist_buf(R, stp), stp, ent.id, c, ok && mine, d);
+                    if (ok && c == 0) atomicAdd(R.state + kWritten * R.nsteps + stp, 1ull);
                     const int slt = persist_slot(R, stp);
                     lids = R.log_ids[slt];
                     lrows = R.log_rows[slt];
                     lcnt = R.cnt + stp;
                     lcap = R.cap;
-                    log = R.world > 1;
+                    log = !mine;
                 }
                 long long sl = 0;
-                if (ok && c == 0) sl = (long long)atomicAdd(lcnt, 1ull);
+                if (ok && log && c == 0) sl = (long long)atomicAdd(lcnt, 1ull);
                 sl = __shfl_sync(kFull, sl, g * 8);
                 if (log && ok && sl < lcap) {
                     if (c == 0) lids[sl] = ent.id;

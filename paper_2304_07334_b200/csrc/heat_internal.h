@@ -66,7 +66,8 @@ constexpr int kPersistSlots = 8;  // log slots / accumulation buffers (lag <= 7)
 constexpr int kPersistMaxWorld = 32;  // one lane per rank in the device checks
 // per-step local state words (PersistRank::state, [kStepWords][nsteps])
 // (kRows: rows the step touched = its accumulation buffer's slots in use)
-enum StepWord { kDone = 0, kAccClaim, kAccDone, kCvtClaim, kCvtDone, kFin, kRows, kStepWords };
+// (kWritten: item rows this rank's pairs of the step wrote, owned or logged)
+enum StepWord { kDone = 0, kAccClaim, kAccDone, kCvtClaim, kCvtDone, kFin, kRows, kWritten, kStepWords };
 // entries (peer phase) / rows (convert phase) per claim of the apply work
 constexpr int kApplyChunk = 16;
 struct PersistRank {
@@ -82,9 +83,12 @@ struct PersistRank {
     float *log_rows[kPersistSlots];
     const int32_t *const *pids[kPersistSlots];  // per slot: device table [world] of every rank's ids
     const float *const *prows[kPersistSlots];
+    float *const *t_tab;                  // [world]: every rank's T replica (the owner's convert writes them all)
     unsigned long long *const *mbox_tab;  // [world]: every rank's mailbox
     unsigned long long *const *rel_tab;   // [world]: every rank's released words
-    const unsigned long long *mbox;       // own mailbox [2][mbox_steps][world]
+    // own mailbox [2][mbox_steps][world]: word (tag & 0xffff) << 48 | written
+    // << 24 | logged of rank q's step s (24-bit counts)
+    const unsigned long long *mbox;
     const unsigned long long *rel;        // own released words [world]
     // per accumulation buffer b = global step % lag (steps in flight never
     // share one): 2^-40 fixed-point sums [t_rows * K], each row's touched flag

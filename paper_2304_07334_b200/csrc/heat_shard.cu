@@ -161,6 +161,15 @@ struct heat_shard {
     unsigned long long *pstate = nullptr, *pcnt = nullptr, *pclaim = nullptr;
     int64_t pstate_steps = 0;
     heat::PersistRank *pctx = nullptr;  // device contexts (a loopback group's live in rank 0's)
+    // every rank's T replica (the owners' converts store into all of them):
+    // device table, and per peer the IPC mapping in use (handle, offset, base)
+    float **t_tab = nullptr;
+    struct TMap {
+        cudaIpcMemHandle_t handle;
+        int64_t offset = -1;
+        void *base = nullptr;
+    };
+    std::vector<TMap> tmaps;
     int pctx_n = 0;
     // accumulation buffers of the persistent epoch (one per step in flight)
     long long *pacc[heat::kSlots] = {};
@@ -563,6 +572,64 @@ static bool ensure_mailbox(heat_shard *h, ShardErr &er, int64_t nsteps) {
                    "released table");
 }
 
+// base of the device allocation holding p (driver API, resolved from the
+// libcuda torch loaded: an IPC handle names a whole cudaMalloc block)
+static bool alloc_base(const void *p, void **base) {
+    using Fn = int (*)(unsigned long long *, size_t *, unsigned long long);
+    static Fn fn = [] {
+        void *lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib) lib = dlopen("libcuda.so.1", RTLD_NOW);
+        return lib ? (Fn)dlsym(lib, "cuMemGetAddressRange_v2") : (Fn) nullptr;
+    }();
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (!fn || fn(&b, &sz, (unsigned long long)(uintptr_t)p) != 0) return false;
+    *base = (void *)(uintptr_t)b;
+    return true;
+}
+
+// every rank's T replica into h->t_tab: plain pointers in a loopback group
+// (filled by the caller), CUDA IPC mappings between processes, reopened only
+// when a peer's allocation changes (collective at world > 1)
+static bool map_replicas(heat_shard *h, ShardErr &er, float *T) {
+    const int W = h->world;
+    if (!h->t_tab && !er.cuda(cudaMalloc((void **)&h->t_tab, kMaxWorld * sizeof(float *)), "replica table"))
+        return false;
+    std::vector<float *> tt(W, nullptr);
+    tt[h->rank] = T;
+    if (W > 1 && !h->loopback) {
+        void *base = nullptr;
+        if (!alloc_base(T, &base)) return er.invalid("cannot resolve the allocation of T for CUDA IPC");
+        constexpr int64_t hw = sizeof(cudaIpcMemHandle_t) / sizeof(int64_t);
+        std::vector<int64_t> mine(hw + 1), all(W * (hw + 1));
+        cudaIpcMemHandle_t hd;
+        if (!er.cuda(cudaIpcGetMemHandle(&hd, base), "ipc handle (T)")) return false;
+        memcpy(mine.data(), &hd, sizeof(hd));
+        mine[hw] = (int64_t)((const char *)T - (const char *)base);
+        if (!host_all_gather(h, er, mine.data(), hw + 1, all.data())) return false;
+        h->tmaps.resize(W);
+        for (int q = 0; q < W; ++q) {
+            if (q == h->rank) continue;
+            auto &m = h->tmaps[q];
+            const int64_t *w = &all[(int64_t)q * (hw + 1)];
+            cudaIpcMemHandle_t qh;
+            memcpy(&qh, w, sizeof(qh));
+            if (!m.base || m.offset != w[hw] || memcmp(&m.handle, &qh, sizeof(qh)) != 0) {
+                if (m.base) cudaIpcCloseMemHandle(m.base);
+                m.base = nullptr;
+                if (!er.cuda(cudaIpcOpenMemHandle(&m.base, qh, cudaIpcMemLazyEnablePeerAccess),
+                             "map a peer's T"))
+                    return false;
+                m.handle = qh;
+                m.offset = w[hw];
+            }
+            tt[q] = reinterpret_cast<float *>((char *)m.base + m.offset);
+        }
+    }
+    return er.cuda(cudaMemcpy(h->t_tab, tt.data(), W * sizeof(float *), cudaMemcpyHostToDevice),
+                   "replica table");
+}
+
 // local per-epoch state of the persistent epoch, `nctx` device contexts
 static bool ensure_persist_state(heat_shard *h, ShardErr &er, int64_t nsteps, int nctx,
                                  int64_t t_rows, int64_t dim, int nb) {
@@ -724,6 +791,9 @@ int heat_shard_destroy(heat_shard *h) {
     for (void *q : h->opened_mbox) cudaIpcCloseMemHandle(q);
     cudaFree(h->mbox); cudaFree(h->rel); cudaFree(h->mbox_tab); cudaFree(h->rel_tab);
     cudaFree(h->pstate); cudaFree(h->pcnt); cudaFree(h->pclaim); cudaFree(h->pctx);
+    for (auto &m : h->tmaps)
+        if (m.base) cudaIpcCloseMemHandle(m.base);
+    cudaFree(h->t_tab);
     for (int k = 0; k < kSlots; ++k) {
         cudaFree(h->pacc[k]); cudaFree(h->pflags[k]); cudaFree(h->ptouched[k]);
     }
@@ -1037,6 +1107,7 @@ struct EpochRun {
         // N = 1), HEAT_SHARD_PERSIST=2 forces the persistent epoch there too
         if (K != 128 && !(K == 64 && h->persist_force)) return false;
         if (!p->use_cosine || (p->flags & 1)) return false;
+        if (cap >= (1 << 24)) return false;  // the mailbox words carry 24-bit counts
         return ((uintptr_t)S % 16 == 0) && ((uintptr_t)T % 16 == 0);
     }
 
@@ -1044,6 +1115,7 @@ struct EpochRun {
     // a loopback group)
     bool persist_prepare() {
         if (!ensure_mailbox(h, er, nsteps)) return false;
+        if (!map_replicas(h, er, T)) return false;
         if (!ensure_persist_state(h, er, nsteps, group ? W : 1, t_rows, K, lag)) return false;
         if (nsteps + 1 > h->bounds_cap) {
             cudaDeviceSynchronize();
@@ -1084,6 +1156,7 @@ struct EpochRun {
             c.prows[k] = h->slot[k].prows;
         }
         c.mbox_tab = h->mbox_tab;
+        c.t_tab = h->t_tab;
         c.rel_tab = h->rel_tab;
         c.mbox = h->mbox;
         c.rel = h->rel;
@@ -1324,17 +1397,20 @@ int heat_shard_epoch_loopback(heat_shard **hs, int32_t world, const heat_shard_r
     if (persist) {
         for (auto &r : runs)
             if (!r.persist_prepare()) return r.er.rc;
-        std::vector<void *> mt(world), rt(world);
+        std::vector<void *> mt(world), rt(world), tt(world);
         for (int q = 0; q < world; ++q) {
             mt[q] = hs[q]->mbox;
             rt[q] = hs[q]->rel;
+            tt[q] = runs[q].T;
         }
         std::vector<PersistRank> cx(world);
         for (int r = 0; r < world; ++r) {
             if (!runs[r].er.cuda(cudaMemcpy(hs[r]->mbox_tab, mt.data(), world * sizeof(void *),
                                             cudaMemcpyHostToDevice), "mailbox table") ||
                 !runs[r].er.cuda(cudaMemcpy(hs[r]->rel_tab, rt.data(), world * sizeof(void *),
-                                            cudaMemcpyHostToDevice), "released table"))
+                                            cudaMemcpyHostToDevice), "released table") ||
+                !runs[r].er.cuda(cudaMemcpy(hs[r]->t_tab, tt.data(), world * sizeof(void *),
+                                            cudaMemcpyHostToDevice), "replica table"))
                 return runs[r].er.rc;
             cx[r] = runs[r].persist_ctx();
         }
