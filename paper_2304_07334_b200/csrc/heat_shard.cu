@@ -553,16 +553,29 @@ static bool ensure_mailbox(heat_shard *h, ShardErr &er, int64_t nsteps) {
         memcpy(&mine[0], &a, sizeof(a));
         memcpy(&mine[hw], &b, sizeof(b));
         if (!host_all_gather(h, er, mine.data(), 2 * hw, all.data())) return false;
-        for (int q = 0; q < W; ++q) {
+        int64_t mapped = 1;
+        for (int q = 0; q < W && mapped; ++q) {
             if (q == h->rank) continue;
             memcpy(&a, &all[(int64_t)q * 2 * hw], sizeof(a));
             memcpy(&b, &all[(int64_t)q * 2 * hw + hw], sizeof(b));
-            if (!er.cuda(cudaIpcOpenMemHandle(&mt[q], a, cudaIpcMemLazyEnablePeerAccess), "map mailbox"))
-                return false;
+            if (cudaIpcOpenMemHandle(&mt[q], a, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                mapped = 0;
+                break;
+            }
             h->opened_mbox.push_back(mt[q]);
-            if (!er.cuda(cudaIpcOpenMemHandle(&rt[q], b, cudaIpcMemLazyEnablePeerAccess), "map released"))
-                return false;
+            if (cudaIpcOpenMemHandle(&rt[q], b, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                mapped = 0;
+                break;
+            }
             h->opened_mbox.push_back(rt[q]);
+        }
+        cudaGetLastError();
+        // collective: the persistent epoch only if every rank mapped every peer
+        std::vector<int64_t> all_mapped(W);
+        if (!host_all_gather(h, er, &mapped, 1, all_mapped.data())) return false;
+        if (*std::min_element(all_mapped.begin(), all_mapped.end()) == 0) {
+            h->persist = false;  // every rank: stream-ordered steps from now on
+            return true;
         }
     }
     // (a loopback group fills its tables with every rank's buffers itself)
@@ -598,32 +611,48 @@ static bool map_replicas(heat_shard *h, ShardErr &er, float *T) {
     std::vector<float *> tt(W, nullptr);
     tt[h->rank] = T;
     if (W > 1 && !h->loopback) {
-        void *base = nullptr;
-        if (!alloc_base(T, &base)) return er.invalid("cannot resolve the allocation of T for CUDA IPC");
+        // (handle, offset, ok) per rank; every rank takes part in both
+        // collectives whatever happens locally, and all fall back together
         constexpr int64_t hw = sizeof(cudaIpcMemHandle_t) / sizeof(int64_t);
-        std::vector<int64_t> mine(hw + 1), all(W * (hw + 1));
+        std::vector<int64_t> mine(hw + 2, 0), all(W * (hw + 2));
+        void *base = nullptr;
         cudaIpcMemHandle_t hd;
-        if (!er.cuda(cudaIpcGetMemHandle(&hd, base), "ipc handle (T)")) return false;
-        memcpy(mine.data(), &hd, sizeof(hd));
-        mine[hw] = (int64_t)((const char *)T - (const char *)base);
-        if (!host_all_gather(h, er, mine.data(), hw + 1, all.data())) return false;
+        if (alloc_base(T, &base) && cudaIpcGetMemHandle(&hd, base) == cudaSuccess) {
+            memcpy(mine.data(), &hd, sizeof(hd));
+            mine[hw] = (int64_t)((const char *)T - (const char *)base);
+            mine[hw + 1] = 1;
+        }
+        cudaGetLastError();
+        if (!host_all_gather(h, er, mine.data(), hw + 2, all.data())) return false;
+        int64_t mapped = 1;
+        for (int q = 0; q < W; ++q)
+            if (all[(int64_t)q * (hw + 2) + hw + 1] == 0) mapped = 0;
         h->tmaps.resize(W);
-        for (int q = 0; q < W; ++q) {
+        for (int q = 0; q < W && mapped; ++q) {
             if (q == h->rank) continue;
             auto &m = h->tmaps[q];
-            const int64_t *w = &all[(int64_t)q * (hw + 1)];
+            const int64_t *w = &all[(int64_t)q * (hw + 2)];
             cudaIpcMemHandle_t qh;
             memcpy(&qh, w, sizeof(qh));
             if (!m.base || m.offset != w[hw] || memcmp(&m.handle, &qh, sizeof(qh)) != 0) {
                 if (m.base) cudaIpcCloseMemHandle(m.base);
                 m.base = nullptr;
-                if (!er.cuda(cudaIpcOpenMemHandle(&m.base, qh, cudaIpcMemLazyEnablePeerAccess),
-                             "map a peer's T"))
-                    return false;
+                if (cudaIpcOpenMemHandle(&m.base, qh, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    m.base = nullptr;
+                    mapped = 0;
+                    break;
+                }
                 m.handle = qh;
                 m.offset = w[hw];
             }
             tt[q] = reinterpret_cast<float *>((char *)m.base + m.offset);
+        }
+        cudaGetLastError();
+        std::vector<int64_t> all_mapped(W);
+        if (!host_all_gather(h, er, &mapped, 1, all_mapped.data())) return false;
+        if (*std::min_element(all_mapped.begin(), all_mapped.end()) == 0) {
+            h->persist = false;  // every rank: stream-ordered steps from now on
+            return true;
         }
     }
     return er.cuda(cudaMemcpy(h->t_tab, tt.data(), W * sizeof(float *), cudaMemcpyHostToDevice),
@@ -1113,9 +1142,13 @@ struct EpochRun {
 
     // per-rank buffers and the host context (tables filled by the caller for
     // a loopback group)
+    // false: an error (er.rc set); true with h->persist cleared: the ranks
+    // agreed to fall back to the stream-ordered steps (a peer mapping failed)
     bool persist_prepare() {
         if (!ensure_mailbox(h, er, nsteps)) return false;
+        if (!h->persist) return true;
         if (!map_replicas(h, er, T)) return false;
+        if (!h->persist) return true;
         if (!ensure_persist_state(h, er, nsteps, group ? W : 1, t_rows, K, lag)) return false;
         if (nsteps + 1 > h->bounds_cap) {
             cudaDeviceSynchronize();
@@ -1288,8 +1321,7 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         }
     }
     if (run.setup(cap) != HEAT_OK) return run.er.rc;
-    if (run.persist_eligible()) {
-        if (!run.persist_prepare()) return run.er.rc;
+    if (run.persist_eligible() && run.persist_prepare() && h->persist) {
         const PersistRank c = run.persist_ctx();
         const cudaError_t e = launch_shard_persist(run.persist_args(), &c, h->pctx, 1, run.caller);
         if (e == cudaSuccess) {
@@ -1305,6 +1337,7 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
         }
         cudaGetLastError();  // no persistent kernel for these parameters: stream-ordered steps
     }
+    if (run.er.rc != HEAT_OK) return run.er.rc;
     run.run_single();
     return run.finish(stats);
 }
