@@ -152,6 +152,52 @@ def exchange_deltas(ids: torch.Tensor, rows: torch.Tensor, count, group=None,
     return all_ids, all_rows, valid
 
 
+FIX_SCALE = 2.0 ** 40  # the fixed point of every order-free apply (heat_shard.cu)
+
+
+def owner_exchange(T: torch.Tensor, ids: torch.Tensor, rows: torch.Tensor, count,
+                   group=None) -> int:
+    """One step of the persistent epoch's owner-computes exchange
+    (csrc/heat_hogwild_stream.cu MODE 2/3), as collectives — the mirror the
+    multi-process CPU tests run.  Item row id belongs to rank id % G.  The
+    logged entries are all-gathered (the kernel's owners pull only their
+    partition from the peers' logs; the mirror filters), each owner sums the
+    entries of ITS rows in 2^-40 fixed point (integer adds: order-free) and
+    converts each touched row once, T[id] += float(sum); the owners' new rows
+    are then all-gathered into every replica, so every replica holds the one
+    value its owner computed.  Returns the entries this rank applied."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    all_ids, all_rows, valid = exchange_deltas(ids, rows, count, group)
+    K = T.shape[1]
+    mine = valid & (all_ids.to(torch.int64) % world == rank) if all_ids.numel() else valid
+    mids = all_ids[mine].to(torch.int64)
+    acc = torch.zeros((T.shape[0], K), dtype=torch.int64, device=T.device)
+    if mids.numel():
+        fixed = torch.round(all_rows[mine].to(torch.float64) * FIX_SCALE).to(torch.int64)
+        acc.index_add_(0, mids, fixed)
+    touched = torch.unique(mids)
+    if touched.numel():
+        T[touched] += (acc[touched].to(torch.float64) / FIX_SCALE).to(torch.float32)
+    # the owners' new rows into every replica (padded all-gather)
+    n = torch.tensor([touched.numel()], dtype=torch.int64, device=T.device)
+    ns = torch.empty(world, dtype=torch.int64, device=T.device)
+    _all_gather_flat(ns, n, group)
+    nmax = int(ns.max())
+    if nmax:
+        send_ids = torch.full((nmax,), -1, dtype=torch.int64, device=T.device)
+        send_rows = torch.zeros((nmax, K), dtype=T.dtype, device=T.device)
+        send_ids[:touched.numel()] = touched
+        send_rows[:touched.numel()] = T[touched]
+        g_ids = torch.empty(world * nmax, dtype=torch.int64, device=T.device)
+        g_rows = torch.empty((world * nmax, K), dtype=T.dtype, device=T.device)
+        _all_gather_flat(g_ids, send_ids, group)
+        _all_gather_flat(g_rows, send_rows, group)
+        keep = g_ids >= 0
+        T[g_ids[keep]] = g_rows[keep]
+    return int(mids.numel())
+
+
 @dataclass
 class StepStats:
     entries: int

@@ -281,6 +281,56 @@ def test_gloo_world2_delta_exchange_keeps_replicas_identical():
     assert np.allclose(T0, want, atol=1e-6)
 
 
+def _owner_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2304_07334_b200.parallel import owner_exchange
+    K, rows_n = 4, 9
+    T = torch.from_numpy((np.random.default_rng(7).standard_normal((rows_n, K)) * 0.1)
+                         .astype(np.float32))  # the same initial replica everywhere
+    logs = []
+    for step in range(3):
+        rng = np.random.default_rng(1000 * step + 100 + rank)
+        n = [5, 11, 0][(rank + step) % 3]  # ragged logs, an empty one
+        cap = 12
+        ids = torch.zeros(cap, dtype=torch.int32)
+        rows = torch.zeros((cap, K), dtype=torch.float32)
+        ids[:n] = torch.from_numpy(rng.integers(0, rows_n, n).astype(np.int32))
+        rows[:n] = torch.from_numpy((rng.standard_normal((n, K)) * 1e-3).astype(np.float32))
+        owner_exchange(T, ids, rows, n)
+        logs.append((ids[:n].numpy(), rows[:n].numpy()))
+    out[rank] = (T.numpy().copy(), logs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_owner_exchange_matches_every_rank_applying_everything():
+    """The persistent epoch's owner-computes exchange (row id owned by rank
+    id % G, which alone sums its rows' entries in fixed point and stores the
+    new rows into every replica) against applying every rank's log on every
+    rank with the same fixed point: bit-identical replicas, bit-identical to
+    the all-apply result, over three ragged steps (one log empty)."""
+    world = 2
+    port = _free_port()
+    with mp.Manager() as man:
+        out = man.dict()
+        mp.spawn(_owner_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    T0, T1 = res[0][0], res[1][0]
+    assert T0.tobytes() == T1.tobytes()
+    want = (np.random.default_rng(7).standard_normal((9, 4)) * 0.1).astype(np.float32)
+    for step in range(3):  # every rank applies every log: per row, one fixed-point sum
+        acc = np.zeros((9, 4), dtype=np.int64)
+        hit = np.zeros(9, dtype=bool)
+        for r in range(world):
+            ids, rows = res[r][1][step]
+            for j in range(len(ids)):
+                acc[ids[j]] += np.round(rows[j].astype(np.float64) * 2.0 ** 40).astype(np.int64)
+                hit[ids[j]] = True
+        want[hit] += (acc[hit].astype(np.float64) / 2.0 ** 40).astype(np.float32)
+    assert T0.tobytes() == want.tobytes()
+
+
 def test_native_epoch_shuffle_is_numpy_bit_identical():
     import time
     from paper_2304_07334_b200.dataset import epoch_pairs_numpy
