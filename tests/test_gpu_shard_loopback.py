@@ -251,3 +251,39 @@ def test_default_mode_by_dim(torch_cuda, monkeypatch, K, launches_one):
     if not launches_one:
         assert st.launches == 3 * st.steps
     tr.close()
+
+
+@pytest.mark.parametrize("lag", ["1", "3"])
+def test_persistent_epoch_with_empty_steps(torch_cuda, monkeypatch, lag):
+    """Steps in which a rank has no pairs at all (its log is published empty
+    at kernel start) and steps with nothing to apply: the first half of the
+    epoch only holds rank 0's users.  Every pair is trained once, the
+    replicas agree bit for bit, and at one pair in flight with lag 1 the
+    world-2 epoch equals the world-1 epoch bit for bit."""
+    from paper_2304_07334_b200.dataset import epoch_pairs
+    from paper_2304_07334_b200.device import DeviceModel
+    from paper_2304_07334_b200.parallel import LoopbackShardGroup, NativeShardTrainer
+    from paper_2304_07334_b200.rng import shuffle_seed
+    monkeypatch.setenv("HEAT_SHARD_LAG", lag)
+    monkeypatch.setenv("HEAT_SHARD_GRAPH", "0")
+    train, S, T = _setup(128)
+    u, i = epoch_pairs(train, shuffle_seed(0, 0))
+    order = np.argsort(u % 2, kind="stable")  # rank 0's users (even) first
+    u, i = u[order][:4000], i[order][:4000]
+    window = 1 if lag == "1" else 0
+    grp = LoopbackShardGroup([DeviceModel(S, T) for _ in range(2)])
+    for m in grp.models:
+        m.counters.reset()
+    st = grp.train_epoch(u, i, _params(grp.models[0], 0, window), 256)
+    assert sum(m.counters.read().pairs for m in grp.models) == len(u)
+    assert st[0].launches == 1 and st[0].steps > 4
+    T0 = grp.models[0].T.cpu().numpy()
+    assert grp.models[1].T.cpu().numpy().tobytes() == T0.tobytes()
+    if lag == "1":
+        ref = DeviceModel(S, T)
+        one = NativeShardTrainer(ref, 1, 0)
+        ref.counters.reset()
+        one.train_epoch(u, i, _params(ref, 0, 1), 256)
+        assert T0.tobytes() == ref.T.cpu().numpy().tobytes()
+        one.close()
+    grp.close()
