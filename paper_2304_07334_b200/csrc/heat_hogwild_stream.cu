@@ -489,7 +489,11 @@ __device__ __forceinline__ void persist_init(const PersistRank *ctx, int nctx, i
 // 2 = persistent sharded epoch of one rank (tables and pairs in `a`, the
 // rank's exchange state in ctx[0]), 3 = persistent epoch of a loopback group
 // (ctx: the ranks; block b serves rank b % nctx)
-template <int K, int MINB, int MODE>
+// PAIR2 (default): two rounds share one transposed butterfly (8 quantities
+// over the row's 8 lanes: 8 shuffles instead of 10, and half the dependent
+// shuffle depth per round — the per-round chain bounds this kernel; c4
+// 33.5-33.8 M vs 31.9 M samples/s one round at a time)
+template <int K, int MINB, int MODE, bool PAIR2 = true>
 __global__ void __launch_bounds__(32, MINB)
     hogwild_stream(HogwildArgs a, FastMod fm, int snap_cap, float band_lo,
                    unsigned long long *claim, const PersistRank *__restrict__ ctx, int nctx,
@@ -734,6 +738,7 @@ __global__ void __launch_bounds__(32, MINB)
         const double ss = seq_dot<K>(urow, urow);
         const bool decay_all = a.l2 != 0.f;
         int cnt = 0;  // rows recorded for writing (same value in every lane)
+        int32_t nidsA0 = 0, nidsA1 = 0, nidsB0 = 0, nidsB1 = 0;  // (PAIR2)
 
         // one round: FFMA2 partials of its 8 rows, the buffer refilled two
         // rounds ahead as soon as they are consumed, then the reduction and
@@ -803,16 +808,91 @@ __global__ void __launch_bounds__(32, MINB)
             cnt += __popc(mrec);
         };
 
+        // PAIR2: rounds rd (buffer 0) and rd + 1 (buffer 1) reduced together
+        auto round2 = [&](int rd, bool refill) {
+            float q[8];  // q[4 rb + 2 x + t]: t 0 = tt, 1 = st; rb 0 = round rd, 1 = rd + 1
+#pragma unroll
+            for (int rb = 0; rb < 2; ++rb) {
+                int32_t nids[2];
+                if (refill) round_ids(rd + rb + 2, nids);
+                float2 tl[2], th[2], sl[2], sh[2];
+#pragma unroll
+                for (int x = 0; x < 2; ++x) tl[x] = th[x] = sl[x] = sh[x] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    const float4 w = *reinterpret_cast<const float4 *>(urow + 32 * j + 4 * c);
+#pragma unroll
+                    for (int x = 0; x < 2; ++x) {
+                        const float2 vlo = make_float2(R[rb][x][j].x, R[rb][x][j].y);
+                        const float2 vhi = make_float2(R[rb][x][j].z, R[rb][x][j].w);
+                        tl[x] = __ffma2_rn(vlo, vlo, tl[x]);
+                        th[x] = __ffma2_rn(vhi, vhi, th[x]);
+                        sl[x] = __ffma2_rn(make_float2(w.x, w.y), vlo, sl[x]);
+                        sh[x] = __ffma2_rn(make_float2(w.z, w.w), vhi, sh[x]);
+                    }
+                }
+                // the ids leave with the buffer: keep them for the recording
+                if (rb == 0) {
+                    nidsA0 = rid[0][0];
+                    nidsA1 = rid[0][1];
+                } else {
+                    nidsB0 = rid[1][0];
+                    nidsB1 = rid[1][1];
+                }
+                if (refill) load(rb, nids, opaque_zero(th[1].x) + opaque_zero(sh[1].y));
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    const float2 t2 = __fadd2_rn(tl[x], th[x]);
+                    const float2 s2 = __fadd2_rn(sl[x], sh[x]);
+                    q[4 * rb + 2 * x] = t2.x + t2.y;
+                    q[4 * rb + 2 * x + 1] = s2.x + s2.y;
+                }
+            }
+            // transposed butterfly: afterwards lane c holds quantity c
+            const bool b2 = (c & 4) != 0, b1 = (c & 2) != 0, b0 = (c & 1) != 0;
+            float k[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                k[i] = (b2 ? q[4 + i] : q[i]) + __shfl_xor_sync(kFull, b2 ? q[i] : q[4 + i], 4);
+            float h0 = (b1 ? k[2] : k[0]) + __shfl_xor_sync(kFull, b1 ? k[0] : k[2], 2);
+            float h1 = (b1 ? k[3] : k[1]) + __shfl_xor_sync(kFull, b1 ? k[1] : k[3], 2);
+            const float mq = (b0 ? h1 : h0) + __shfl_xor_sync(kFull, b0 ? h0 : h1, 1);
+            const float o = __shfl_xor_sync(kFull, mq, 1);
+            const float ttf = b0 ? o : mq, stf = b0 ? mq : o;
+            // lanes with even c screen row (round rd + (c >> 2), group (c >> 1) & 1, slot g)
+            const int rb = b2 ? 1 : 0, x = b1 ? 1 : 0;
+            const int r = 8 * (rd + rb) + 4 * x + g;
+            const float sim32 = stf * rss * rsqrt_approx(ttf);
+            const bool valid = r <= N;
+            const bool band = valid & (!screen | (r == 0) | !(ttf > 1e-30f) | (sim32 > band_lo));
+            const bool rec = band | (valid & decay_all);
+            const bool me = rec & !b0;
+            const unsigned mrec = __ballot_sync(kFull, me);
+            if (me) {
+                const int32_t id = rb ? (x ? nidsB1 : nidsB0) : (x ? nidsA1 : nidsA0);
+                const int idx = cnt + __popc(mrec & ((1u << lane) - 1u));
+                recs[idx] = make_int2(id, band ? (r == 0 ? 3 : 1) : 0);
+            }
+            cnt += __popc(mrec);
+        };
+
 #pragma unroll 1
         for (int it = 0; it < niter; ++it) {
             const int rd = 4 * it;
             const bool more = it + 1 < niter;
-            round(0, rd, true);
-            round(1, rd + 1, true);
-            rstate += 32ull * kGamma;  // rounds rd+4, rd+5 need the next block
-            idv = draw(it + 1);
-            round(0, rd + 2, more);
-            round(1, rd + 3, more);
+            if constexpr (PAIR2) {
+                round2(rd, true);
+                rstate += 32ull * kGamma;
+                idv = draw(it + 1);
+                round2(rd + 2, more);
+            } else {
+                round(0, rd, true);
+                round(1, rd + 1, true);
+                rstate += 32ull * kGamma;  // rounds rd+4, rd+5 need the next block
+                idv = draw(it + 1);
+                round(0, rd + 2, more);
+                round(1, rd + 3, more);
+            }
         }
 
         // resolve: re-read every recorded row into its snapshot slot (shared
@@ -1019,7 +1099,16 @@ template <int K, int MINB>
 static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
     const int snap_cap = K <= 64 ? 16 : 8;
     const size_t smem = K * sizeof(float) + (size_t)snap_cap * K * sizeof(float);
-    auto kern = a.range_dev ? hogwild_stream<K, MINB, 1> : hogwild_stream<K, MINB, 0>;
+    static const bool pair2 = [] {  // HEAT_STREAM_PAIR2=0: one round at a time (A/B)
+        const char *e = getenv("HEAT_STREAM_PAIR2");
+        return e ? atoi(e) != 0 : true;
+    }();
+    // DELTA launches (the stream-ordered shard steps) keep the persistent
+    // epoch's one-round order, so the two runtimes record rows, and sum the
+    // user gradient, in the same order (bit-identical at one pair in flight)
+    auto kern = a.range_dev              ? hogwild_stream<K, MINB, 1, false>
+                : pair2 && !a.delta_ids ? hogwild_stream<K, MINB, 0, true>
+                                        : hogwild_stream<K, MINB, 0, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
     if (e != cudaSuccess) return e;
@@ -1060,7 +1149,9 @@ static cudaError_t launch_persist_k(const HogwildArgs &a, const PersistRank *ctx
                                     PersistRank *ctx_dev, int nctx, cudaStream_t st) {
     const int snap_cap = K <= 64 ? 16 : 8;
     const size_t smem = K * sizeof(float) + (size_t)snap_cap * K * sizeof(float);
-    auto kern = nctx == 1 ? hogwild_stream<K, MINB, 2> : hogwild_stream<K, MINB, 3>;
+    // (one round at a time: with the pair-boundary state machine, PAIR2 spills
+    // in the round loop of this mode)
+    auto kern = nctx == 1 ? hogwild_stream<K, MINB, 2, false> : hogwild_stream<K, MINB, 3, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
     if (e != cudaSuccess) return e;
