@@ -166,11 +166,19 @@ __device__ __forceinline__ P *shfl_ptr(P *p, int src) {
         __shfl_sync(kFull, (unsigned long long)reinterpret_cast<uintptr_t>(p), src));
 }
 // accumulator traffic with an evict-first L2 policy, so it does not displace
-// the tables' evict-last lines (HEAT_PERSIST_ACC_EF=0: default policy)
+// the tables' evict-last lines (HEAT_PERSIST_ACC_EF=0: evict-normal)
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t acc_policy(const PersistRank &R) {
+    return R.acc_ef ? policy_evict_first() : policy_evict_normal();
 }
 __device__ __forceinline__ void red_u64_ef(unsigned long long *p, unsigned long long v, uint64_t pol) {
     asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
@@ -250,18 +258,41 @@ __device__ __forceinline__ void persist_publish(const PersistRank &R, long long 
 }
 
 // one logged row (this lane's columns 32j + 4c .. +3) into buffer b, when
-// `ok` (all lanes call it): the sums are indexed by row id, so the adds never
-// wait on anything; the row's first adder of the step (its flag word) appends
-// it to the step's row list, which the convert walks
+// `ok` (all lanes of the warp call it, each 8-lane group with its own row).
+// The sums are compact: the row's first adder of the step claims the next
+// entry of the step's row list (its map word goes 0 -> kMapBusy -> entry + 1)
+// and the row's sums live at that entry, so a step's buffer is the rows it
+// touched, contiguous and reused step after step (it stays in L2; sums
+// indexed by row id spread every step over t_rows * K * 8 bytes and went to
+// DRAM: 9 GB of writes per c4 epoch).  A later adder of the same row waits
+// only for the first adder's two atomics.
+constexpr int32_t kMapBusy = -1;
+__device__ __forceinline__ int32_t ld_acquire_gpu_s32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 template <int K>
 __device__ __forceinline__ void persist_accumulate(const PersistRank &R, int b, long long step,
                                                    int32_t id, int c, bool ok,
                                                    const float4 (&d)[K / 32]) {
+    int32_t e = 0;
+    if (ok && c == 0) {
+        int32_t *mw = R.map[b] + id;
+        int32_t v = atomicCAS(mw, 0, kMapBusy);
+        if (v == 0) {
+            e = (int32_t)atomicAdd(R.state + kRows * R.nsteps + step, 1ull);
+            R.touched[b][e] = id;
+            atomicExch(mw, e + 1);  // (the entry's sums start zeroed)
+        } else {
+            while (v == kMapBusy) v = ld_acquire_gpu_s32(mw);
+            e = v - 1;
+        }
+    }
+    e = __shfl_sync(kFull, e, threadIdx.x & ~7);
     if (!ok) return;
-    if (c == 0 && atomicExch(R.map[b] + id, 1) == 0)
-        R.touched[b][atomicAdd(R.state + kRows * R.nsteps + step, 1ull)] = id;
-    unsigned long long *ac = reinterpret_cast<unsigned long long *>(R.acc[b] + (int64_t)id * K + 4 * c);
-    const uint64_t pol = policy_evict_first();
+    unsigned long long *ac = reinterpret_cast<unsigned long long *>(R.acc[b] + (int64_t)e * K + 4 * c);
+    const uint64_t pol = acc_policy(R);
 #pragma unroll
     for (int j = 0; j < K / 32; ++j) {
         red_u64_ef(ac + 32 * j, fix40(d[j].x), pol);
@@ -390,7 +421,7 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
         // rows i0 .. i0 + m - 1 of the step's list
         int32_t myid = 0;
         if (lane < m) myid = __ldcg(R.touched[b] + i0 + lane);
-        const uint64_t pef = policy_evict_first();
+        const uint64_t pef = acc_policy(R);
         for (int hb = 0; hb < m; hb += 8) {
         longlong2 q01[2][V], q23[2][V];
         float4 tv[2][V];
@@ -400,7 +431,7 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
             const int j = hb + 4 * h + g;
             ids[h] = __shfl_sync(kFull, myid, j & 31);
             if (j < m) {
-                const long long *ac = R.acc[b] + (int64_t)ids[h] * K + 4 * c;
+                const long long *ac = R.acc[b] + (i0 + j) * K + 4 * c;
                 const float *tr = R.T + (int64_t)ids[h] * K + 4 * c;
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
@@ -414,7 +445,7 @@ __device__ __forceinline__ int persist_help(const PersistRank &R, int lane) {
         for (int h = 0; h < 2; ++h) {
             const int j = hb + 4 * h + g;
             if (j < m) {
-                long long *ac = R.acc[b] + (int64_t)ids[h] * K + 4 * c;
+                long long *ac = R.acc[b] + (i0 + j) * K + 4 * c;
                 float *tr = R.T + (int64_t)ids[h] * K + 4 * c;
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
@@ -1095,6 +1126,17 @@ __global__ void __launch_bounds__(32, MINB)
     }
 }
 
+// the persistent epoch (and the stream-ordered DELTA launches, which keep its
+// order) reduce two rounds per butterfly as well: c4 sharded at N = 1 28.9 M
+// vs 26.4 M samples/s one round at a time (HEAT_PERSIST_PAIR2=0)
+static bool persist_pair2() {
+    static const bool on = [] {
+        const char *e = getenv("HEAT_PERSIST_PAIR2");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 template <int K, int MINB>
 static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
     const int snap_cap = K <= 64 ? 16 : 8;
@@ -1104,11 +1146,12 @@ static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *w
         return e ? atoi(e) != 0 : true;
     }();
     // DELTA launches (the stream-ordered shard steps) keep the persistent
-    // epoch's one-round order, so the two runtimes record rows, and sum the
-    // user gradient, in the same order (bit-identical at one pair in flight)
-    auto kern = a.range_dev              ? hogwild_stream<K, MINB, 1, false>
-                : pair2 && !a.delta_ids ? hogwild_stream<K, MINB, 0, true>
-                                        : hogwild_stream<K, MINB, 0, false>;
+    // epoch's round order, so the two runtimes record rows, and sum the user
+    // gradient, in the same order (bit-identical at one pair in flight)
+    const bool p2 = a.delta_ids ? persist_pair2() : pair2;
+    auto kern = a.range_dev ? hogwild_stream<K, MINB, 1, false>
+                : p2        ? hogwild_stream<K, MINB, 0, true>
+                            : hogwild_stream<K, MINB, 0, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
     if (e != cudaSuccess) return e;
@@ -1149,9 +1192,9 @@ static cudaError_t launch_persist_k(const HogwildArgs &a, const PersistRank *ctx
                                     PersistRank *ctx_dev, int nctx, cudaStream_t st) {
     const int snap_cap = K <= 64 ? 16 : 8;
     const size_t smem = K * sizeof(float) + (size_t)snap_cap * K * sizeof(float);
-    // (one round at a time: with the pair-boundary state machine, PAIR2 spills
-    // in the round loop of this mode)
-    auto kern = nctx == 1 ? hogwild_stream<K, MINB, 2, false> : hogwild_stream<K, MINB, 3, false>;
+    const bool p2 = persist_pair2();
+    auto kern = nctx == 1 ? (p2 ? hogwild_stream<K, MINB, 2, true> : hogwild_stream<K, MINB, 2, false>)
+                          : (p2 ? hogwild_stream<K, MINB, 3, true> : hogwild_stream<K, MINB, 3, false>);
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
     if (e != cudaSuccess) return e;
@@ -1222,15 +1265,18 @@ void persist_prof_report() {
 cudaError_t launch_shard_persist(const HogwildArgs &a, const PersistRank *ctx_host,
                                  PersistRank *ctx_dev, int nctx, cudaStream_t st) {
     if (!hogwild_stream_supported(a) || nctx < 1) return cudaErrorNotSupported;
-    // resident warps per SM the persistent build is compiled for (12, as the
-    // single-GPU kernel; 10 / 11 / 14 for A/B runs)
-    int warps = 12;
+    // launch bounds the persistent build is compiled for: K = 128 at 10 (the
+    // registers still come out at 168, 12 warps per SM, and the codegen of the
+    // pair loop is better: 28.9 M vs 27.1 M samples/s at 12 on c4), K = 64 at
+    // 12; 8 / 11 / 12 / 14 for A/B runs
+    int warps = a.K == 128 ? 10 : 12;
     if (const char *e = getenv("HEAT_PERSIST_WARPS")) warps = atoi(e) > 0 ? atoi(e) : warps;
     if (a.K == 128) {
         switch (warps) {
-        case 10: return launch_persist_k<128, 10>(a, ctx_host, ctx_dev, nctx, st);
+        case 8: return launch_persist_k<128, 8>(a, ctx_host, ctx_dev, nctx, st);
+        case 11: return launch_persist_k<128, 11>(a, ctx_host, ctx_dev, nctx, st);
         case 12: return launch_persist_k<128, 12>(a, ctx_host, ctx_dev, nctx, st);
-        default: return launch_persist_k<128, 11>(a, ctx_host, ctx_dev, nctx, st);
+        default: return launch_persist_k<128, 10>(a, ctx_host, ctx_dev, nctx, st);
         }
     }
     switch (warps) {
@@ -1253,6 +1299,7 @@ cudaError_t launch_hogwild_stream(const HogwildArgs &a, cudaStream_t st, int *wo
     if (a.K == 128) {
         switch (warps) {
         case 8: return launch_stream_k<128, 8>(a, st, workers_out);
+        case 10: return launch_stream_k<128, 10>(a, st, workers_out);
         case 16: return launch_stream_k<128, 16>(a, st, workers_out);
         default: return launch_stream_k<128, 12>(a, st, workers_out);
         }

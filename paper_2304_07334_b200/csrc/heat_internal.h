@@ -104,6 +104,7 @@ struct PersistRank {
     unsigned tag;              // epoch tag (>= 1) of the mailbox words
     int rank, world, lag, nslots, nblocks;  // nblocks: CTAs serving this rank
     int gmod_lag, gmod_slots;               // gbase % lag, gbase % nslots
+    int acc_ef;                             // accumulator traffic evict-first (else evict-normal)
 };
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);

@@ -1208,6 +1208,11 @@ struct EpochRun {
         c.rank = h->rank;
         c.world = W;
         c.lag = lag;
+        static const int acc_ef = [] {  // HEAT_PERSIST_ACC_EF=0: evict-normal accumulator lines
+            const char *e = getenv("HEAT_PERSIST_ACC_EF");
+            return e ? (atoi(e) != 0 ? 1 : 0) : 1;
+        }();
+        c.acc_ef = acc_ef;
         c.nslots = nslots;
         c.gmod_lag = (int)(h->gstep % (unsigned long long)lag);
         c.gmod_slots = (int)(h->gstep % (unsigned long long)nslots);
