@@ -23,6 +23,8 @@
  *   heat_epoch_pairs       <- dataset.epoch_pairs (host)    dataset.py:146-158
  *   heat_aggregate_users   <- evaluator._aggregated_user_vectors evaluator.py:91-110
  *   heat_train_range(agg)  <- _train_chunk agg_on branch     trainer.py:148-173, 299-331
+ *   heat_phase_collect/_read <- collect_phases cycle counters trainer.py:120-331, 452-457;
+ *                             timing.py:20-53
  *   heat_agg_scratch_bytes <- _ThreadState agg buffers      trainer.py:334-363
  */
 #ifndef HEAT_B200_H
@@ -261,6 +263,21 @@ int heat_epoch_pairs(const int64_t *offsets, int64_t num_users, const int32_t *i
                      uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                      int32_t has_uint32, uint32_t uinteger, int32_t *out_users,
                      int32_t *out_items);
+
+/* Phase profile: the per-phase times of trainer.py's collect_phases
+ * (trainer.py:120-331 cycle counters, timing.py:20-53; PHASE_NAMES order
+ * read_emb, similarity, loss, gradient, update, aggregate).  While on
+ * (heat_phase_collect(1)), heat_train_range runs phase-instrumented kernels
+ * on the current device: EXACT the serial kernel (same bits; its phases are
+ * the reference's, one pair at a time), HOGWILD at dim 64/128 (cosine,
+ * fp32) the register-streamed kernel, whose fused phases are split by where
+ * the time goes.  Other launches add nothing.
+ * heat_phase_read returns seconds per phase averaged over the workers (one
+ * worker = one warp / one CTA, as the reference averages its threads),
+ * converted from clock64 with the workers' own clock/globaltimer ratio, plus
+ * the worker and pair counts; reset != 0 zeroes the sums. */
+int heat_phase_collect(int32_t on);
+int heat_phase_read(double *seconds6, int64_t *workers, int64_t *pairs, int32_t reset);
 
 /* Diagnostics of the parallel deterministic (EXACT) kernel: out[0..2] clock64
  * totals of speculate / commit-token wait / commit, out[3..5] partial

@@ -26,7 +26,8 @@ EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
            "heat_epoch_pairs", "heat_aggregate_users", "heat_agg_scratch_bytes",
            "heat_exact_stats", "heat_nccl_unique_id", "heat_shard_create", "heat_shard_epoch",
            "heat_shard_last_error", "heat_shard_destroy", "heat_shard_create_loopback",
-           "heat_shard_epoch_loopback", "heat_probe_l2_read", "heat_probe_l2_gather", "heat_last_error", "heat_version")
+           "heat_shard_epoch_loopback", "heat_phase_collect", "heat_phase_read",
+           "heat_probe_l2_read", "heat_probe_l2_gather", "heat_last_error", "heat_version")
 
 
 class SgdParams(ctypes.Structure):
@@ -159,6 +160,10 @@ def lib():
     L.heat_probe_l2_read.argtypes = [P, i64, i32, P, P]
     L.heat_probe_l2_gather.restype = ctypes.c_int
     L.heat_probe_l2_gather.argtypes = [P, i64, i32, i32, P, P, P]
+    L.heat_phase_collect.restype = ctypes.c_int
+    L.heat_phase_collect.argtypes = [i32]
+    L.heat_phase_read.restype = ctypes.c_int
+    L.heat_phase_read.argtypes = [P, P, P, i32]
     L.heat_last_error.restype = ctypes.c_char_p
     L.heat_last_error.argtypes = []
     L.heat_version.restype = ctypes.c_int

@@ -309,6 +309,79 @@ int heat_probe_l2_gather(const float *table, int64_t rows, int32_t dim, int32_t 
 
 int heat_version(void) { return 1; }
 
+// ---- phase profile (trainer.py:120-331 collect_phases, timing.py:20-53)
+static std::mutex g_phase_mu;
+static unsigned long long *g_phase = nullptr;
+static int g_phase_dev = -1;
+static bool g_phase_on = false;
+
+}  // extern "C"
+namespace heat {
+unsigned long long *phase_buffer() {
+    std::lock_guard<std::mutex> lk(g_phase_mu);
+    if (!g_phase_on || !g_phase) return nullptr;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev != g_phase_dev) return nullptr;
+    return g_phase;
+}
+}  // namespace heat
+extern "C" {
+
+int heat_phase_collect(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_phase_mu);
+    if (!on) {
+        g_phase_on = false;
+        return HEAT_OK;
+    }
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "phase profile: device");
+    if (g_phase && g_phase_dev != dev) {
+        int cur = dev;
+        cudaSetDevice(g_phase_dev);
+        cudaFree(g_phase);
+        cudaSetDevice(cur);
+        g_phase = nullptr;
+    }
+    if (!g_phase) {
+        e = cudaMalloc(&g_phase, heat::kPhaseWords * sizeof(unsigned long long));
+        if (e != cudaSuccess) return cuda_fail(e, "phase profile: allocation");
+        e = cudaMemset(g_phase, 0, heat::kPhaseWords * sizeof(unsigned long long));
+        if (e != cudaSuccess) return cuda_fail(e, "phase profile: zero");
+        g_phase_dev = dev;
+    }
+    g_phase_on = true;
+    return HEAT_OK;
+}
+
+int heat_phase_read(double *seconds, int64_t *workers, int64_t *pairs, int32_t reset) {
+    if (!seconds) return fail(HEAT_ERR_INVALID, "phase profile: NULL output");
+    std::lock_guard<std::mutex> lk(g_phase_mu);
+    for (int i = 0; i < 6; ++i) seconds[i] = 0.0;
+    if (workers) *workers = 0;
+    if (pairs) *pairs = 0;
+    if (!g_phase) return HEAT_OK;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g_phase_dev) cudaSetDevice(g_phase_dev);
+    unsigned long long v[heat::kPhaseWords];
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(v, g_phase, sizeof(v), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && reset) e = cudaMemset(g_phase, 0, sizeof(v));
+    if (cur != g_phase_dev) cudaSetDevice(cur);
+    if (e != cudaSuccess) return cuda_fail(e, "phase profile: read");
+    // seconds per phase averaged over the workers, as the reference averages
+    // its threads' cycle counts (trainer.py:452-455); clocks -> seconds with
+    // the workers' own clock/globaltimer ratio (timing.py:39-53 calibrates
+    // rdtsc against perf_counter the same way)
+    const double hz = v[7] ? (double)v[6] / ((double)v[7] * 1e-9) : 0.0;
+    if (v[8] && hz > 0.0)
+        for (int i = 0; i < 6; ++i) seconds[i] = (double)v[i] / (double)v[8] / hz;
+    if (workers) *workers = (int64_t)v[8];
+    if (pairs) *pairs = (int64_t)v[9];
+    return HEAT_OK;
+}
+
 /* Diagnostics of the parallel deterministic kernel (not part of the
  * reference interface): clock64 totals [speculate, token wait, commit],
  * [partial recomputes, full recomputes, pairs]; `reset` zeroes them. */
@@ -383,7 +456,10 @@ static int train_range_core(float *S, int64_t s_rows, float *T, int64_t t_rows,
     case HEAT_MODE_EXACT: {
         // speculative in-order-commit kernel (parallel, bit-identical) unless
         // the shape or the aggregator needs the serial one
-        if (!agg && exact_spec_supported(p->dim, p->n_neg) && !getenv("HEAT_EXACT_SERIAL")) {
+        // (a phase profile runs the serial kernel: its phases are the
+        // reference's, one pair at a time; results are the same bits)
+        unsigned long long *ph = phase_buffer();
+        if (!agg && !ph && exact_spec_supported(p->dim, p->n_neg) && !getenv("HEAT_EXACT_SERIAL")) {
             void *sc = scratch ? scratch
                                : get_scratch((size_t)heat_scratch_bytes(p->n_neg, p->dim, s_rows,
                                                                         t_rows), st);
@@ -402,7 +478,7 @@ static int train_range_core(float *S, int64_t s_rows, float *T, int64_t t_rows,
         if (!snap) return fail(HEAT_ERR_CUDA, "exact mode: scratch allocation failed");
         e = launch_exact(S, T, ep_users, ep_items, start, stop, p->dim, p->n_neg, p->use_cosine,
                          p->lr, p->l2, p->mu, p->theta, p->stream_base, t_rows, counters,
-                         (float *)snap, pair_index, agg, st);
+                         (float *)snap, pair_index, agg, st, ph);
         break;
     }
     case HEAT_MODE_HOGWILD:
@@ -424,6 +500,7 @@ static int train_range_core(float *S, int64_t s_rows, float *T, int64_t t_rows,
         a.pair_index = pair_index;
         a.range_dev = range_dev;
         a.s0_dev = s0_dev;
+        if (!range_dev && p->mode == HEAT_MODE_HOGWILD) a.phase = phase_buffer();
         if (agg) {
             if (range_dev) return fail(HEAT_ERR_UNSUPPORTED, "aggregation with a device range");
             void *sc = scratch ? scratch

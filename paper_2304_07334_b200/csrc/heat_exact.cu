@@ -44,12 +44,23 @@ struct ExactSmem {
     int warp_cnt[kExactWarps];
 };
 
+// phase profile (PH, heat_phase_collect): [0, 6) clocks per phase, [6] the
+// last mark, [7] the start clock, [8] the start globaltimer, [9] the clocks
+// thread 0 spent on its column's gradient in the fused gradient/update loop
+__shared__ long long s_xph[10];
+
+// PH: the clocks of the pair's phases (trainer.py:120-331 collect_phases)
+// into `phase`, the phases in the reference's order and extent; the fused
+// gradient + update loop (one column per thread) is split by thread 0's own
+// share of it
+template <bool PH>
 __global__ void __launch_bounds__(kExactThreads, 1)
     exact_kernel(float *__restrict__ S, float *__restrict__ T, const int32_t *__restrict__ users,
                  const int32_t *__restrict__ items, int64_t start, int64_t stop, int K, int N,
                  int cosine, double lr, double l2, double mu, double theta, uint64_t s0,
                  FastMod fm, heat_counters *ctr, float *__restrict__ snap,
-                 const int64_t *__restrict__ pair_index, heat_agg_params ag, int agg_on) {
+                 const int64_t *__restrict__ pair_index, heat_agg_params ag, int agg_on,
+                 unsigned long long *phase) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ExactSmem &sh = *reinterpret_cast<ExactSmem *>(smem_raw);
     double *ubuf = reinterpret_cast<double *>(smem_raw + sizeof(ExactSmem) + 16 -
@@ -67,6 +78,28 @@ __global__ void __launch_bounds__(kExactThreads, 1)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
+    auto gtimer = []() -> long long {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return (long long)t;
+    };
+    if constexpr (PH) {
+        if (tid == 0) {
+            for (int i = 0; i < 6; ++i) s_xph[i] = 0;
+            s_xph[7] = clock64();
+            s_xph[8] = gtimer();
+        }
+    }
+    auto mark = [&](int i) {  // phase i ends here (every thread calls it)
+        if constexpr (PH) {
+            __syncthreads();
+            if (tid == 0) {
+                const long long t = clock64();
+                s_xph[i] += t - s_xph[6];
+                s_xph[6] = t;
+            }
+        }
+    };
     const double inv_n = DDIV(1.0, (double)N);  // trainer.py:113
     const double dneg_w = DMUL(mu, inv_n);      // trainer.py:219
     const double dpos = -1.0;                   // trainer.py:223
@@ -77,6 +110,10 @@ __global__ void __launch_bounds__(kExactThreads, 1)
     const double gamma = ag.gamma;
 
     for (int64_t p = start; p < stop; ++p) {
+        if constexpr (PH) {
+            __syncthreads();
+            if (tid == 0) s_xph[6] = clock64();
+        }
         const int64_t u = users[p];
         const int64_t pos = items[p];
         // ---- read (trainer.py:121-142): S[u] -> f64, T[pos] snapshot, ids
@@ -86,6 +123,7 @@ __global__ void __launch_bounds__(kExactThreads, 1)
         }
         const int64_t pg = pair_index ? pair_index[p] : p;  // RNG key
         for (int j = tid; j < N; j += kExactThreads) nids[j] = neg_id(s0, pg, N, j, fm);
+        mark(0);
         // ---- aggregate forward (trainer.py:150-169): pooled = mean of the
         // first max_history history rows, h = gamma*S[u] + (1-gamma)*pooled.W
         int64_t hb = 0, hist_len = 0;
@@ -107,6 +145,7 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                 for (int k = 0; k < K; ++k) acc = DADD(acc, DMUL(pooled[k], (double)ag.W[k * K + j]));
                 ubuf[j] = DADD(DMUL(gamma, (double)S[u * K + j]), DMUL(DSUB(1.0, gamma), acc));
             }
+            mark(5);
         }
         __syncthreads();
 
@@ -153,6 +192,7 @@ __global__ void __launch_bounds__(kExactThreads, 1)
             if (r == 0) sh.sim_p = sim; else sims[r - 1] = sim;
         }
         __syncthreads();
+        mark(1);
 
         // ---- loss (trainer.py:214-222): ordered list of j with d > 0
         int base = 0;
@@ -183,6 +223,11 @@ __global__ void __launch_bounds__(kExactThreads, 1)
         }
         // negatives with dnegs[j] != 0 (trainer.py:219: dneg = mu*inv_n)
         const int n_upd = dneg_w != 0.0 ? n_loss : 0;
+        mark(2);
+        long long tg0 = 0;
+        if constexpr (PH) {
+            if (tid == 0) tg0 = clock64();
+        }
 
         // ---- gradient + update, thread k owns column k
         const double tt_p = sh.tt_p, st_p = sh.st_p;
@@ -214,6 +259,9 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                     snap[(int64_t)a * K + k] = v;
                     ug = DADD(ug, DMUL(dneg_w, (double)v));
                 }
+            }
+            if constexpr (PH) {
+                if (tid == 0) s_xph[9] = clock64() - tg0;
             }
             // T[pos] (trainer.py:259-271)
             float *tp = T + pos * K + k;
@@ -283,6 +331,16 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                 ugs[k] = ug;
             }
         }
+        if constexpr (PH) {  // the loop: thread 0's gradient share, then the update
+            __syncthreads();
+            if (tid == 0) {
+                const long long t = clock64();
+                const long long gpart = K > 0 ? s_xph[9] : 0;
+                s_xph[3] += gpart;
+                s_xph[4] += t - s_xph[6] - gpart;
+                s_xph[6] = t;
+            }
+        }
         if (agg_on) {
             // ---- aggregate backward (trainer.py:304-328)
             __syncthreads();
@@ -315,8 +373,18 @@ __global__ void __launch_bounds__(kExactThreads, 1)
                     }
                 }
             }
+            mark(5);
         }
         __syncthreads();
+    }
+    if constexpr (PH) {
+        if (tid == 0 && phase) {
+            for (int i = 0; i < 6; ++i) atomicAdd(phase + i, (unsigned long long)s_xph[i]);
+            atomicAdd(phase + 6, (unsigned long long)(clock64() - s_xph[7]));
+            atomicAdd(phase + 7, (unsigned long long)(gtimer() - s_xph[8]));
+            atomicAdd(phase + 8, 1ull);
+            atomicAdd(phase + 9, (unsigned long long)(stop - start));
+        }
     }
     if (agg_on && tid == 0) *ag.counter = agg_ctr;
     // telemetry (order-free integer sums)
@@ -339,16 +407,17 @@ cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t
                          int64_t start, int64_t stop, int K, int N, int cosine, double lr,
                          double l2, double mu, double theta, uint64_t s0, int64_t num_items,
                          heat_counters *ctr, float *snap, const int64_t *pair_index,
-                         const heat_agg_params *agg, cudaStream_t stream) {
+                         const heat_agg_params *agg, cudaStream_t stream,
+                         unsigned long long *phase) {
     size_t smem = exact_smem_bytes(K, N);
-    cudaError_t e = cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = phase ? exact_kernel<true> : exact_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    exact_kernel<<<1, kExactThreads, smem, stream>>>(S, T, users, items, start, stop, K, N,
-                                                     cosine, lr, l2, mu, theta, s0,
-                                                     FastMod::make((uint64_t)num_items), ctr, snap,
-                                                     pair_index, agg ? *agg : heat_agg_params{},
-                                                     agg != nullptr);
+    kern<<<1, kExactThreads, smem, stream>>>(S, T, users, items, start, stop, K, N, cosine, lr,
+                                             l2, mu, theta, s0, FastMod::make((uint64_t)num_items),
+                                             ctr, snap, pair_index,
+                                             agg ? *agg : heat_agg_params{}, agg != nullptr, phase);
     return cudaGetLastError();
 }
 

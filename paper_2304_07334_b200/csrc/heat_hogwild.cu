@@ -41,7 +41,12 @@ __device__ __forceinline__ T shfl_xor_t(T v, int o) { return __shfl_xor_sync(0xf
 // ---------------------------------------------------------------------------
 constexpr int kMaxC = 16;
 
-template <int C>
+// PH: phase profile (heat_phase_collect) of the warp's pairs into a.phase:
+// read_emb = the user row, similarity = each row's read and dots (one
+// statement: the load latency lands here), loss = the margin decisions and
+// hinge, gradient = the flush's row coefficients and deltas, update = its
+// atomics and the user row's
+template <int C, bool PH = false>
 __global__ void __launch_bounds__(kHogThreads)
     hogwild_generic(HogwildArgs a, FastMod fm, int n_workers) {
     __shared__ WriteEntry lists[kHogWarps][kListCap];
@@ -55,8 +60,27 @@ __global__ void __launch_bounds__(kHogThreads)
     const bool dmode = a.delta_ids != nullptr;
     double loss = 0.0;
     long long degen = 0, active = 0, mine = 0;
+    long long ph[6] = {0, 0, 0, 0, 0, 0}, tm = 0;
+    long long c_start = 0, g_start = 0;
+    auto gtimer = []() -> long long {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return (long long)t;
+    };
+    if constexpr (PH) {
+        c_start = clock64();
+        g_start = gtimer();
+    }
+    auto mark = [&](int i) {  // phase i ends here
+        if constexpr (PH) {
+            const long long t = clock64();
+            ph[i] += t - tm;
+            tm = t;
+        }
+    };
 
     for (int64_t p = a.start + gw; p < a.stop; p += n_workers) {
+        if constexpr (PH) tm = clock64();
         ++mine;
         const int64_t u = a.users[p];
         const int64_t pos = a.items[p];
@@ -75,6 +99,7 @@ __global__ void __launch_bounds__(kHogThreads)
         const double ss = ssp;
         const double rs = ss > 0.0 ? sqrt(ss) : 0.0;
         int cnt = 0;
+        mark(0);
 
         // rows of one flush round are all loaded before any update, so a row
         // written twice in a pair uses its pre-pair snapshot both times
@@ -100,6 +125,7 @@ __global__ void __launch_bounds__(kHogThreads)
                     float d[C];
 #pragma unroll
                     for (int c = 0; c < C; ++c) row_apply(co, ur[c], x[j][c], d[c], ug[c]);
+                    mark(3);
                     if (!dmode) {
 #pragma unroll
                         for (int c = 0; c < C; ++c) {
@@ -120,6 +146,7 @@ __global__ void __launch_bounds__(kHogThreads)
                             }
                         }
                     }
+                    mark(4);
                 }
             }
             cnt = 0;
@@ -143,6 +170,7 @@ __global__ void __launch_bounds__(kHogThreads)
                 stp += shfl_xor_t(stp, o);
             }
             const double tt = ttp, st = stp;
+            mark(1);
             bool degenerate = false;
             double sim = st;
             if (a.cosine) {
@@ -169,17 +197,30 @@ __global__ void __launch_bounds__(kHogThreads)
                 write = (w != 0.0 && !(a.cosine && degenerate)) || (w == 0.0 && a.l2 != 0.f);
             }
             if (write) {
+                mark(2);
                 if (cnt == kListCap) flush();
                 if (lane == 0) list[cnt] = WriteEntry{tt, st, w, id, 0};
                 ++cnt;
             }
+            mark(2);
         }
         flush();
         loss += (1.0 - sim_p) + wneg * hinge;
+        mark(2);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const int k = lane + 32 * c;
             if (k < K) atomicAdd(a.S + u * K + k, -a.lr * (ug[c] + a.l2 * ur[c]));
+        }
+        mark(4);
+    }
+    if constexpr (PH) {
+        if (lane == 0 && a.phase) {
+            for (int i = 0; i < 6; ++i) atomicAdd(a.phase + i, (unsigned long long)ph[i]);
+            atomicAdd(a.phase + 6, (unsigned long long)(clock64() - c_start));
+            atomicAdd(a.phase + 7, (unsigned long long)(gtimer() - g_start));
+            atomicAdd(a.phase + 8, 1ull);
+            atomicAdd(a.phase + 9, (unsigned long long)mine);
         }
     }
     if (lane == 0) {
@@ -192,16 +233,16 @@ __global__ void __launch_bounds__(kHogThreads)
 
 template <int C>
 static cudaError_t launch_generic_c(const HogwildArgs &a, cudaStream_t st, int *workers_out) {
+    auto kern = a.phase ? hogwild_generic<C, true> : hogwild_generic<C, false>;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hogwild_generic<C>, kHogThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHogThreads, 0);
     if (per_sm < 1) per_sm = 1;
     int64_t nw = (int64_t)per_sm * kHogWarps * sm_count();
     if (a.window > 0 && a.window < nw) nw = a.window;
     if (a.stop - a.start < nw) nw = a.stop - a.start;
     if (workers_out) *workers_out = (int)nw;
     const int blocks = (int)((nw + kHogWarps - 1) / kHogWarps);
-    hogwild_generic<C><<<blocks, kHogThreads, 0, st>>>(a, FastMod::make((uint64_t)a.num_items),
-                                                       (int)nw);
+    kern<<<blocks, kHogThreads, 0, st>>>(a, FastMod::make((uint64_t)a.num_items), (int)nw);
     return cudaGetLastError();
 }
 
@@ -478,6 +519,10 @@ cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *worke
     const char *impl = getenv("HEAT_HOGWILD_IMPL");
     const bool aligned = ((uintptr_t)a.S % 16 == 0) && ((uintptr_t)a.T % 16 == 0);
     if (getenv("HEAT_FORCE_GENERIC")) impl = "generic";
+    // phase profile: the instrumented kernels only (register-streamed at
+    // dim 64/128, generic otherwise)
+    if (a.phase && !a.delta_ids && !a.range_dev)
+        impl = aligned && (a.K == 64 || a.K == 128) && hogwild_stream_supported(a) ? "wide" : "generic";
     if (aligned && (!impl || impl[0] == 'r' && impl[1] == 'e')) {
         cudaError_t e = launch_hogwild_resident(a, stream, workers_out);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;

@@ -202,6 +202,14 @@ __device__ __forceinline__ unsigned long long fix40(float v) {
 // diagnostics: [8] help calls, [9] calls with nothing to do, [10] clocks in
 // accumulate units, [11] clocks in convert units, [12] accumulate units
 __shared__ long long s_pw[16];
+// phase profile of one warp (PH builds): [0, 6) clocks per phase, [6] the
+// last mark, [7] the start clock, [8] the start globaltimer
+__shared__ long long s_ph[9];
+__device__ __forceinline__ long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (long long)t;
+}
 
 // Watchdog of the device-side waits: a wait longer than ~20 s of clocks
 // records (site, rank, step, block) in g_watchdog and traps, so a protocol
@@ -524,7 +532,14 @@ __device__ __forceinline__ void persist_init(const PersistRank *ctx, int nctx, i
 // over the row's 8 lanes: 8 shuffles instead of 10, and half the dependent
 // shuffle depth per round — the per-round chain bounds this kernel; c4
 // 33.5-33.8 M vs 31.9 M samples/s one round at a time)
-template <int K, int MINB, int MODE, bool PAIR2 = true>
+// PH: phase profile (trainer.py:120-331 collect_phases): clocks of the
+// pair's phases into a.phase.  The phases are fused here, so the marks split
+// them by where the time goes: read_emb = the user row, the pair's ids and
+// the first rounds' loads; similarity = the streaming rounds (the negative
+// rows' reads and their dots, one pass); loss = the resolve (recorded rows
+// re-read, binary64 decisions, hinge); gradient = row coefficients, item
+// deltas and the user gradient; update = the row writes.
+template <int K, int MINB, int MODE, bool PAIR2 = true, bool PH = false>
 __global__ void __launch_bounds__(32, MINB)
     hogwild_stream(HogwildArgs a, FastMod fm, int snap_cap, float band_lo,
                    unsigned long long *claim, const PersistRank *__restrict__ ctx, int nctx,
@@ -539,6 +554,23 @@ __global__ void __launch_bounds__(32, MINB)
     const int lane = threadIdx.x;
     const int g = lane >> 3;  // row slot of a group
     const int c = lane & 7;   // column chunk: columns 32j + 4c .. +3
+    if constexpr (PH) {
+        if (lane == 0) {
+            for (int i = 0; i < 6; ++i) s_ph[i] = 0;
+            s_ph[7] = clock64();
+            s_ph[8] = globaltimer_ns();
+        }
+    }
+    auto mark = [&](int i) {  // phase i ends here
+        if constexpr (PH) {
+            __syncwarp();
+            if (lane == 0) {
+                const long long t = clock64();
+                s_ph[i] += t - s_ph[6];
+                s_ph[6] = t;
+            }
+        }
+    };
     int64_t k_start = a.start, k_stop = a.stop;
     uint64_t k_s0 = a.s0;
     if constexpr (DR) {
@@ -694,6 +726,9 @@ __global__ void __launch_bounds__(32, MINB)
         const int32_t u = nx.u;
         const int32_t pos = nx.pos;
         const uint64_t pg = nx.pg;
+        if constexpr (PH) {
+            if (lane == 0) s_ph[6] = clock64();
+        }
 
         float4 uv[V];
 #pragma unroll
@@ -770,6 +805,7 @@ __global__ void __launch_bounds__(32, MINB)
         const bool decay_all = a.l2 != 0.f;
         int cnt = 0;  // rows recorded for writing (same value in every lane)
         int32_t nidsA0 = 0, nidsA1 = 0, nidsB0 = 0, nidsB1 = 0;  // (PAIR2)
+        mark(0);
 
         // one round: FFMA2 partials of its 8 rows, the buffer refilled two
         // rounds ahead as soon as they are consumed, then the reduction and
@@ -925,6 +961,7 @@ __global__ void __launch_bounds__(32, MINB)
                 round(1, rd + 3, more);
             }
         }
+        mark(1);
 
         // resolve: re-read every recorded row into its snapshot slot (shared
         // memory, then the worker's spill rows; four rows per pass, one per
@@ -980,6 +1017,7 @@ __global__ void __launch_bounds__(32, MINB)
             }
         }
         __syncwarp();
+        mark(2);
 
         float4 ug[V];
 #pragma unroll
@@ -1009,6 +1047,7 @@ __global__ void __launch_bounds__(32, MINB)
                     row_apply(co, uv[j].w, v.w, d[j].w, ug[j].w);
                 }
             }
+            mark(3);
             if (!dmode) {
                 if (ok) {
                     float *dst = T + (int64_t)ent.id * K + 4 * c;
@@ -1046,6 +1085,7 @@ __global__ void __launch_bounds__(32, MINB)
                     for (int j = 0; j < V; ++j) *reinterpret_cast<float4 *>(dst + 32 * j) = d[j];
                 }
             }
+            mark(4);
         }
         // user row (trainer.py:291-293): S[u] -= lr * (ugrad + l2 * S[u]),
         // the four row slots' partial gradients summed first
@@ -1059,6 +1099,7 @@ __global__ void __launch_bounds__(32, MINB)
                 ug[j].w += __shfl_xor_sync(kFull, ug[j].w, o);
             }
         }
+        mark(3);
         if (g == 0) {
 #pragma unroll
             for (int j = 0; j < V; ++j)
@@ -1074,6 +1115,7 @@ __global__ void __launch_bounds__(32, MINB)
         if (lane == 0) loss += (1.0 - sim_p) + wneg * hinge;
         ++npairs_mine;
         __syncwarp();
+        mark(4);
         if constexpr (PS) {
             // the pair's log entries are written: count it into its step; the
             // step's last pair publishes the log; then apply work is helped
@@ -1103,6 +1145,15 @@ __global__ void __launch_bounds__(32, MINB)
             atomicAdd(prof + 8, (unsigned long long)s_pw[10]);
             atomicAdd(prof + 9, (unsigned long long)s_pw[11]);
             atomicAdd(prof + 10, (unsigned long long)s_pw[12]);
+        }
+    }
+    if constexpr (PH) {
+        if (lane == 0 && a.phase) {
+            for (int i = 0; i < 6; ++i) atomicAdd(a.phase + i, (unsigned long long)s_ph[i]);
+            atomicAdd(a.phase + 6, (unsigned long long)(clock64() - s_ph[7]));
+            atomicAdd(a.phase + 7, (unsigned long long)(globaltimer_ns() - s_ph[8]));
+            atomicAdd(a.phase + 8, 1ull);
+            atomicAdd(a.phase + 9, (unsigned long long)npairs_mine);
         }
     }
 #pragma unroll
@@ -1149,9 +1200,10 @@ static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *w
     // epoch's round order, so the two runtimes record rows, and sum the user
     // gradient, in the same order (bit-identical at one pair in flight)
     const bool p2 = a.delta_ids ? persist_pair2() : pair2;
-    auto kern = a.range_dev ? hogwild_stream<K, MINB, 1, false>
-                : p2        ? hogwild_stream<K, MINB, 0, true>
-                            : hogwild_stream<K, MINB, 0, false>;
+    auto kern = a.range_dev                   ? hogwild_stream<K, MINB, 1, false>
+                : a.phase && !a.delta_ids     ? hogwild_stream<K, MINB, 0, true, true>
+                : p2                          ? hogwild_stream<K, MINB, 0, true>
+                                              : hogwild_stream<K, MINB, 0, false>;
     cudaError_t e;
     const int per_sm = kernel_occupancy((const void *)kern, 32, smem, &e);
     if (e != cudaSuccess) return e;

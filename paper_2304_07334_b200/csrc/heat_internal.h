@@ -15,7 +15,8 @@ cudaError_t launch_exact(float *S, float *T, const int32_t *users, const int32_t
                          int64_t start, int64_t stop, int K, int N, int cosine, double lr,
                          double l2, double mu, double theta, uint64_t s0, int64_t num_items,
                          heat_counters *ctr, float *snap, const int64_t *pair_index,
-                         const heat_agg_params *agg, cudaStream_t stream);
+                         const heat_agg_params *agg, cudaStream_t stream,
+                         unsigned long long *phase = nullptr);
 
 struct HogwildArgs {
     float *S;
@@ -44,6 +45,9 @@ struct HogwildArgs {
     // start/stop above only size the grid (stop - start = the largest step)
     const int64_t *range_dev = nullptr;
     const uint64_t *s0_dev = nullptr;
+    // phase profile (heat_phase_collect): device clock sums, kPhaseWords
+    // words; non-NULL selects the phase-instrumented kernel
+    unsigned long long *phase = nullptr;
     // behaviour aggregation (throughput mode): the query of local pair p is
     // query[(p - start) * K] instead of S[u]; the user gradient is written to
     // ugrad_out[(p - start) * K] and S[u] -= lr * (ugamma * ugrad + l2 * S[u])
@@ -106,6 +110,13 @@ struct PersistRank {
     int gmod_lag, gmod_slots;               // gbase % lag, gbase % nslots
     int acc_ef;                             // accumulator traffic evict-first (else evict-normal)
 };
+
+// Phase profile (trainer.py:120-331 collect_phases; timing.py): words
+// [0, 6) clocks per phase in PHASE_NAMES order (read_emb, similarity, loss,
+// gradient, update, aggregate), [6] clocks the workers spanned, [7] the
+// same spans in globaltimer ns (clock calibration), [8] workers, [9] pairs.
+constexpr int kPhaseWords = 10;
+unsigned long long *phase_buffer();  // NULL unless heat_phase_collect(1)
 
 cudaError_t launch_hogwild(const HogwildArgs &a, cudaStream_t stream, int *workers_out);
 cudaError_t launch_hogwild_resident(const HogwildArgs &a, cudaStream_t stream, int *workers_out);

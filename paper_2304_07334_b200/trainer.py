@@ -22,6 +22,7 @@ sampler is outside the built path and raises ValueError (no CPU fallback).
 
 from __future__ import annotations
 
+import ctypes
 import os
 import time
 from dataclasses import dataclass, field
@@ -207,10 +208,14 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     order comes from the native shuffle, prefetched up to four epochs ahead on host
     thread (hostio.PairPrefetcher); the caller's tables are page-locked once
     so the per-call host<->device copies are async DMA.  wall_time spans the
-    whole call.  With collect_phases the phase dict carries measured times:
-    read_emb = host->device upload, similarity = the fused kernel (read,
-    similarity, loss, gradient and update are one pass), update =
-    device->host write-back.
+    whole call.  With collect_phases the phase dict carries the reference's
+    phases (trainer.py:120-331, seconds averaged over the workers as
+    trainer.py:452-455 averages its threads), measured on the device with
+    clock64 by the phase-instrumented kernels (heat_phase_collect): EXACT
+    mode runs the serial kernel (same bits), Hogwild mode at dim 64/128 the
+    register-streamed kernel with its fused phases split by where the time
+    goes.  Launches without an instrumented kernel
+    (other dims, the Hogwild aggregator) leave the phases at zero.
     """
     from .hostio import PREFETCH, pin_array
 
@@ -222,43 +227,56 @@ def train_epoch(S, T, train, cfg, weights=None, epoch: int = 0,
     model = _session_model(S.values, T.values)  # raises without CUDA: no CPU fallback
     bufs = PREFETCH.get(train, shuffle_seed(cfg.seed, epoch))
     dev = model.device
-    stream = torch.cuda.current_stream(dev)
     pin_array(S.values)
     pin_array(T.values)
-    t_up = time.perf_counter()
     model.S.copy_(torch.from_numpy(S.values), non_blocking=True)
     model.T.copy_(torch.from_numpy(T.values), non_blocking=True)
     pairs = bufs[2].to(dev, non_blocking=True)  # users and items in one copy
     du, di = pairs[0], pairs[1]
-    if collect_phases:
-        stream.synchronize()
     agg = _make_aggregator(model, weights, train, cfg)
-    t_run = time.perf_counter()
-    ev_down = torch.cuda.Event(enable_timing=True)
-    ev_end = torch.cuda.Event(enable_timing=True)
 
     def write_back():  # queued behind the kernel; one host sync for everything
-        ev_down.record()
         torch.from_numpy(S.values).copy_(model.S, non_blocking=True)
         torch.from_numpy(T.values).copy_(model.T, non_blocking=True)
-        ev_end.record()
 
     def prefetch():  # host threads produce the next orders while the GPU runs
         for ahead in range(1, PREFETCH.depth_for(train.num_pairs) + 1):
             PREFETCH.prefetch(train, shuffle_seed(cfg.seed, epoch + ahead))
 
-    rep, timing = run_epoch_on_device(model, train, cfg, epoch, pairs=(du, di), agg=agg,
-                                      before_read=write_back, before_sync=prefetch)
+    if collect_phases:
+        _phase_begin()
+    try:
+        rep, _ = run_epoch_on_device(model, train, cfg, epoch, pairs=(du, di), agg=agg,
+                                     before_read=write_back, before_sync=prefetch)
+    finally:
+        phases = _phase_end() if collect_phases else None
     PREFETCH.release(bufs)
     if agg is not None:  # the reference updates the shared weights in place
         np.copyto(weights, agg.W.cpu().numpy())
     t_end = time.perf_counter()
     rep.wall_time = t_end - t_start
-    if collect_phases:
-        rep.phase_times["read_emb"] = t_run - t_up
-        rep.phase_times["similarity"] = timing["kernel_s"]
-        rep.phase_times["update"] = ev_down.elapsed_time(ev_end) / 1e3
+    if phases is not None:
+        rep.phase_times.update(phases)
     return rep
+
+
+def _phase_begin() -> None:
+    L = N.lib()
+    N.check(L.heat_phase_read((ctypes.c_double * 6)(), None, None, 1))  # zero the sums
+    N.check(L.heat_phase_collect(1))
+
+
+def _phase_end() -> dict:
+    """Seconds per phase (PHASE_NAMES order) of the launches since
+    _phase_begin, averaged over the workers; collection off again."""
+    L = N.lib()
+    sec = (ctypes.c_double * 6)()
+    workers = ctypes.c_int64(0)
+    try:
+        N.check(L.heat_phase_read(sec, ctypes.byref(workers), None, 1))
+    finally:
+        N.check(L.heat_phase_collect(0))
+    return {name: float(sec[i]) for i, name in enumerate(PHASE_NAMES)}
 
 
 _SESSION: dict = {}
