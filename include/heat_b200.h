@@ -222,6 +222,24 @@ int heat_shard_epoch(heat_shard *h, float *S, int64_t s_rows, float *T, int64_t 
 const char *heat_shard_last_error(heat_shard *h);
 int heat_shard_destroy(heat_shard *h);
 
+/* Host transport: the per-process runtime with its collectives carried by a
+ * caller-supplied host all-gather instead of NCCL, for `world` PROCESSES that
+ * share one GPU (NCCL refuses two ranks on a device).  `allgather(user, in,
+ * nbytes, out)` gathers nbytes from every rank into out (world * nbytes, rank
+ * order) and returns 0; every rank calls it in the same order.  The entry-
+ * count exchange of each step becomes that call between two synchronisations
+ * of the comm stream (the same cross-rank fence, with the host in the loop);
+ * the peers' logs are read through CUDA IPC mappings by the same fused
+ * gather+apply kernels as over NVLink (or, with HEAT_SHARD_EXCHANGE=gather,
+ * all-gathered through host memory).  Stream-ordered steps only: the
+ * persistent epoch and captured graphs are off, so no kernel of one process
+ * ever waits on a kernel of another.  A test and bring-up path (it covers
+ * the IPC mapping, the fence ordering and replica identity of the
+ * multi-process runtime on a one-GPU box), not a fast one. */
+typedef int (*heat_host_allgather_fn)(void *user, const void *in, int64_t nbytes, void *out);
+int heat_shard_create_host(int32_t world, int32_t rank, heat_host_allgather_fn allgather,
+                           void *user, int32_t device, heat_shard **out);
+
 /* Loopback group: `world` ranks in ONE process on one device, for testing
  * the runtime's multi-rank step logic where only one GPU exists (no NCCL,
  * no CUDA IPC).  The collectives become stream-ordered copies into a shared

@@ -25,9 +25,15 @@ EXPORTS = ("heat_train_range", "heat_scratch_bytes", "heat_sample_negatives",
            "heat_eval_users", "heat_apply_row_deltas", "heat_apply_row_deltas_fixed",
            "heat_epoch_pairs", "heat_aggregate_users", "heat_agg_scratch_bytes",
            "heat_exact_stats", "heat_nccl_unique_id", "heat_shard_create", "heat_shard_epoch",
-           "heat_shard_last_error", "heat_shard_destroy", "heat_shard_create_loopback",
+           "heat_shard_last_error", "heat_shard_destroy", "heat_shard_create_host",
+           "heat_shard_create_loopback",
            "heat_shard_epoch_loopback", "heat_phase_collect", "heat_phase_read",
            "heat_probe_l2_read", "heat_probe_l2_gather", "heat_last_error", "heat_version")
+
+
+# heat_host_allgather_fn: int (*)(void *user, const void *in, int64_t nbytes, void *out)
+HOST_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_int64, ctypes.c_void_p)
 
 
 class SgdParams(ctypes.Structure):
@@ -144,6 +150,9 @@ def lib():
     L.heat_shard_last_error.argtypes = [P]
     L.heat_shard_destroy.restype = ctypes.c_int
     L.heat_shard_destroy.argtypes = [P]
+    L.heat_shard_create_host.restype = ctypes.c_int
+    L.heat_shard_create_host.argtypes = [i32, i32, HOST_ALLGATHER_FN, P, i32,
+                                         ctypes.POINTER(ctypes.c_void_p)]
     L.heat_shard_create_loopback.restype = ctypes.c_int
     L.heat_shard_create_loopback.argtypes = [i32, i32, P]
     L.heat_shard_epoch_loopback.restype = ctypes.c_int

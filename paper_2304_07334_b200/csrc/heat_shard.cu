@@ -119,6 +119,13 @@ struct heat_shard {
     int lag = 2, lag_persist = 3;
     int nalloc = 0;  // log slots allocated (max(lag, lag_persist, 2) + 1)
     ncclComm_t comm = nullptr;
+    // host transport (heat_shard_create_host): the collectives of the
+    // per-process runtime as calls of a caller-supplied host all-gather
+    // (e.g. torch.distributed over gloo) around stream synchronisations,
+    // for ranks that share one GPU (NCCL refuses two ranks on a device).
+    // Same-device CUDA IPC carries the logs exactly as NVLink would.
+    heat_host_allgather_fn hostx = nullptr;
+    void *hostx_user = nullptr;
     cudaStream_t comm_stream = nullptr;
     cudaStream_t cstream[2] = {nullptr, nullptr};
     cudaEvent_t ev_start = nullptr, ev_cdone[2] = {nullptr, nullptr}, ev_comm = nullptr;
@@ -367,6 +374,10 @@ struct ShardErr {
 static bool host_all_gather(heat_shard *h, ShardErr &er, const int64_t *in, int64_t n,
                             int64_t *out) {
     const int64_t bytes = n * (int64_t)sizeof(int64_t);
+    if (h->hostx) {
+        if (h->hostx(h->hostx_user, in, bytes, out) != 0) return er.invalid("host all-gather failed");
+        return true;
+    }
     int64_t *d = h->scratch;  // 1 + world entries of 64 B handles fit (see create)
     if (!er.cuda(cudaMemcpyAsync(d, in, bytes, cudaMemcpyHostToDevice, h->comm_stream), "stage"))
         return false;
@@ -727,8 +738,9 @@ int heat_nccl_unique_id(unsigned char *out128) {
     return HEAT_OK;
 }
 
-int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id, int32_t device,
-                      heat_shard **out) {
+static int shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
+                        heat_host_allgather_fn hostx, void *hostx_user, int32_t device,
+                        heat_shard **out) {
     if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
         return HEAT_ERR_INVALID;
     heat_shard *h = new heat_shard();
@@ -775,7 +787,14 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
         heat_shard_destroy(h);
         return HEAT_ERR_CUDA;
     }
-    if (world > 1) {
+    if (hostx) {
+        // no kernel of one rank may wait on a kernel of another rank when the
+        // ranks share a GPU: stream-ordered steps only, no captured graphs
+        h->hostx = hostx;
+        h->hostx_user = hostx_user;
+        h->persist = false;
+        h->graphs = false;
+    } else if (world > 1) {
         const NcclApi &n = nccl();
         if (!n.ok || !nccl_id) {
             heat_shard_destroy(h);
@@ -791,6 +810,17 @@ int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id,
     }
     *out = h;
     return HEAT_OK;
+}
+
+int heat_shard_create(int32_t world, int32_t rank, const unsigned char *nccl_id, int32_t device,
+                      heat_shard **out) {
+    return shard_create(world, rank, nccl_id, nullptr, nullptr, device, out);
+}
+
+int heat_shard_create_host(int32_t world, int32_t rank, heat_host_allgather_fn allgather,
+                           void *user, int32_t device, heat_shard **out) {
+    if (!allgather) return HEAT_ERR_INVALID;
+    return shard_create(world, rank, nullptr, allgather, user, device, out);
 }
 
 int heat_shard_destroy(heat_shard *h) {
@@ -971,13 +1001,53 @@ struct EpochRun {
         er.cuda(cudaEventRecord(h->slot[s % nslots].cnt_ready, h->comm_stream), "record counts");
     }
 
+    // host transport: the count all-gather as a host collective between two
+    // synchronisations of the comm stream — the same fence (no rank leaves it
+    // before every rank's step-s log and apply(s-1) are complete), with the
+    // host in the loop
+    void host_count(Slot &sl, int64_t *cnts) {
+        int64_t mine = 0;
+        std::vector<int64_t> all(W);
+        er.cuda(cudaMemcpyAsync(&mine, sl.cnt, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                h->comm_stream), "count to host");
+        er.cuda(cudaStreamSynchronize(h->comm_stream), "count sync");
+        // every rank makes the call whatever its own error state (a collective)
+        if (h->hostx(h->hostx_user, &mine, sizeof(int64_t), all.data()) != 0)
+            er.invalid("host all-gather failed");
+        er.cuda(cudaMemcpyAsync(cnts, all.data(), W * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                h->comm_stream), "counts to device");
+        er.cuda(cudaStreamSynchronize(h->comm_stream), "count sync");  // `all` leaves scope
+    }
+
+    // gather fallback under the host transport: logs through host memory
+    void host_gather(Slot &sl, int64_t cmax) {
+        const int64_t ib = cmax * (int64_t)sizeof(int32_t), rb = cmax * K * (int64_t)sizeof(float);
+        std::vector<char> mine(ib + rb), all((ib + rb) * W);
+        er.cuda(cudaMemcpyAsync(mine.data(), sl.ids, ib, cudaMemcpyDeviceToHost, h->comm_stream),
+                "log to host");
+        er.cuda(cudaMemcpyAsync(mine.data() + ib, sl.rows, rb, cudaMemcpyDeviceToHost,
+                                h->comm_stream), "log to host");
+        er.cuda(cudaStreamSynchronize(h->comm_stream), "log sync");
+        if (h->hostx(h->hostx_user, mine.data(), ib + rb, all.data()) != 0)
+            er.invalid("host all-gather failed");
+        for (int q = 0; q < W; ++q) {
+            er.cuda(cudaMemcpyAsync(sl.g_ids + q * cmax, all.data() + q * (ib + rb), ib,
+                                    cudaMemcpyHostToDevice, h->comm_stream), "log to device");
+            er.cuda(cudaMemcpyAsync(sl.g_rows + q * cmax * K, all.data() + q * (ib + rb) + ib, rb,
+                                    cudaMemcpyHostToDevice, h->comm_stream), "log to device");
+        }
+        er.cuda(cudaStreamSynchronize(h->comm_stream), "log sync");
+    }
+
     // counts of step s: the fence every rank passes before reading slot s
     // (NCCL all-gather between processes; at world 1 a local copy)
     void count(int64_t s) {
         Slot &sl = h->slot[s % nslots];
         er.cuda(cudaStreamWaitEvent(h->comm_stream, sl.log_ready, 0), "wait log");
         int64_t *cnts = h->step_counts + s * W;
-        if (W > 1)  // (world 1, direct: the apply records the log's own counter)
+        if (W > 1 && h->hostx)
+            host_count(sl, cnts);
+        else if (W > 1)  // (world 1, direct: the apply records the log's own counter)
             er.nccl(nccl().all_gather(sl.cnt, cnts, 1, ncclInt64, h->comm, h->comm_stream),
                     "all_gather counts");
         else if (!direct)
@@ -1028,6 +1098,8 @@ struct EpochRun {
                                                 cmax * K * sizeof(float), cudaMemcpyDeviceToDevice,
                                                 h->comm_stream), "gather");
                     }
+                } else if (h->hostx) {
+                    host_gather(sl, cmax);
                 } else {
                     const NcclApi &n = nccl();
                     er.nccl(n.group_start(), "group start");

@@ -499,8 +499,15 @@ class NativeShardTrainer(ShardedTrainer):
     no host wait between steps; kernel(s) sees every applied step up to
     s - lag (lag 2, ``HEAT_SHARD_LAG``)."""
 
-    def __init__(self, model: DeviceModel, world: int, rank: int, group=None):
+    def __init__(self, model: DeviceModel, world: int, rank: int, group=None,
+                 transport: str = "nccl"):
         super().__init__(model, world, rank, group)
+        self.stats = N.ShardStats()
+        if transport == "host":
+            self._h = self._create_host(group)
+            return
+        if transport != "nccl":
+            raise ValueError("transport must be 'nccl' or 'host'")
         uid = None
         if world > 1:
             buf = (ctypes.c_ubyte * 128)()
@@ -513,7 +520,32 @@ class NativeShardTrainer(ShardedTrainer):
         N.check(N.lib().heat_shard_create(world, rank, uid, model.device.index or 0,
                                           ctypes.byref(h)))
         self._h = h
-        self.stats = N.ShardStats()
+
+    def _create_host(self, group):
+        """heat_shard_create_host: the runtime's collectives as torch.distributed
+        all-gathers of host bytes over `group` (gloo), for ranks that share
+        one GPU.  The peers' logs still travel through CUDA IPC mappings."""
+        world = self.world
+
+        def allgather(_user, src, nbytes, dst):
+            try:
+                mine = torch.frombuffer((ctypes.c_ubyte * nbytes).from_address(src),
+                                        dtype=torch.uint8).clone()
+                parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, mine, group=group)
+                flat = torch.cat(parts).numpy()  # held until the copy is done
+                ctypes.memmove(dst, flat.ctypes.data, nbytes * world)
+                return 0
+            except Exception:  # never unwind through the C caller
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._hostx = N.HOST_ALLGATHER_FN(allgather)  # keep the thunk alive
+        h = ctypes.c_void_p()
+        N.check(N.lib().heat_shard_create_host(world, self.rank, self._hostx, None,
+                                               self.model.device.index or 0, ctypes.byref(h)))
+        return h
 
     def _buffers(self, cap: int):  # logs live in the native runtime
         return None
