@@ -8,7 +8,8 @@ Exercised: the rank-local DELTA steps, the count "collective" as the
 cross-rank fence, the fused gather+apply reading the peers' logs through
 device pointers, the gather fallback, the log-slot rotation under each lag,
 the exact-capacity logs, and replica bit-identity.  Not exercised here: the
-CUDA IPC mapping and the NCCL calls themselves (they need two GPUs).
+CUDA IPC mapping (tests/test_gpu_shard_ipc.py runs two processes for that)
+and the NCCL calls themselves (they need two GPUs).
 
 Determinism argument used by the first test: with one pair in flight per
 rank (one warp per pair) and lag 1, step s of every rank reads T as left by the apply of step
