@@ -23,10 +23,12 @@ JSON line keys beyond the base contract:
                 ``train_epoch(S, T, train, cfg)`` with host numpy tables:
                 shuffle + H2D of tables and pairs + kernel + D2H of tables
 
-The ``--impl reference`` arm imports nothing from the product package: its
-data come from ``workloads`` (pure numpy) and its epoch order and timed
-training from ``oracle`` (numpy + the C port), so it never maps
-libheat_b200.so.
+The ``--impl reference`` arm imports nothing from the product package and
+never maps libheat_b200.so.  It times the UNMODIFIED reference, heatcf's own
+``train_epoch`` (numba, all host cores) from baseline/_ref, on a bounded
+sample of the workload cut with the oracle's numpy shuffle
+(cpu_baseline.kind "reference"); if heatcf or numba cannot be imported it
+falls back to the C oracle port (kind "port").
 """
 
 from __future__ import annotations
@@ -200,10 +202,98 @@ def cpu_baseline_timed(spec, train, S0, T0, threads: int, seconds: float = 10.0)
             "seconds": dt}
 
 
+def _heatcf():
+    """The UNMODIFIED reference package (heatcf: Python + numba, installed by
+    build() into baseline/_ref, which travels to the GPU box) or None when it
+    or numba cannot be imported.  Nothing of the product is involved."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.environ.get("HEAT_BENCH_REF") == "port" or \
+            not os.path.isdir(os.path.join(ref, "heatcf")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.dont_write_bytecode = True
+    try:
+        import numba  # noqa: F401
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import heatcf.dataset
+        import heatcf.embeddings
+        import heatcf.trainer
+        return heatcf
+    except Exception as exc:  # fall back to the C port, and say so
+        print(f"[bench] heatcf not usable ({exc!r}); reference arm = the C port",
+              file=sys.stderr)
+        return None
+
+
+def heatcf_sample(H, spec, train, sample_pairs: int):
+    """A bounded sample of the workload as a heatcf InteractionSet: the first
+    `sample_pairs` pairs of epoch 0's order over the SAME user and item
+    universe, so a pair costs what it costs in the full epoch (same tables,
+    N, K, chunk size).  Built with numpy from the oracle's shuffle (test
+    infrastructure, allowed in this arm)."""
+    from oracle import oracle as O
+    u, i = O.epoch_pairs(train.offsets, train.items, train.num_users, O.shuffle_seed(0, 0))
+    n = min(sample_pairs, len(u))
+    u, i = u[:n].astype(np.int64), i[:n].astype(np.int32)
+    order = np.lexsort((i, u))
+    offsets = np.zeros(train.num_users + 1, dtype=np.int64)
+    np.cumsum(np.bincount(u, minlength=train.num_users), out=offsets[1:])
+    return H.dataset.InteractionSet(train.num_users, train.num_items, offsets, i[order])
+
+
+def run_reference_heatcf(H, args):
+    """`--impl reference`, the reference itself: heatcf.trainer.train_epoch
+    (trainer.py:385-466: the threaded Hogwild driver over the numba chunk
+    loop) with every host core, each step one epoch over a bounded sample of
+    the workload; value = heatcf's own pairs_per_s (bench.py:75-84:
+    num_pairs / EpochReport.wall_time, i.e. without the shuffle)."""
+    train, _, spec, S, T = build_workload(args.config)
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample or {"c1": 20000, "c2": 2_000_000, "c3": 600_000, "c4": 200_000,
+                                 "c5": 100_000}[spec.name]
+    sub = heatcf_sample(H, spec, train, sample)
+    cfg = H.trainer.TrainingConfig(
+        emb_dim=spec.dim, num_negatives=spec.negatives, learning_rate=spec.learning_rate,
+        epochs=1, num_threads=threads, similarity="cosine",
+        loss=H.trainer.LossParams(mu=spec.mu, theta=spec.theta), seed=0, l2_reg=0.0,
+        chunk_pairs=2048)
+    Sm, Tm = H.embeddings.EmbeddingMatrix(S.copy()), H.embeddings.EmbeddingMatrix(T.copy())
+    small = heatcf_sample(H, spec, train, min(sample, 4096 * threads))
+    for w in range(max(args.warmup, 1)):  # (the first call also JIT-compiles the chunk loop)
+        H.trainer.train_epoch(Sm, Tm, small, cfg, epoch=w)
+    vals, secs = [], []
+    for s in range(args.steps):
+        r = H.trainer.train_epoch(Sm, Tm, sub, cfg, epoch=args.warmup + s)
+        vals.append(r.num_pairs)
+        secs.append(r.wall_time)
+    v = float(np.sum(vals) / np.sum(secs))  # heatcf bench: num_pairs / mean epoch time
+    what = (f"{sub.num_pairs} pairs = the first {sub.num_pairs} pairs of epoch 0 of {spec.name} "
+            f"as one heatcf epoch ({float(np.mean(secs)):.1f} s; heatcf.trainer."
+            f"train_epoch, numba, {threads} threads, chunk 2048)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean(secs)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(spec, train),
+            "run": {"mode": "hogwild (host threads)", "threads": threads,
+                    "step": "one heatcf epoch over a bounded sample (cpu_baseline.sample)",
+                    "code": "heatcf.trainer.train_epoch from baseline/_ref (unmodified)"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads,
+                             "kind": "reference", "sample": what},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    H = _heatcf()
+    if H is not None:
+        return run_reference_heatcf(H, args)
     train, _, spec, S, T = build_workload(args.config)
     threads = os.cpu_count() or 1
     sample = args.ref_sample or {"c1": 20000, "c2": 400_000, "c3": 100_000, "c4": 60_000,

@@ -108,3 +108,29 @@ def test_kernels_spec_restatement_matches_reference(heatcf_mod):
     z = np.zeros(4)
     assert KS.cosine_forward(z, np.ones(4))[3:] == (0.0, True)
     assert not KS.cosine_grad_user(z, np.ones(4)).any()
+
+
+def test_reference_arm_sample_is_a_valid_subset(heatcf_mod):
+    """bench.py --impl reference times heatcf itself on a bounded sample: the
+    sample is a well-formed heatcf InteractionSet over the full universe whose
+    pairs are a subset of the workload's, and one heatcf epoch over it runs."""
+    import numpy as np
+
+    import bench
+    import heatcf.embeddings
+    import heatcf.trainer
+    train, _, spec, S, T = bench.build_workload("c1")
+    sub = bench.heatcf_sample(heatcf_mod, spec, train, 5000)
+    assert (sub.num_users, sub.num_items, sub.num_pairs) == (train.num_users, train.num_items, 5000)
+    full = {(u, int(i)) for u in range(train.num_users)
+            for i in train.items[train.offsets[u]:train.offsets[u + 1]]}
+    for u in range(sub.num_users):
+        sl = sub.slice(u)
+        assert np.all(np.diff(sl) > 0)  # ascending, no duplicates
+        assert all((u, int(i)) in full for i in sl)
+    cfg = heatcf.trainer.TrainingConfig(emb_dim=spec.dim, num_negatives=spec.negatives,
+                                        learning_rate=spec.learning_rate, num_threads=2,
+                                        loss=heatcf.trainer.LossParams(mu=spec.mu, theta=spec.theta))
+    r = heatcf.trainer.train_epoch(heatcf.embeddings.EmbeddingMatrix(S.copy()),
+                                   heatcf.embeddings.EmbeddingMatrix(T.copy()), sub, cfg)
+    assert r.num_pairs == 5000 and np.isfinite(r.mean_loss) and r.wall_time > 0
