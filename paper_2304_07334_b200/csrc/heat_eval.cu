@@ -248,10 +248,18 @@ __global__ void __launch_bounds__(kEvalThreads)
 // into registers while the current one is scored.
 constexpr int kRbUsers = 32;
 constexpr int kRbItems = 128;
-#ifndef EVAL_TILE_F64
-#define EVAL_TILE_F64 0  // 1: binary64 tile (measured slower: 17.4 vs 16.2 ms on c2)
+// The MMA variant keeps the tile in binary64 (converted once when it is
+// stored, not once per fragment load: every tile element is a B operand of
+// four warps) and, so that this costs no shared memory, writes the tile's
+// scores over the tile itself once every warp has finished its products.
+// EVAL_TILE_F32=1 restores the float tile with a separate score buffer.
+#ifndef EVAL_TILE_F32
+#define EVAL_TILE_F32 0
 #endif
-using TileT = std::conditional_t<EVAL_TILE_F64 != 0, double, float>;
+template <bool MMA>
+using RbTile = std::conditional_t<MMA && EVAL_TILE_F32 == 0, double, float>;
+template <bool MMA>
+constexpr bool kRbAlias = MMA && EVAL_TILE_F32 == 0;
 
 // MMA variant: the 32 x 128 x K product of a tile on the FP64 tensor path
 // (mma.sync m8n8k4 f64; tcgen05 has no binary64 kind), the user matrix and
@@ -269,13 +277,14 @@ template <bool MMA = false>
 __host__ __device__ inline size_t eval_rb_smem_bytes(int K, int k) {
     size_t b = 0;
     b += align16(sizeof(double) * K * rb_ldu<MMA>());        // user vectors, transposed
-    b += align16(sizeof(TileT) * kRbItems * rb_ldt<MMA>(K));  // item tile (padded rows)
-    if (MMA) b += align16(sizeof(double) * kRbUsers * kRbScoreLd);  // tile scores
+    const size_t tile = align16(sizeof(RbTile<MMA>) * kRbItems * rb_ldt<MMA>(K));  // padded rows
+    const size_t score = MMA ? align16(sizeof(double) * kRbUsers * kRbScoreLd) : 0;
+    b += kRbAlias<MMA> ? (tile > score ? tile : score) : tile + score;  // (scores over the tile)
     b += align16(sizeof(double) * kRbUsers * k);     // list scores
     b += align16(sizeof(int32_t) * kRbUsers * k);    // list ids
     b += align16(sizeof(uint32_t) * kRbUsers * 4);   // train-positive mask of the tile
     b += align16(sizeof(double) * kRbUsers * 2);     // user norms and reciprocals
-    b += align16(sizeof(int64_t) * kRbUsers * 2);    // train cursors and ends
+    b += align16(sizeof(int64_t) * kRbUsers * 3);    // train cursors, ends, next train item
     return b;
 }
 
@@ -310,10 +319,19 @@ __global__ void __launch_bounds__(256)
     const int LDT = rb_ldt<MMA>(K);
     double *uT = reinterpret_cast<double *>(ptr);
     ptr += align16(sizeof(double) * K * LDU);
+    using TileT = RbTile<MMA>;
     TileT *tile = reinterpret_cast<TileT *>(ptr);
-    ptr += align16(sizeof(TileT) * kRbItems * LDT);
     double *tscore = reinterpret_cast<double *>(ptr);  // MMA: [32 users][128 items]
-    if (MMA) ptr += align16(sizeof(double) * kRbUsers * kRbScoreLd);
+    {
+        const size_t tb = align16(sizeof(TileT) * kRbItems * LDT);
+        const size_t sb = MMA ? align16(sizeof(double) * kRbUsers * kRbScoreLd) : 0;
+        if constexpr (kRbAlias<MMA>) {
+            ptr += tb > sb ? tb : sb;
+        } else {
+            tscore = reinterpret_cast<double *>(ptr + tb);
+            ptr += tb + sb;
+        }
+    }
     double *ls = reinterpret_cast<double *>(ptr);
     ptr += align16(sizeof(double) * kRbUsers * k);
     int32_t *lid = reinterpret_cast<int32_t *>(ptr);
@@ -322,7 +340,9 @@ __global__ void __launch_bounds__(256)
     ptr += align16(sizeof(uint32_t) * kRbUsers * 4);
     double *unv = reinterpret_cast<double *>(ptr);  // [0, 32) norms, [32, 64) reciprocals
     ptr += align16(sizeof(double) * kRbUsers * 2);
-    int64_t *curv = reinterpret_cast<int64_t *>(ptr);  // [0, 32) cursors, [32, 64) ends
+    // [0, 32) cursors, [32, 64) ends, [64, 96) the item at the cursor
+    // (INT64_MAX when exhausted): a tile below it has no train positive
+    int64_t *curv = reinterpret_cast<int64_t *>(ptr);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ubase = (int64_t)blockIdx.x * kRbUsers;
@@ -350,6 +370,8 @@ __global__ void __launch_bounds__(256)
         const bool has = b < nub && u < tr_num_users;
         curv[b] = has ? tr_off[u] : 0;
         curv[kRbUsers + b] = has ? tr_off[u + 1] : 0;
+        curv[2 * kRbUsers + b] =
+            (has && tr_off[u] < tr_off[u + 1]) ? (int64_t)tr_items[tr_off[u]] : INT64_MAX;
     }
     int n_l[4] = {0, 0, 0, 0};
     // tile staging: 128 rows x K floats, float4 loads held in registers
@@ -373,7 +395,12 @@ __global__ void __launch_bounds__(256)
             const int r = f / (KC / 4), c = (f % (KC / 4)) * 4;
             if (r < kRbItems && c < K) {
                 TileT *d = tile + r * LDT + c;
-                d[0] = pre[q].x; d[1] = pre[q].y; d[2] = pre[q].z; d[3] = pre[q].w;
+                if constexpr (sizeof(TileT) == 8) {  // (LDT even, c % 4 == 0: 16-byte aligned)
+                    *reinterpret_cast<double2 *>(d) = make_double2(pre[q].x, pre[q].y);
+                    *reinterpret_cast<double2 *>(d + 2) = make_double2(pre[q].z, pre[q].w);
+                } else {
+                    d[0] = pre[q].x; d[1] = pre[q].y; d[2] = pre[q].z; d[3] = pre[q].w;
+                }
             }
         }
     };
@@ -388,6 +415,7 @@ __global__ void __launch_bounds__(256)
         if (i0 + kRbItems < t_rows) load_tile(i0 + kRbItems);  // overlaps the scoring
         for (int j = 0; j < 4; ++j) {
             const int b = warp * 4 + j;
+            if (curv[2 * kRbUsers + b] >= i0 + kRbItems) continue;  // (warp-uniform)
             int64_t c0 = curv[b];
             const int64_t cend = curv[kRbUsers + b];
             while (c0 < cend) {
@@ -403,7 +431,10 @@ __global__ void __launch_bounds__(256)
                 if (m != 0xffffffffu) break;
             }
             __syncwarp();
-            if (lane == 0) curv[b] = c0;
+            if (lane == 0) {
+                curv[b] = c0;
+                curv[2 * kRbUsers + b] = c0 < cend ? (int64_t)tr_items[c0] : INT64_MAX;
+            }
         }
         __syncwarp();
         // 4 users x 4 items of dot products per lane
@@ -433,6 +464,7 @@ __global__ void __launch_bounds__(256)
                         : "d"(av), "d"(bv));
                 }
             }
+            if constexpr (kRbAlias<MMA>) __syncthreads();  // every warp is done with the tile
             double *srow = tscore + (size_t)(8 * ub + g) * kRbScoreLd + 64 * ih + 2 * tq;
 #pragma unroll
             for (int ni = 0; ni < 8; ++ni)
@@ -459,6 +491,15 @@ __global__ void __launch_bounds__(256)
             }
         }
         __syncwarp();
+        // this lane's four items of the tile: reciprocal norms for the screen
+        // (0 past the table: such a slot can only pass the screen when the
+        // k-th score is <= 0, and the merge below rejects it as invalid)
+        double rin[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int64_t item = i0 + lane + 32 * m;
+            rin[m] = (cosine && item < t_rows) ? rinorm_g[item] : 0.0;
+        }
         // merge, one user at a time (items in increasing id order per lane
         // group; the tie rule keeps the lower id, so order of arrival within
         // equal scores does not matter: the insertion point compares ids)
@@ -469,6 +510,22 @@ __global__ void __launch_bounds__(256)
             double *lsb = ls + b * k;
             int32_t *lidb = lid + b * k;
             int n = n_l[j];
+            // Screen of the whole tile for this user, before anything else is
+            // looked at: once the list is full almost no tile holds a score
+            // near the k-th one.  The test is the merge's own approximate
+            // screen (same expression, same slack) without the validity and
+            // mask lookups, so it passes a superset of the merge's candidates.
+            if (n == k) {
+                const double lim = lsb[k - 1] - 1e-9;
+                const double run = cosine ? unv[kRbUsers + b] : 1.0;
+                bool any = false;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const double approx = cosine ? acc[j][m] * run * rin[m] : acc[j][m];
+                    any |= !(approx < lim);
+                }
+                if (!__any_sync(0xffffffffu, any)) continue;
+            }
             for (int m = 0; m < 4; ++m) {
                 const int o = lane + 32 * m;
                 const int64_t item = i0 + o;
