@@ -51,11 +51,11 @@ def heatcf():
     return h
 
 
-def _run(h, threads, installed, tmp_path=None):
+def _run(h, threads, installed, tmp_path=None, seed=7):
     from paper_2304_07334_b200.install import install, uninstall
     train_set, test_set = h.synth.make_clustered(400, 1200, 8, 24, seed=3)
     cfg = h.TrainingConfig(emb_dim=32, num_negatives=16, learning_rate=0.05, epochs=4,
-                           num_threads=threads, seed=7)
+                           num_threads=threads, seed=seed)
     S = h.init_matrix(train_set.num_users, 32, h.InitSpec(seed=1))
     T = h.init_matrix(train_set.num_items, 32, h.InitSpec(seed=2))
     if installed:
@@ -89,9 +89,22 @@ def test_heatcf_train_deterministic_is_bit_identical(heatcf, tmp_path):
 
 
 def test_heatcf_train_hogwild_matches_reference_quality(heatcf):
-    _, _, rr = _run(heatcf, 8, installed=False)
-    _, _, rg = _run(heatcf, 8, installed=True)
-    assert np.isfinite([r.mean_loss for r in rg.reports]).all()
-    # the reference's own thread-parity bound (test_trainer.py:199-208)
-    assert abs(rg.final_metrics.recall_at_k - rr.final_metrics.recall_at_k) <= 0.01, (
-        rg.final_metrics.recall_at_k, rr.final_metrics.recall_at_k)
+    """Hogwild runs are not reproducible on either side (thread / warp
+    interleaving), and one run's recall@20 moves in steps of ~1/400 on this
+    data, so single runs of the two differ by up to ~0.011.  Compared here:
+    the 5-seed mean of heatcf.train through install() (throughput kernel)
+    against the 5-seed mean of the reference's own 8-thread runs AND against
+    the deterministic single-thread runs (bit-identical between the two
+    implementations, previous test), each within the reference's thread-parity
+    bound (test_trainer.py:199-208)."""
+    seeds = (7, 8, 9, 10, 11)
+    gpu, ref8, det = [], [], []
+    for sd in seeds:
+        rg = _run(heatcf, 8, installed=True, seed=sd)[2]
+        assert np.isfinite([r.mean_loss for r in rg.reports]).all()
+        gpu.append(rg.final_metrics.recall_at_k)
+        ref8.append(_run(heatcf, 8, installed=False, seed=sd)[2].final_metrics.recall_at_k)
+        det.append(_run(heatcf, 1, installed=False, seed=sd)[2].final_metrics.recall_at_k)
+    g, r8, d1 = float(np.mean(gpu)), float(np.mean(ref8)), float(np.mean(det))
+    assert abs(g - d1) <= 0.01, (gpu, det)
+    assert abs(g - r8) <= 0.01, (gpu, ref8)
