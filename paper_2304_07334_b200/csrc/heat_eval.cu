@@ -611,6 +611,292 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---- fragment-resident variant (K % 4 == 0, K <= 128; the default) ----------
+// The same FP64 tensor-path product, re-tiled so that the scores never leave
+// the registers: a CTA holds 64 users, warp w OWNS users 8w .. 8w+7 and
+// scores them against a 64-item tile (8 m8n8k4 tiles, 16 accumulators per
+// thread), the tile kept in binary64 (converted once when stored).  Each
+// thread screens its own 16 scores of user 8w + (lane >> 2) against that
+// user's limit — (k-th score - 2e-9) / (1 / |u|), so one multiply by the
+// item's reciprocal norm and one compare per score — and only a warp with a
+// survivor enters the merge, which is the register-blocked kernel's (exact
+// cosine s / (|u| |v|) as evaluator.py:48-58 divides it, order (score desc,
+// id asc), train positives masked).  A warp is the only writer of its users'
+// lists, so a tile costs two CTA barriers (tile stored / tile consumed) and
+// no score buffer: the register-blocked kernel above spent a quarter of its
+// stall samples on four barriers per 128 items (profiles/r02_ncu_eval.txt).
+constexpr int kFrUsers = 64;
+constexpr int kFrItems = 64;
+
+__host__ __device__ inline size_t eval_fr_smem_bytes(int K, int k) {
+    size_t b = 0;
+    b += align16(sizeof(double) * K * (kFrUsers + 4));  // user vectors, transposed
+    b += align16(sizeof(double) * kFrItems * (K + 4));  // item tile, binary64, padded rows
+    b += align16(sizeof(double) * kFrItems);            // reciprocal item norms of the tile
+    b += align16(sizeof(double) * kFrUsers * k);        // list scores
+    b += align16(sizeof(int32_t) * kFrUsers * k);       // list ids
+    b += align16(sizeof(uint32_t) * kFrUsers * 2);      // train-positive mask of the tile
+    b += align16(sizeof(double) * kFrUsers * 3);        // user norm, reciprocal, screen limit
+    b += align16(sizeof(int64_t) * kFrUsers * 3);       // train cursor, end, item at the cursor
+    b += align16(sizeof(int32_t) * kFrUsers);           // list sizes
+    return b;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(256, 2)
+    eval_fr_kernel(const void *__restrict__ S, int s_f64, const float *__restrict__ T,
+                   int64_t t_rows, int K, const double *__restrict__ inorm_g,
+                   const double *__restrict__ rinorm_g, const int32_t *__restrict__ users,
+                   int64_t n_users, const int64_t *__restrict__ tr_off,
+                   const int32_t *__restrict__ tr_items, int64_t tr_num_users,
+                   const int64_t *__restrict__ te_off, const int32_t *__restrict__ te_items,
+                   int k, int cosine, const double *__restrict__ dcg_w,
+                   const double *__restrict__ idcg, int32_t *__restrict__ topk,
+                   double *__restrict__ recall, double *__restrict__ ndcg) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char *ptr = smem;
+    constexpr int LDU = kFrUsers + 4;
+    const int LDT = K + 4;
+    double *uT = reinterpret_cast<double *>(ptr);
+    ptr += align16(sizeof(double) * K * LDU);
+    double *tile = reinterpret_cast<double *>(ptr);
+    ptr += align16(sizeof(double) * kFrItems * LDT);
+    double *rin = reinterpret_cast<double *>(ptr);
+    ptr += align16(sizeof(double) * kFrItems);
+    double *ls = reinterpret_cast<double *>(ptr);
+    ptr += align16(sizeof(double) * kFrUsers * k);
+    int32_t *lid = reinterpret_cast<int32_t *>(ptr);
+    ptr += align16(sizeof(int32_t) * kFrUsers * k);
+    uint32_t *pmask = reinterpret_cast<uint32_t *>(ptr);
+    ptr += align16(sizeof(uint32_t) * kFrUsers * 2);
+    double *unv = reinterpret_cast<double *>(ptr);  // [0,64) norm, [64,128) 1/norm, [128,192) limit
+    ptr += align16(sizeof(double) * kFrUsers * 3);
+    int64_t *curv = reinterpret_cast<int64_t *>(ptr);  // cursor, end, item at the cursor
+    ptr += align16(sizeof(int64_t) * kFrUsers * 3);
+    int32_t *nl = reinterpret_cast<int32_t *>(ptr);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, tq = lane & 3;
+    const int64_t ubase = (int64_t)blockIdx.x * kFrUsers;
+    const int nub = (int)imin64(kFrUsers, n_users - ubase);
+    for (int i = tid; i < kFrUsers * K; i += 256) {
+        const int b = i / K, c = i % K;
+        double v = 0.0;
+        if (b < nub) {
+            const int64_t off = (int64_t)users[ubase + b] * K + c;
+            v = s_f64 ? reinterpret_cast<const double *>(S)[off]
+                      : (double)reinterpret_cast<const float *>(S)[off];
+        }
+        uT[c * LDU + b] = v;
+    }
+    __syncthreads();
+    // the limit a score (times the item's reciprocal norm) must reach to be
+    // looked at: -inf while the list is short (or the user's norm is zero:
+    // every cosine is then 0 and the merge decides), +inf for a padding slot
+    auto limit_of = [&](int b, double kth) -> double {
+        if (!cosine) return kth - 2e-9;
+        const double run = unv[kFrUsers + b];
+        return run > 0.0 ? (kth - 2e-9) * unv[b] : -INFINITY;
+    };
+    if (tid < kFrUsers) {
+        const int b = tid;
+        double a = 0.0;
+        for (int c = 0; c < K; ++c) a = fma(uT[c * LDU + b], uT[c * LDU + b], a);
+        const double n = sqrt(a);
+        unv[b] = n;
+        unv[kFrUsers + b] = n > 0.0 ? 1.0 / n : 0.0;
+        unv[2 * kFrUsers + b] = b < nub ? -INFINITY : INFINITY;
+        const int64_t u = b < nub ? users[ubase + b] : 0;
+        const bool has = b < nub && u < tr_num_users;
+        curv[b] = has ? tr_off[u] : 0;
+        curv[kFrUsers + b] = has ? tr_off[u + 1] : 0;
+        curv[2 * kFrUsers + b] =
+            (has && tr_off[u] < tr_off[u + 1]) ? (int64_t)tr_items[tr_off[u]] : INT64_MAX;
+        nl[b] = 0;
+    }
+    constexpr int PER = (kFrItems * KC / 4 + 255) / 256;  // float4 per thread
+    float4 pre[PER];
+    auto load_tile = [&](int64_t i0) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int f = tid + q * 256;
+            const int r = f / (KC / 4), c4 = f % (KC / 4);
+            const int64_t row = i0 + r;
+            pre[q] = (r < kFrItems && row < t_rows && c4 * 4 < K)
+                         ? *reinterpret_cast<const float4 *>(T + row * K + c4 * 4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto store_tile = [&]() {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int f = tid + q * 256;
+            const int r = f / (KC / 4), c = (f % (KC / 4)) * 4;
+            if (r < kFrItems && c < K) {
+                double *d = tile + r * LDT + c;  // (LDT even, c % 4 == 0: 16-byte aligned)
+                *reinterpret_cast<double2 *>(d) = make_double2(pre[q].x, pre[q].y);
+                *reinterpret_cast<double2 *>(d + 2) = make_double2(pre[q].z, pre[q].w);
+            }
+        }
+    };
+    load_tile(0);
+    for (int64_t i0 = 0; i0 < t_rows; i0 += kFrItems) {
+        __syncthreads();  // previous tile consumed (its products, masks and norms)
+        store_tile();
+        if (tid < kFrItems) {
+            const int64_t item = i0 + tid;
+            rin[tid] = item < t_rows ? (cosine ? rinorm_g[item] : 1.0) : 0.0;
+        }
+        if (lane < 16) pmask[warp * 16 + lane] = 0u;  // the warp's 8 users x 2 words
+        __syncthreads();
+        if (i0 + kFrItems < t_rows) load_tile(i0 + kFrItems);  // overlaps the scoring
+        // this tile's train positives of the warp's users -> 64-bit masks
+        for (int j = 0; j < 8; ++j) {
+            const int b = warp * 8 + j;
+            if (curv[2 * kFrUsers + b] >= i0 + kFrItems) continue;  // (warp-uniform)
+            int64_t c0 = curv[b];
+            const int64_t cend = curv[kFrUsers + b];
+            while (c0 < cend) {
+                const int64_t idx = c0 + lane;
+                const int64_t item = idx < cend ? (int64_t)tr_items[idx] : INT64_MAX;
+                const bool in_tile = item < i0 + kFrItems;
+                if (in_tile) {
+                    const int o = (int)(item - i0);
+                    atomicOr(&pmask[b * 2 + (o >> 5)], 1u << (o & 31));
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, in_tile);
+                c0 += __popc(m);
+                if (m != 0xffffffffu) break;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                curv[b] = c0;
+                curv[2 * kFrUsers + b] = c0 < cend ? (int64_t)tr_items[c0] : INT64_MAX;
+            }
+        }
+        __syncwarp();
+        // users 8w .. 8w+7 x the tile's 64 items: 8 m8n8k4 tiles per k-step.
+        // Thread (g, tq) ends with scores of user 8w + g for items
+        // 8 ni + 2 tq and 8 ni + 2 tq + 1.
+        double c0[8], c1[8];
+#pragma unroll
+        for (int ni = 0; ni < 8; ++ni) c0[ni] = c1[ni] = 0.0;
+        {
+            const double *ucol = uT + 8 * warp + g;
+            const double *trow = tile + (size_t)g * LDT + tq;
+            for (int k0 = 0; k0 < K; k0 += 4) {
+                const double av = ucol[(k0 + tq) * LDU];  // A[user g][k0 + tq]
+#pragma unroll
+                for (int ni = 0; ni < 8; ++ni) {
+                    const double bv = trow[(size_t)8 * ni * LDT + k0];  // B[k0 + tq][item 8 ni + g]
+                    asm volatile(
+                        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+                        "{%0, %1};"
+                        : "+d"(c0[ni]), "+d"(c1[ni])
+                        : "d"(av), "d"(bv));
+                }
+            }
+        }
+        // screen in registers
+        const double lim = unv[2 * kFrUsers + warp * 8 + g];
+        bool any = false;
+#pragma unroll
+        for (int ni = 0; ni < 8; ++ni) {
+            const double2 r2 = *reinterpret_cast<const double2 *>(rin + 8 * ni + 2 * tq);
+            any |= !(c0[ni] * r2.x < lim);
+            any |= !(c1[ni] * r2.y < lim);
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        // merge the survivors (any order: the insertion point compares ids)
+#pragma unroll
+        for (int ni = 0; ni < 8; ++ni) {
+            const double2 r2 = *reinterpret_cast<const double2 *>(rin + 8 * ni + 2 * tq);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double s = e ? c1[ni] : c0[ni];
+                unsigned mk = __ballot_sync(0xffffffffu, !(s * (e ? r2.y : r2.x) < lim));
+                while (mk) {
+                    const int src = __ffs(mk) - 1;
+                    mk &= mk - 1;
+                    const double sr = __shfl_sync(0xffffffffu, s, src);
+                    const int b = warp * 8 + (src >> 2);
+                    const int o = 8 * ni + 2 * (src & 3) + e;
+                    const int64_t item = i0 + o;
+                    if (b >= nub || item >= t_rows || ((pmask[b * 2 + (o >> 5)] >> (o & 31)) & 1u))
+                        continue;
+                    double cs = sr;
+                    if (cosine) {
+                        const double in = inorm_g[item], un = unv[b];
+                        cs = (un == 0.0 || in == 0.0) ? 0.0 : sr / (un * in);
+                    }
+                    const int32_t cid = (int32_t)item;
+                    double *lsb = ls + b * k;
+                    int32_t *lidb = lid + b * k;
+                    const int n = nl[b];
+                    if (n == k && !(cs > lsb[k - 1] || (cs == lsb[k - 1] && cid < lidb[k - 1])))
+                        continue;
+                    int posn = 0;
+                    for (int e0 = 0; e0 < n; e0 += 32) {
+                        const int q = e0 + lane;
+                        const bool better = q < n && (lsb[q] > cs || (lsb[q] == cs && lidb[q] < cid));
+                        posn += __popc(__ballot_sync(0xffffffffu, better));
+                    }
+                    const int newn = n < k ? n + 1 : k;
+                    for (int hi = newn - 1; hi > posn; hi -= 32) {
+                        const int dst = hi - lane;
+                        const bool mv = dst > posn;
+                        double vs = 0.0;
+                        int32_t vi = 0;
+                        if (mv) { vs = lsb[dst - 1]; vi = lidb[dst - 1]; }
+                        __syncwarp();
+                        if (mv) { lsb[dst] = vs; lidb[dst] = vi; }
+                        __syncwarp();
+                    }
+                    if (lane == 0 && posn < k) { lsb[posn] = cs; lidb[posn] = cid; }
+                    __syncwarp();
+                    if (lane == 0) {
+                        nl[b] = newn;
+                        if (newn == k) unv[2 * kFrUsers + b] = limit_of(b, lsb[k - 1]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    __syncwarp();
+    // hits / recall / NDCG: lane j of the warp takes user 8w + j, ranks in order
+    for (int j = 0; j < 8; ++j) {
+        const int b = warp * 8 + j;
+        if (b >= nub || !topk) continue;
+        const int n = nl[b];
+        for (int e = lane; e < k; e += 32) topk[(ubase + b) * k + e] = e < n ? lid[b * k + e] : -1;
+    }
+    if (lane < 8 && warp * 8 + lane < nub) {
+        const int b = warp * 8 + lane;
+        const int64_t ug = ubase + b;
+        const int64_t u = users[ug];
+        const int n = nl[b];
+        const int64_t tb = te_off[u], te = te_off[u + 1];
+        const int64_t nt = te - tb;
+        int hits = 0;
+        double dcg = 0.0;
+        for (int r = 0; r < n; ++r) {
+            const int32_t item = lid[b * k + r];
+            int64_t lo = tb, hi2 = te;
+            while (lo < hi2) {
+                const int64_t mid = (lo + hi2) >> 1;
+                if (te_items[mid] < item) lo = mid + 1; else hi2 = mid;
+            }
+            if (lo < te && te_items[lo] == item) {
+                ++hits;
+                dcg += dcg_w[r];
+            }
+        }
+        recall[ug] = (double)hits / (double)nt;
+        ndcg[ug] = dcg / idcg[(k < nt ? k : nt) - 1];
+    }
+}
+
 template <int UB>
 static cudaError_t launch_eval_ub(const void *S, int s_f64, const float *T, int64_t t_rows, int K,
                                   const int32_t *users, int64_t n_users, const int64_t *tr_off,
@@ -626,6 +912,30 @@ static cudaError_t launch_eval_ub(const void *S, int s_f64, const float *T, int6
     eval_kernel<UB><<<(unsigned)blocks, kEvalThreads, smem, st>>>(
         S, s_f64, T, t_rows, K, users, n_users, tr_off, tr_items, tr_nu, te_off, te_items, k, cosine, dw,
         idcg, topk, rec, nd);
+    return cudaGetLastError();
+}
+
+
+template <int KC>
+static cudaError_t launch_eval_fr(const void *S, int s_f64, const float *T, int64_t t_rows,
+                                  int K, const int32_t *users, int64_t n_users,
+                                  const int64_t *tr_off, const int32_t *tr_items, int64_t tr_nu,
+                                  const int64_t *te_off, const int32_t *te_items, int k,
+                                  int cosine, const double *dw, const double *idcg, int32_t *topk,
+                                  double *rec, double *nd, cudaStream_t st) {
+    const size_t smem = eval_fr_smem_bytes(K, k);
+    cudaError_t e = cudaFuncSetAttribute(eval_fr_kernel<KC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // item norms and reciprocals, once per call (evaluator.py:140-141)
+    double *norms = static_cast<double *>(stream_scratch(2, (size_t)t_rows * 16, st));
+    if (!norms) return cudaErrorMemoryAllocation;
+    item_norms_kernel<<<(unsigned)((t_rows + 255) / 256), 256, 0, st>>>(T, t_rows, K, norms,
+                                                                        norms + t_rows);
+    const int64_t blocks = (n_users + kFrUsers - 1) / kFrUsers;
+    eval_fr_kernel<KC><<<(unsigned)blocks, 256, smem, st>>>(
+        S, s_f64, T, t_rows, K, norms, norms + t_rows, users, n_users, tr_off, tr_items, tr_nu,
+        te_off, te_items, k, cosine, dw, idcg, topk, rec, nd);
     return cudaGetLastError();
 }
 
@@ -670,6 +980,17 @@ cudaError_t launch_eval(const void *S, int s_f64, const float *T, int64_t t_rows
                : launch_eval_rb<KCV, false>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, \
                                             tr_items, tr_num_users, te_offsets, te_items, k,    \
                                             cosine, dcg_w, idcg, topk, recall, ndcg, stream)
+    // the fragment-resident kernel (default; HEAT_EVAL_RB=1 selects the register-blocked one)
+    const bool fr_ok = mma && rb_ok && K % 4 == 0 && !getenv("HEAT_EVAL_RB") &&
+                       eval_fr_smem_bytes(K, k) <= cap;
+#define HEAT_EVAL_FR(KCV)                                                                    \
+    return launch_eval_fr<KCV>(S, s_f64, T, t_rows, K, users, n_users, tr_offsets, tr_items, \
+                               tr_num_users, te_offsets, te_items, k, cosine, dcg_w, idcg,   \
+                               topk, recall, ndcg, stream)
+    if (fr_ok && K <= 32) HEAT_EVAL_FR(32);
+    if (fr_ok && K <= 64) HEAT_EVAL_FR(64);
+    if (fr_ok && K <= 128) HEAT_EVAL_FR(128);
+#undef HEAT_EVAL_FR
     if (rb_ok && K <= 32) HEAT_EVAL_RB(32);
     if (rb_ok && K <= 64) HEAT_EVAL_RB(64);
     if (rb_ok && K <= 128) HEAT_EVAL_RB(128);
