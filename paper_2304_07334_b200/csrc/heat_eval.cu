@@ -8,12 +8,21 @@
 // 1/log2(r+1) / IDCG[min(k, n_test)] (evaluator.py:164-172; the two weight
 // tables come from the host in the reference's arithmetic).
 //
-// One CTA scores UB users against 64-item tiles of T staged in shared memory
-// (fp64 FMA dot products; scores are a pure function of (user, item), so
-// exact ties stay exact ties), then each warp merges its users' candidates
-// into a sorted top-k list kept in shared memory.  Items stream in increasing
-// id order, so a candidate that ties the current k-th score never displaces
-// it (the incumbent has the lower id) — exactly the reference's tie rule.
+// Three kernels, the fastest that fits is launched (launch_eval):
+//  * eval_fr_kernel (default, K % 4 == 0 and K <= 128): FP64 tensor path
+//    (mma.sync m8n8k4), a warp owns 8 users, scores screened in registers,
+//    lists merged by eval_finish_kernel when the catalog is cut into ranges;
+//  * eval_rb_kernel (HEAT_EVAL_RB=1): round 1's register-blocked kernel, the
+//    scores of a 32 x 128 tile through shared memory;
+//  * eval_kernel: the plain one below, for any K and k.
+// The plain kernel: one CTA scores UB users against 64-item tiles of T staged
+// in shared memory (fp64 FMA dot products; scores are a pure function of
+// (user, item), so exact ties stay exact ties), then each warp merges its
+// users' candidates into a sorted top-k list kept in shared memory.  Items
+// stream in increasing id order, so a candidate that ties the current k-th
+// score never displaces it (the incumbent has the lower id) — exactly the
+// reference's tie rule.
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
@@ -650,9 +659,9 @@ __global__ void __launch_bounds__(256, 2)
                    int64_t n_users, const int64_t *__restrict__ tr_off,
                    const int32_t *__restrict__ tr_items, int64_t tr_num_users,
                    const int64_t *__restrict__ te_off, const int32_t *__restrict__ te_items,
-                   int k, int cosine, const double *__restrict__ dcg_w,
-                   const double *__restrict__ idcg, int32_t *__restrict__ topk,
-                   double *__restrict__ recall, double *__restrict__ ndcg) {
+                   int k, int cosine, int nsplit, int64_t split_items,
+                   double *__restrict__ part_scores, int32_t *__restrict__ part_ids,
+                   int32_t *__restrict__ part_n) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned char *ptr = smem;
     constexpr int LDU = kFrUsers + 4;
@@ -677,7 +686,13 @@ __global__ void __launch_bounds__(256, 2)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tq = lane & 3;
-    const int64_t ubase = (int64_t)blockIdx.x * kFrUsers;
+    // CTA = (user block, item range): the catalog is cut into nsplit ranges
+    // of whole tiles so that the grid fills the SMs evenly (and small user
+    // sets still use every SM); eval_finish_kernel merges the ranges' lists
+    const int split = (int)(blockIdx.x % (unsigned)nsplit);
+    const int64_t ubase = (int64_t)(blockIdx.x / (unsigned)nsplit) * kFrUsers;
+    const int64_t i_begin = (int64_t)split * split_items;
+    const int64_t i_end = imin64(t_rows, i_begin + split_items);
     const int nub = (int)imin64(kFrUsers, n_users - ubase);
     for (int i = tid; i < kFrUsers * K; i += 256) {
         const int b = i / K, c = i % K;
@@ -708,10 +723,15 @@ __global__ void __launch_bounds__(256, 2)
         unv[2 * kFrUsers + b] = b < nub ? -INFINITY : INFINITY;
         const int64_t u = b < nub ? users[ubase + b] : 0;
         const bool has = b < nub && u < tr_num_users;
-        curv[b] = has ? tr_off[u] : 0;
-        curv[kFrUsers + b] = has ? tr_off[u + 1] : 0;
-        curv[2 * kFrUsers + b] =
-            (has && tr_off[u] < tr_off[u + 1]) ? (int64_t)tr_items[tr_off[u]] : INT64_MAX;
+        int64_t lo = has ? tr_off[u] : 0;
+        const int64_t cend = has ? tr_off[u + 1] : 0;
+        for (int64_t hi = cend; lo < hi;) {  // first train positive inside the item range
+            const int64_t mid = (lo + hi) >> 1;
+            if (tr_items[mid] < i_begin) lo = mid + 1; else hi = mid;
+        }
+        curv[b] = lo;
+        curv[kFrUsers + b] = cend;
+        curv[2 * kFrUsers + b] = lo < cend ? (int64_t)tr_items[lo] : INT64_MAX;
         nl[b] = 0;
     }
     constexpr int PER = (kFrItems * KC / 4 + 255) / 256;  // float4 per thread
@@ -739,8 +759,8 @@ __global__ void __launch_bounds__(256, 2)
             }
         }
     };
-    load_tile(0);
-    for (int64_t i0 = 0; i0 < t_rows; i0 += kFrItems) {
+    load_tile(i_begin);
+    for (int64_t i0 = i_begin; i0 < i_end; i0 += kFrItems) {
         __syncthreads();  // previous tile consumed (its products, masks and norms)
         store_tile();
         if (tid < kFrItems) {
@@ -749,7 +769,7 @@ __global__ void __launch_bounds__(256, 2)
         }
         if (lane < 16) pmask[warp * 16 + lane] = 0u;  // the warp's 8 users x 2 words
         __syncthreads();
-        if (i0 + kFrItems < t_rows) load_tile(i0 + kFrItems);  // overlaps the scoring
+        if (i0 + kFrItems < i_end) load_tile(i0 + kFrItems);  // overlaps the scoring
         // this tile's train positives of the warp's users -> 64-bit masks
         for (int j = 0; j < 8; ++j) {
             const int b = warp * 8 + j;
@@ -807,94 +827,165 @@ __global__ void __launch_bounds__(256, 2)
             any |= !(c1[ni] * r2.y < lim);
         }
         if (!__any_sync(0xffffffffu, any)) continue;
-        // merge the survivors (any order: the insertion point compares ids)
+        // merge the survivors (any order: the insertion point compares ids).
+        // ONE copy of the merge code, looped over the 16 score slots: sixteen
+        // unrolled copies thrashed the instruction cache (no_instructions was
+        // 18 % of the stall samples).
+        unsigned mine = 0;  // bit 2 ni + e: my score in slot (ni, e) passed the screen
 #pragma unroll
         for (int ni = 0; ni < 8; ++ni) {
             const double2 r2 = *reinterpret_cast<const double2 *>(rin + 8 * ni + 2 * tq);
+            mine |= (!(c0[ni] * r2.x < lim) ? 1u : 0u) << (2 * ni);
+            mine |= (!(c1[ni] * r2.y < lim) ? 1u : 0u) << (2 * ni + 1);
+        }
+        unsigned slots = __reduce_or_sync(0xffffffffu, mine);
+#pragma unroll 1
+        while (slots) {
+            const int slot = __ffs(slots) - 1;
+            slots &= slots - 1;
+            const int ni = slot >> 1, e = slot & 1;
+            double s = 0.0;  // my score of the slot (register select, no local memory)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double s = e ? c1[ni] : c0[ni];
-                unsigned mk = __ballot_sync(0xffffffffu, !(s * (e ? r2.y : r2.x) < lim));
-                while (mk) {
-                    const int src = __ffs(mk) - 1;
-                    mk &= mk - 1;
-                    const double sr = __shfl_sync(0xffffffffu, s, src);
-                    const int b = warp * 8 + (src >> 2);
-                    const int o = 8 * ni + 2 * (src & 3) + e;
-                    const int64_t item = i0 + o;
-                    if (b >= nub || item >= t_rows || ((pmask[b * 2 + (o >> 5)] >> (o & 31)) & 1u))
-                        continue;
-                    double cs = sr;
-                    if (cosine) {
-                        const double in = inorm_g[item], un = unv[b];
-                        cs = (un == 0.0 || in == 0.0) ? 0.0 : sr / (un * in);
+            for (int q = 0; q < 8; ++q) {
+                if (q == ni) s = e ? c1[q] : c0[q];
+            }
+            unsigned mk = __ballot_sync(0xffffffffu, (mine >> slot) & 1u);
+#pragma unroll 1
+            while (mk) {
+                const int src = __ffs(mk) - 1;
+                mk &= mk - 1;
+                const double sr = __shfl_sync(0xffffffffu, s, src);
+                const int b = warp * 8 + (src >> 2);
+                const int o = 8 * ni + 2 * (src & 3) + e;
+                const int64_t item = i0 + o;
+                if (b >= nub || item >= t_rows || ((pmask[b * 2 + (o >> 5)] >> (o & 31)) & 1u))
+                    continue;
+                double cs = sr;
+                if (cosine) {
+                    const double in = inorm_g[item], un = unv[b];
+                    cs = (un == 0.0 || in == 0.0) ? 0.0 : sr / (un * in);
+                }
+                const int32_t cid = (int32_t)item;
+                double *lsb = ls + b * k;
+                int32_t *lidb = lid + b * k;
+                const int n = nl[b];
+                const int newn = n < k ? n + 1 : k;
+                if (k <= 32) {
+                    // the list across the lanes: lane l holds entry l; the
+                    // entries behind the insertion point move up one lane
+                    const bool in_list = lane < n;
+                    const double own = in_list ? lsb[lane] : 0.0;
+                    const int32_t oid = in_list ? lidb[lane] : 0;
+                    const bool better = in_list && (own > cs || (own == cs && oid < cid));
+                    const int posn = __popc(__ballot_sync(0xffffffffu, better));
+                    const double up = __shfl_up_sync(0xffffffffu, own, 1);
+                    const int32_t upid = __shfl_up_sync(0xffffffffu, oid, 1);
+                    if (posn < k) {  // (a full list whose last entry beats the candidate: no change)
+                        if (lane == posn) { lsb[lane] = cs; lidb[lane] = cid; }
+                        else if (lane > posn && lane < newn) { lsb[lane] = up; lidb[lane] = upid; }
+                        if (lane == 0) nl[b] = newn;
                     }
-                    const int32_t cid = (int32_t)item;
-                    double *lsb = ls + b * k;
-                    int32_t *lidb = lid + b * k;
-                    const int n = nl[b];
-                    if (n == k && !(cs > lsb[k - 1] || (cs == lsb[k - 1] && cid < lidb[k - 1])))
-                        continue;
-                    int posn = 0;
-                    for (int e0 = 0; e0 < n; e0 += 32) {
-                        const int q = e0 + lane;
-                        const bool better = q < n && (lsb[q] > cs || (lsb[q] == cs && lidb[q] < cid));
-                        posn += __popc(__ballot_sync(0xffffffffu, better));
-                    }
-                    const int newn = n < k ? n + 1 : k;
-                    for (int hi = newn - 1; hi > posn; hi -= 32) {
-                        const int dst = hi - lane;
-                        const bool mv = dst > posn;
-                        double vs = 0.0;
-                        int32_t vi = 0;
-                        if (mv) { vs = lsb[dst - 1]; vi = lidb[dst - 1]; }
-                        __syncwarp();
-                        if (mv) { lsb[dst] = vs; lidb[dst] = vi; }
-                        __syncwarp();
-                    }
-                    if (lane == 0 && posn < k) { lsb[posn] = cs; lidb[posn] = cid; }
                     __syncwarp();
-                    if (lane == 0) {
-                        nl[b] = newn;
-                        if (newn == k) unv[2 * kFrUsers + b] = limit_of(b, lsb[k - 1]);
-                    }
+                    if (posn < k && newn == k && lane == 0)
+                        unv[2 * kFrUsers + b] = limit_of(b, lsb[k - 1]);
+                    __syncwarp();
+                    continue;
+                }
+                if (n == k && !(cs > lsb[k - 1] || (cs == lsb[k - 1] && cid < lidb[k - 1])))
+                    continue;
+                int posn = 0;
+                for (int e0 = 0; e0 < n; e0 += 32) {
+                    const int q = e0 + lane;
+                    const bool better = q < n && (lsb[q] > cs || (lsb[q] == cs && lidb[q] < cid));
+                    posn += __popc(__ballot_sync(0xffffffffu, better));
+                }
+                for (int hi = newn - 1; hi > posn; hi -= 32) {
+                    const int dst = hi - lane;
+                    const bool mv = dst > posn;
+                    double vs = 0.0;
+                    int32_t vi = 0;
+                    if (mv) { vs = lsb[dst - 1]; vi = lidb[dst - 1]; }
+                    __syncwarp();
+                    if (mv) { lsb[dst] = vs; lidb[dst] = vi; }
                     __syncwarp();
                 }
+                if (lane == 0 && posn < k) { lsb[posn] = cs; lidb[posn] = cid; }
+                __syncwarp();
+                if (lane == 0) {
+                    nl[b] = newn;
+                    if (newn == k) unv[2 * kFrUsers + b] = limit_of(b, lsb[k - 1]);
+                }
+                __syncwarp();
             }
         }
     }
     __syncwarp();
-    // hits / recall / NDCG: lane j of the warp takes user 8w + j, ranks in order
+    // this range's lists out (scores, ids, sizes), merged by eval_finish_kernel
     for (int j = 0; j < 8; ++j) {
         const int b = warp * 8 + j;
-        if (b >= nub || !topk) continue;
+        if (b >= nub) continue;
+        const int64_t slot = (int64_t)split * n_users + ubase + b;
         const int n = nl[b];
-        for (int e = lane; e < k; e += 32) topk[(ubase + b) * k + e] = e < n ? lid[b * k + e] : -1;
-    }
-    if (lane < 8 && warp * 8 + lane < nub) {
-        const int b = warp * 8 + lane;
-        const int64_t ug = ubase + b;
-        const int64_t u = users[ug];
-        const int n = nl[b];
-        const int64_t tb = te_off[u], te = te_off[u + 1];
-        const int64_t nt = te - tb;
-        int hits = 0;
-        double dcg = 0.0;
-        for (int r = 0; r < n; ++r) {
-            const int32_t item = lid[b * k + r];
-            int64_t lo = tb, hi2 = te;
-            while (lo < hi2) {
-                const int64_t mid = (lo + hi2) >> 1;
-                if (te_items[mid] < item) lo = mid + 1; else hi2 = mid;
-            }
-            if (lo < te && te_items[lo] == item) {
-                ++hits;
-                dcg += dcg_w[r];
-            }
+        for (int e = lane; e < n; e += 32) {
+            part_scores[slot * k + e] = ls[b * k + e];
+            part_ids[slot * k + e] = lid[b * k + e];
         }
-        recall[ug] = (double)hits / (double)nt;
-        ndcg[ug] = dcg / idcg[(k < nt ? k : nt) - 1];
+        if (lane == 0) part_n[slot] = n;
     }
+}
+
+// One thread per user: the k best of the item ranges' lists under (score
+// desc, id asc) — each list is sorted that way, so a k-step selection over
+// the list heads — then hits / recall / NDCG as evaluator.py:164-172.
+__global__ void eval_finish_kernel(const double *__restrict__ part_scores,
+                                   const int32_t *__restrict__ part_ids,
+                                   const int32_t *__restrict__ part_n, int nsplit,
+                                   const int32_t *__restrict__ users, int64_t n_users,
+                                   const int64_t *__restrict__ te_off,
+                                   const int32_t *__restrict__ te_items, int k,
+                                   const double *__restrict__ dcg_w,
+                                   const double *__restrict__ idcg, int32_t *__restrict__ topk,
+                                   double *__restrict__ recall, double *__restrict__ ndcg) {
+    const int64_t ug = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ug >= n_users) return;
+    constexpr int kMaxSplit = 32;
+    int head[kMaxSplit];
+    for (int q = 0; q < nsplit; ++q) head[q] = 0;
+    const int64_t u = users[ug];
+    const int64_t tb = te_off[u], te = te_off[u + 1];
+    const int64_t nt = te - tb;
+    int hits = 0;
+    double dcg = 0.0;
+    for (int r = 0; r < k; ++r) {
+        int best = -1;
+        double bs = 0.0;
+        int32_t bi = 0;
+        for (int q = 0; q < nsplit; ++q) {
+            const int64_t slot = (int64_t)q * n_users + ug;
+            if (head[q] >= part_n[slot]) continue;
+            const double cs = part_scores[slot * k + head[q]];
+            const int32_t ci = part_ids[slot * k + head[q]];
+            if (best < 0 || cs > bs || (cs == bs && ci < bi)) { best = q; bs = cs; bi = ci; }
+        }
+        if (best < 0) {
+            if (topk)
+                for (int e = r; e < k; ++e) topk[ug * k + e] = -1;
+            break;
+        }
+        ++head[best];
+        if (topk) topk[ug * k + r] = bi;
+        int64_t lo = tb, hi2 = te;
+        while (lo < hi2) {
+            const int64_t mid = (lo + hi2) >> 1;
+            if (te_items[mid] < bi) lo = mid + 1; else hi2 = mid;
+        }
+        if (lo < te && te_items[lo] == bi) {
+            ++hits;
+            dcg += dcg_w[r];
+        }
+    }
+    recall[ug] = (double)hits / (double)nt;
+    ndcg[ug] = dcg / idcg[(k < nt ? k : nt) - 1];
 }
 
 template <int UB>
@@ -932,10 +1023,34 @@ static cudaError_t launch_eval_fr(const void *S, int s_f64, const float *T, int6
     if (!norms) return cudaErrorMemoryAllocation;
     item_norms_kernel<<<(unsigned)((t_rows + 255) / 256), 256, 0, st>>>(T, t_rows, K, norms,
                                                                         norms + t_rows);
+    // Item ranges: one, unless the user blocks alone leave SMs idle (small
+    // user sets) — then as many ranges (at most 32, at least 16 tiles each) as
+    // fill two CTAs per SM.  Measured on c2 (434 blocks on 296 slots): 10.2 ms
+    // unsplit, 10.6 / 12.5 / 13.3 ms at 2 / 3 / 4 ranges — every range builds
+    // its own list from scratch (k ln(n / k) insertions each) and a lone CTA
+    // on an SM runs faster, so evening out the waves does not pay.
     const int64_t blocks = (n_users + kFrUsers - 1) / kFrUsers;
-    eval_fr_kernel<KC><<<(unsigned)blocks, 256, smem, st>>>(
+    const int64_t tiles = (t_rows + kFrItems - 1) / kFrItems;
+    const int64_t slots = 2 * (int64_t)sm_count();
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(32, tiles / 16),
+                                                             slots / blocks));
+    if (const char *f = getenv("HEAT_EVAL_SPLIT")) nsplit = std::min(std::max(atoi(f), 1), 32);
+    const int64_t split_items = ((tiles + nsplit - 1) / nsplit) * kFrItems;
+    const size_t per = (size_t)nsplit * (size_t)n_users;
+    unsigned char *part = static_cast<unsigned char *>(
+        stream_scratch(4, per * (size_t)k * 12 + per * 4 + 64, st));
+    if (!part) return cudaErrorMemoryAllocation;
+    double *part_scores = reinterpret_cast<double *>(part);
+    int32_t *part_ids = reinterpret_cast<int32_t *>(part + per * (size_t)k * 8);
+    int32_t *part_n = part_ids + per * (size_t)k;
+    eval_fr_kernel<KC><<<(unsigned)(blocks * nsplit), 256, smem, st>>>(
         S, s_f64, T, t_rows, K, norms, norms + t_rows, users, n_users, tr_off, tr_items, tr_nu,
-        te_off, te_items, k, cosine, dw, idcg, topk, rec, nd);
+        te_off, te_items, k, cosine, nsplit, split_items, part_scores, part_ids, part_n);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    eval_finish_kernel<<<(unsigned)((n_users + 127) / 128), 128, 0, st>>>(
+        part_scores, part_ids, part_n, nsplit, users, n_users, te_off, te_items, k, dw, idcg, topk,
+        rec, nd);
     return cudaGetLastError();
 }
 
