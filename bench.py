@@ -628,6 +628,13 @@ def main():
             "bytes_per_pair": "4K(N+2)+8 read + 4K(2+A_p) written (SURVEY.md §8(d))",
             "table_bytes": table_bytes,
             "active_negatives_per_pair": act_total / args.steps / npairs})
+        if clk.get("sm_mhz"):
+            # the same rate per SM clock, at the median clock sampled DURING the
+            # timed region (the live ceiling probe is a short burst at the box's
+            # top clock; a long epoch may run under sw_power_cap): an SM's L2
+            # fill port moves 64 B per clock
+            n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            roofline["achieved_bytes_per_clk_per_sm"] = achieved * 1e9 / (n_sm * clk["sm_mhz"] * 1e6)
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
