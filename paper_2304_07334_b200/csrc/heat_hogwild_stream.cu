@@ -98,6 +98,37 @@ unsigned long long *stream_claim(cudaStream_t st) {
     return p;
 }
 
+__global__ void row_policy_kernel(uint64_t *out) { *out = policy_evict_last(); }
+
+// The evict-last descriptor createpolicy returns on this device (it is an
+// opaque 64-bit value; asked from the device once per process and device).
+uint64_t stream_row_policy() {
+    static std::mutex mu;
+    static std::map<int, uint64_t> made;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = made.find(dev);
+    if (it != made.end()) return it->second;
+    uint64_t v = 0, *d = nullptr;
+    // (its own stream; the runtime's captures are relaxed-mode and come after
+    // a plain first epoch, so this never runs inside one)
+    if (cudaMalloc(&d, sizeof(v)) == cudaSuccess) {
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+            row_policy_kernel<<<1, 1, 0, s>>>(d);
+            if (cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                v = 0;
+            cudaStreamDestroy(s);
+        }
+        cudaFree(d);
+    }
+    cudaGetLastError();
+    if (v) made[dev] = v;
+    return v;  // 0: no descriptor, the launchers decline
+}
+
 }  // namespace
 
 // sum_k a[k]*b[k] over K floats widened to binary64, one k at a time, never
@@ -604,7 +635,9 @@ __global__ void __launch_bounds__(32, MINB)
     const int64_t npairs = k_stop - k_start;
     const int N = a.N;
     const int niter = (N + 1 + 31) >> 5;  // 4 rounds of 8 rows per iteration
-    const uint64_t pol = policy_evict_last();
+    // (a launch parameter, not createpolicy's vector-register result: the
+    // loads take it from a uniform register without a move per load)
+    const uint64_t pol = a.l2_policy;
     // per-worker global area: written-row entries, rows past the snapshot
     unsigned char *mine_area = a.spill + (size_t)blockIdx.x * a.spill_stride;
     float *sp_rows = reinterpret_cast<float *>(mine_area);
@@ -1213,6 +1246,8 @@ static cudaError_t launch_stream_k(const HogwildArgs &a, cudaStream_t st, int *w
     if (nw < 1) return cudaSuccess;
     if (workers_out) *workers_out = (int)nw;
     HogwildArgs b = a;
+    b.l2_policy = stream_row_policy();
+    if (!b.l2_policy) return cudaErrorNotSupported;  // (another kernel family takes the launch)
     // spill area: a pair writes at most N+1 rows (all of them when l2 != 0)
     b.spill_cap = a.N + 1;
     b.spill_stride = ((int64_t)b.spill_cap * (K * sizeof(float) + sizeof(WriteEntry) + sizeof(int2)) + 255) &
@@ -1263,6 +1298,8 @@ static cudaError_t launch_persist_k(const HogwildArgs &a, const PersistRank *ctx
     e = cudaMemcpyAsync(ctx_dev, cx.data(), nctx * sizeof(PersistRank), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return e;
     HogwildArgs b = a;
+    b.l2_policy = stream_row_policy();
+    if (!b.l2_policy) return cudaErrorNotSupported;  // (another kernel family takes the launch)
     if (nctx == 1) {  // the rank's tables and pairs as kernel parameters
         b.S = ctx_host->S; b.T = ctx_host->T; b.users = ctx_host->users;
         b.items = ctx_host->items; b.pair_index = ctx_host->pidx; b.ctr = ctx_host->ctr;

@@ -59,6 +59,11 @@ struct HogwildArgs {
     unsigned char *spill = nullptr;
     int64_t spill_stride = 0;  // bytes per worker
     int spill_cap = 0;         // rows per worker
+    // register-streamed kernel: the L2 evict-last policy descriptor as a
+    // launch parameter (made once on the device, stream_row_policy()), so it
+    // lives in the constant bank / a uniform register instead of a vector
+    // register pair re-moved to the uniform file before every load
+    uint64_t l2_policy = 0;
 };
 
 // One rank of the persistent sharded epoch (heat_shard.cu drives it,
