@@ -394,9 +394,9 @@ def l2_probe(dev, table_bytes: int, T=None) -> dict:
 
 def shard_lag(persistent: bool) -> int:
     """The staleness bound heat_shard.cu runs with (HEAT_SHARD_LAG, else 3 for
-    the persistent epoch and 2 for stream-ordered steps)."""
+    both the persistent epoch and the stream-ordered steps)."""
     v = os.environ.get("HEAT_SHARD_LAG")
-    return min(max(int(v), 1), 7 if persistent else 3) if v else (3 if persistent else 2)
+    return min(max(int(v), 1), 7 if persistent else 3) if v else 3
 
 
 def main():

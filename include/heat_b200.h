@@ -198,7 +198,7 @@ int heat_apply_row_deltas_fixed(float *T, int64_t t_rows, int32_t dim, const int
  * which read every rank's log straight from its memory over NVLink (CUDA IPC
  * mappings; HEAT_SHARD_EXCHANGE=gather selects an NCCL all-gather of the logs
  * instead) and add them in order-free fixed point.  Kernel(s) waits for the
- * apply of step s - lag (lag 2; HEAT_SHARD_LAG 1..3).  No host wait inside
+ * apply of step s - lag (lag 3; HEAT_SHARD_LAG 1..3).  No host wait inside
  * the epoch; it returns once the epoch is done, with `stream` ordered after
  * it.  Every rank must pass the same nsteps; capacity is agreed (max). */
 typedef struct heat_shard heat_shard;

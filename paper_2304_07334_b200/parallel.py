@@ -497,7 +497,7 @@ class NativeShardTrainer(ShardedTrainer):
     counts (the cross-rank fence) and the fused gather+apply kernels, which
     read the peers' logs over NVLink through CUDA IPC mappings.  No Python and
     no host wait between steps; kernel(s) sees every applied step up to
-    s - lag (lag 2, ``HEAT_SHARD_LAG``)."""
+    s - lag (lag 3, ``HEAT_SHARD_LAG``)."""
 
     def __init__(self, model: DeviceModel, world: int, rank: int, group=None,
                  transport: str = "nccl"):
